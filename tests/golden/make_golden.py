@@ -1,0 +1,199 @@
+"""Generate the committed golden fixtures from the REAL reference.
+
+Run in the build container only (needs /root/reference, which never
+exists on the GPU box):
+
+    python tests/golden/make_golden.py
+
+The reference is copied to /tmp first so numba's on-disk cache never
+writes into the read-only reference tree.  Every fixture
+records the reference call that produced it.  The fixtures are the pins
+for `oracle/` (tests/test_oracle.py) and the targets of the GPU parity
+tests (tests/test_gpu_parity.py).
+"""
+import json
+import os
+import shutil
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+REF_SRC = "/root/reference/pkg/src"
+TMP_REF = "/tmp/ddschur_ref_copy"
+
+
+def import_reference():
+    if not os.path.isdir(TMP_REF):
+        shutil.copytree(REF_SRC, TMP_REF)
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_golden")
+    sys.path.insert(0, TMP_REF)
+    sys.path.insert(0, REPO)
+    import ddschur  # noqa: F401
+    return ddschur
+
+
+def random_upper(rng, n, diag_sep=1.0, scale=1.0):
+    t = scale * (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    t = np.triu(t)
+    spread = np.cumsum(diag_sep + rng.uniform(0.0, 1.0, size=n))
+    phases = np.exp(1j * rng.uniform(0.0, 2 * np.pi, size=n))
+    t[np.arange(n), np.arange(n)] = spread * phases
+    return t
+
+
+def gen_trisolve(ref):
+    """solve_block on seeded (T, E); clip off / on; n_min 2 and 4."""
+    from ddschur.trisolve import TriEqProblem, solve_block
+    out = {}
+    cases = []
+    k = 0
+    for n in (2, 3, 4, 5, 7, 8, 13, 16, 31, 32, 33, 64, 100):
+        for clip in (None, 0.05):
+            for n_min in (2, 4):
+                rng = np.random.Generator(np.random.Philox(1000 + k))
+                t = random_upper(rng, n)
+                e = np.tril(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)), -1)
+                e *= 0.1
+                sol = solve_block(TriEqProblem(t=t, e=e, clip_threshold=clip), n_min=n_min)
+                out["t_%d" % k] = t
+                out["e_%d" % k] = e
+                out["l_%d" % k] = sol.l
+                cases.append(dict(k=k, n=n, clip=clip, n_min=n_min, clipped=int(sol.clipped_count)))
+                k += 1
+    np.savez_compressed(os.path.join(HERE, "trisolve_ref.npz"), **out)
+    with open(os.path.join(HERE, "trisolve_ref.json"), "w") as f:
+        json.dump(dict(source="ddschur.trisolve.solve_block (trisolve.py:243-262)", cases=cases), f, indent=1)
+
+
+def gen_ddgemm(ref):
+    """matmul_hp (numba gemm_hp, panel 32) on seeded normalised dd inputs."""
+    from ddschur.ddmatrix import DDMatrix
+    from ddschur.matmul import matmul_hp
+    out = {}
+    meta = []
+    for k, (m, kk, n) in enumerate(((5, 7, 3), (16, 16, 16), (33, 70, 20), (64, 64, 64))):
+        rng = np.random.Generator(np.random.Philox(2000 + k))
+
+        def dd(shape):
+            hi = rng.standard_normal(shape) + 0j + 1j * rng.standard_normal(shape)
+            lo = (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) * 2.0 ** -60
+            rh, rl = hi.real + lo.real, None
+            # normalise each (hi, lo) pair with an exact two_sum
+            def norm(h, l_):
+                s = h + l_
+                bb = s - h
+                e = (h - (s - bb)) + (l_ - bb)
+                return s, e
+            rh, rl = norm(hi.real, lo.real)
+            ih, il = norm(hi.imag, lo.imag)
+            return DDMatrix(rh, rl, ih, il)
+        a = dd((m, kk))
+        b = dd((kk, n))
+        c = matmul_hp(a, b)
+        for name, mat in (("a", a), ("b", b), ("c", c)):
+            for cell, arr in zip(("rh", "rl", "ih", "il"), mat.cells()):
+                out["%s%s_%d" % (name, cell, k)] = np.ascontiguousarray(arr)
+        meta.append(dict(k=k, m=m, k_dim=kk, n=n))
+    np.savez_compressed(os.path.join(HERE, "ddgemm_ref.npz"), **out)
+    with open(os.path.join(HERE, "ddgemm_ref.json"), "w") as f:
+        json.dump(dict(source="ddschur.matmul.matmul_hp (numba gemm_hp, panel 32)", cases=meta), f, indent=1)
+
+
+def make_instance(ref, rng, n, strict=0.5):
+    """A = U T U^H with separated eigenvalues, as in test_refine.py's
+    construction (diag spacing >= 0.7); candidate = U * cubic exp slice."""
+    from ddschur.ddmatrix import DDMatrix
+    from ddschur.matmul import matmul_hp
+    from ddschur.orthogonal import qr_retract
+    t = np.triu(strict * (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))), 1)
+    diag = np.arange(n) + 0.7 * rng.random(n) + 1j * rng.uniform(-1.0, 1.0, n)
+    t = t + np.diag(diag)
+    m = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    u = qr_retract(DDMatrix.from_lp(m))
+    a = matmul_hp(matmul_hp(u, DDMatrix.from_lp(t)), u, trans_b=True)
+    return a, u
+
+
+def gen_refine_dd(ref):
+    """refine_template in the reference's native dd mode on small seeded
+    instances: A = U T U^H, Q̂ = U * (I + K + K^2/2 + K^3/6), ||K|| = eps."""
+    from ddschur.ddmatrix import DDMatrix
+    from ddschur.matmul import matmul_hp
+    from ddschur.refine import RefineConfig, refine_template, verify_pair
+    out = {}
+    cases = []
+    for k, (n, eps) in enumerate(((8, 1e-4), (16, 1e-5), (32, 1e-6), (48, 1e-6))):
+        rng = np.random.Generator(np.random.Philox(3000 + k))
+        a, u = make_instance(ref, rng, n)
+        x = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+        kk = x - x.conj().T
+        kk *= eps / np.linalg.norm(kk)
+        poly = np.eye(n) + kk + kk @ kk / 2.0 + kk @ kk @ kk / 6.0
+        qhat = matmul_hp(u, DDMatrix.from_lp(poly))
+        pair, rep = refine_template(a, qhat, RefineConfig())
+        v = verify_pair(a, pair)
+        for name, mat in (("a", a), ("qhat", qhat), ("q", pair.q), ("t", pair.t)):
+            for cell, arr in zip(("rh", "rl", "ih", "il"), mat.cells()):
+                out["%s%s_%d" % (name, cell, k)] = np.ascontiguousarray(arr)
+        cases.append(dict(k=k, n=n, eps=eps, iterations=rep.iterations, status=rep.status.value,
+                          residual_history=[list(map(float, r)) for r in rep.residual_history],
+                          hp_matmul_count=rep.hp_matmul_count, clipped_total=rep.clipped_total,
+                          skip_fired=bool(rep.skip_fired), verify=list(map(float, v))))
+    np.savez_compressed(os.path.join(HERE, "refine_dd_ref.npz"), **out)
+    with open(os.path.join(HERE, "refine_dd_ref.json"), "w") as f:
+        json.dump(dict(source="ddschur.refine.refine_template (refine.py:357-380), default RefineConfig",
+                       cases=cases), f, indent=1)
+
+
+def gen_configs(ref):
+    """BASELINE configs the reference can run here:
+    config 1 (n=256) through the reference as-is (dd hp, binary64 lp) with
+    the FP64 stop rule re-expressed as tol_factor = 10 * 2^53 / n,
+    max_iters = 10 (option 1); config 4 literal at n = 64 / 128 (dd mode,
+    default stop) and its well-conditioned variant (strict part / sqrt(n))
+    at n = 128."""
+    from ddschur.refine import RefineConfig, refine_template
+    from paper_2203_10879_b200 import inputs
+    out = {}
+    cases = []
+    runs = []
+    a1, q1 = inputs.config_inputs(1, 256)
+    runs.append(("config1_n256", a1, q1, RefineConfig(tol_factor=10 * 2.0 ** 53 / 256, max_iters=10),
+                 "option1: reference dd, tol_factor=10*2^53/n, max_iters=10"))
+    for n, scale, tag in ((64, 1.0, "config4_n64"), (128, 1.0, "config4_n128"),
+                          (128, None, "config4wc_n128")):
+        s = 1.0 / np.sqrt(n) if scale is None else scale
+        a = inputs.config4_matrix(n, 0, strict_scale=s)
+        q = inputs.schur_vectors(a, np.complex128)
+        runs.append((tag, a, q, RefineConfig(max_iters=10), "dd mode, default tol_factor=10, max_iters=10"))
+    for tag, a, q, cfg, how in runs:
+        t0 = time.time()
+        try:
+            pair, rep = refine_template(a, q, cfg)
+            res = dict(iterations=rep.iterations, status=rep.status.value,
+                       residual_history=[list(map(float, r)) for r in rep.residual_history],
+                       hp_matmul_count=rep.hp_matmul_count, skip_fired=bool(rep.skip_fired),
+                       detail=rep.detail)
+        except Exception as exc:  # SeparationError etc. are results too
+            res = dict(exception=type(exc).__name__, message=str(exc))
+        res.update(tag=tag, n=int(a.shape[0]), how=how, seconds=time.time() - t0,
+                   norm_a=float(np.linalg.norm(a)))
+        out["qhat_" + tag] = q
+        cases.append(res)
+        print(tag, res.get("status"), res.get("iterations"), "%.1fs" % res["seconds"], flush=True)
+    np.savez_compressed(os.path.join(HERE, "configs_ref.npz"), **out)
+    with open(os.path.join(HERE, "configs_ref.json"), "w") as f:
+        json.dump(dict(source="ddschur.refine.refine_template on BASELINE-config inputs", cases=cases), f,
+                  indent=1)
+
+
+if __name__ == "__main__":
+    ref = import_reference()
+    which = sys.argv[1:] or ["trisolve", "ddgemm", "refine_dd", "configs"]
+    for w in which:
+        t0 = time.time()
+        globals()["gen_" + w](ref)
+        print("generated", w, "%.1fs" % (time.time() - t0), flush=True)

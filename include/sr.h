@@ -1,0 +1,120 @@
+/*
+ * libsr — B200-native Schur-refinement kernels, C ABI.
+ *
+ * The drop-in boundary for the hot path of the reference package `ddschur`
+ * (/root/reference/pkg/src/ddschur): `refine_template` and the operators it
+ * calls.  The reference's "FFI" is Python calling its numba kernels with
+ * caller-allocated output planes and no error path
+ * (matmul.py:71-77 -> _numba_kernels.gemm_hp / gemm_lp).  Every entry below
+ * replaces one such call site (cited per entry).  Conventions:
+ *   - plain device pointers, sizes and leading dimensions (in elements);
+ *     row-major storage, element (i, j) at i*ld + j;
+ *   - hp complex matrices are planar (separate re / im float64 planes),
+ *     lp complex matrices interleaved (complex64 = 8-byte float2 pairs,
+ *     complex128 = 16-byte double2 pairs);
+ *   - the caller (PyTorch on the Python side) owns every buffer; the library
+ *     allocates nothing per call; workspaces are caller-provided;
+ *   - all work is stream-ordered on `stream` (a cudaStream_t); results that
+ *     are scalars (norms, flags, counts) are written to device memory;
+ *   - every entry returns an int status: SR_OK or an SR_E* code; the message
+ *     of the last failure is available from sr_last_error().
+ * No entry has a CPU fallback: without a CUDA device they return SR_ECUDA.
+ */
+#ifndef SR_H_
+#define SR_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (Python maps them onto the reference's exception classes:
+   ValueError, SeparationError, NonFiniteError — trisolve.py:50-55) */
+#define SR_OK 0
+#define SR_EINVAL 1
+#define SR_ESEPARATION 2
+#define SR_ENONFINITE 3
+#define SR_ECUDA 4
+
+/* device flag bits written by the solver / norm kernels */
+#define SR_FLAG_SEPARATION 1
+#define SR_FLAG_NONFINITE 2
+
+/* op(A) selector: A or its conjugate transpose (matmul.py:64, trans_a) */
+#define SR_OP_N 0
+#define SR_OP_C 1
+
+#define SR_TRISOLVE_MAX_CTAS 1184 /* 8 x 148 SMs: cap on tiles x splits per level */
+
+int sr_version(void);
+const char* sr_last_error(void);
+
+/* hp product in FP64 mode: C = alpha * op(A) * B, then C_ii += diag_shift.
+   Replaces matmul_hp (matmul.py:52-81) -> gemm_hp (_numba_kernels.py:18-46).
+   b_im == NULL means B is real (config 3's real A in Q^H A).  lda/ldb/ldc
+   even and planes 16-byte aligned. */
+int sr_zgemm_f64(int op_a, int m, int n, int k, double alpha, double diag_shift, const double* a_re,
+                 const double* a_im, long long lda, const double* b_re, const double* b_im, long long ldb,
+                 double* c_re, double* c_im, long long ldc, void* stream);
+
+/* lp product in FP64 mode (complex64): C = op(A) * B.
+   Replaces matmul_lp (matmul.py:84-110) -> gemm_lp (_numba_kernels.py:49-69). */
+int sr_cgemm_c64(int op_a, int m, int n, int k, const void* a, long long lda, const void* b, long long ldb,
+                 void* c, long long ldc, void* stream);
+
+/* Split T^ into lp T (upper incl. diagonal) and lp E (strictly lower), both
+   complex64, and ||E||_F of the hp values into *d_norm_e (FP64).
+   Replaces stril_extract (ddmatrix.py:190-209) + frobenius_norm (216-251)
+   + the .to_lp() downcasts at refine.py:263-264,284. */
+int sr_split_lp_c64(int n, const double* that_re, const double* that_im, long long ldt, void* t_lp, void* e_lp,
+                    long long ld_lp, double* d_norm_e, void* ws, size_t ws_bytes, void* stream);
+
+/* ||M||_F of a planar FP64 matrix (frobenius_norm, ddmatrix.py:229-251):
+   fixed-shape two-level reduction, deterministic for a given n. */
+int sr_fro_norm_f64(int m, int n, const double* re, const double* im, long long ld, double* d_out, void* ws,
+                    size_t ws_bytes, void* stream);
+
+/* complex64 copy of a planar FP64 matrix (DDMatrix.to_lp / y.to_lp(),
+   orthogonal.py:187). */
+int sr_downcast_c64(int m, int n, const double* re, const double* im, long long ld, void* out, long long ld_out,
+                    void* stream);
+
+/* lp solve of stril(T L - L T) = -E (solve_block, trisolve.py:243-262).
+   clip <= 0 disables clipping; *d_clipped accumulates the clip count;
+   *d_flags |= SR_FLAG_SEPARATION on an exactly repeated diagonal. */
+size_t sr_trisolve_workspace_bytes(int n, int lp_is_c64);
+int sr_trisolve_c64(int n, const void* t, const void* e, long long ld, void* l, float clip,
+                    unsigned long long* d_clipped, int* d_flags, void* ws, size_t ws_bytes, void* stream);
+int sr_trisolve_c128(int n, const void* t, const void* e, long long ld, void* l, double clip,
+                     unsigned long long* d_clipped, int* d_flags, void* ws, size_t ws_bytes, void* stream);
+
+/* W = L - L^H (complex64), ||W||_F into *d_norm_w, SR_FLAG_NONFINITE into
+   *d_flags when L holds a non-finite entry (refine.py:296-297 and
+   _check_finite, trisolve.py:116-118). */
+int sr_skew_c64(int n, const void* l, long long ld, void* w, double* d_norm_w, int* d_flags, void* ws,
+                size_t ws_bytes, void* stream);
+
+/* Sigma of the merged Newton-Schulz update (merged_update,
+   orthogonal.py:191-201), planar FP64, summed left to right:
+   S = ((((2I + 2W) - Y) - YW) + W^2) + W^3 [+ W^2 Y + W^2 Y W].
+   w, yw, w2, w3 (and optional w2y, w2yw, NULL to skip) are complex64. */
+int sr_sigma_merged_f64(int n, const void* w, const double* y_re, const double* y_im, long long ldy,
+                        const void* yw, const void* w2, const void* w3, const void* w2y, const void* w2yw,
+                        long long ld_lp, double* s_re, double* s_im, long long lds, void* stream);
+
+/* Sigma of the entry Newton-Schulz step: S = 3I - G (orthogonal.py:167-168). */
+int sr_sigma_ns_f64(int n, const double* g_re, const double* g_im, long long ldg, double* s_re, double* s_im,
+                    long long lds, void* stream);
+
+/* Zero the strictly lower triangle in place (upper part of the last T^,
+   refine.py:324). */
+int sr_triu_inplace_f64(int n, double* re, double* im, long long ld, void* stream);
+
+/* bytes of reduction workspace the norm kernels need */
+size_t sr_reduce_workspace_bytes(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SR_H_ */

@@ -1,0 +1,26 @@
+"""B200-native Schur refinement (arXiv 2203.10879): a drop-in for the
+reference package's `refine_template` hot path.  Public names follow the
+reference's `ddschur/__init__.py`."""
+from .errors import NonFiniteError, NormTooLarge, NotSymmetric, SeparationError
+from .matmul import counters, matmul_hp, matmul_lp, reset_counters
+from .matrix import ZPlanar
+from .refine import (
+    U_FP64,
+    U_HP,
+    OrthoStrategy,
+    RefineConfig,
+    RefineReport,
+    RefineStatus,
+    SchurPair,
+    refine_template,
+    verify_pair,
+)
+from .trisolve import TriEqProblem, TriEqSolution, solve_block
+
+__version__ = "0.1.0"
+__all__ = [
+    "NonFiniteError", "NormTooLarge", "NotSymmetric", "SeparationError", "counters", "matmul_hp",
+    "matmul_lp", "reset_counters", "ZPlanar", "U_FP64", "U_HP", "OrthoStrategy", "RefineConfig",
+    "RefineReport", "RefineStatus", "SchurPair", "refine_template", "verify_pair", "TriEqProblem",
+    "TriEqSolution", "solve_block",
+]

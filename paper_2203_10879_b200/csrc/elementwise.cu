@@ -1,0 +1,259 @@
+// HBM-bound passes of the refinement loop: split + downcast + norms, Sigma
+// assembly, skew correction, downcasts.  Every kernel is one coalesced pass
+// (row-major, consecutive threads on consecutive columns) with grid-stride
+// loops sized to a multiple of the 148 SMs.  Norms use a fixed two-level
+// reduction (per-block partials in a fixed slot, then one block sums the
+// slots in index order), so a value is bit-reproducible for a given n.
+#include "sr_common.cuh"
+
+namespace {
+
+constexpr int RT = 256;                // threads per block
+constexpr int RBLOCKS = 148 * 4;       // reduction grid (fixed: deterministic)
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double warp_part[RT / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) warp_part[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < RT / 32; ++i) s += warp_part[i];
+  return s;  // valid on thread 0
+}
+
+// Last block to finish reduces the partials in slot order and writes sqrt.
+__device__ __forceinline__ void finish_norm(double mine, double* partials, unsigned int* counter, double* out) {
+  __shared__ bool last;
+  double s = block_sum(mine);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = s;
+    __threadfence();
+    unsigned int prev = atomicAdd(counter, 1u);
+    last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += RT) v += partials[i];
+  double tot = block_sum(v);
+  if (threadIdx.x == 0) {
+    *out = sqrt(tot);
+    *counter = 0u;
+  }
+}
+
+struct RedWs {
+  double* partials;
+  unsigned int* counter;
+};
+inline RedWs red_ws(void* ws) {
+  RedWs r;
+  r.counter = (unsigned int*)ws;
+  r.partials = (double*)((char*)ws + 256);
+  return r;
+}
+
+__global__ void split_lp_kernel(int n, const double* __restrict__ tr, const double* __restrict__ ti, long long ldt,
+                                float2* __restrict__ t_lp, float2* __restrict__ e_lp, long long ld_lp,
+                                double* partials, unsigned int* counter, double* out) {
+  double acc = 0.0;
+  const long long total = (long long)n * n;
+  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
+    int i = (int)(idx / n), j = (int)(idx % n);
+    double re = tr[(size_t)i * ldt + j], im = ti[(size_t)i * ldt + j];
+    float2 v = make_float2((float)re, (float)im);
+    float2 z = make_float2(0.f, 0.f);
+    if (i > j) {
+      acc += re * re + im * im;
+      e_lp[(size_t)i * ld_lp + j] = v;
+      t_lp[(size_t)i * ld_lp + j] = z;
+    } else {
+      e_lp[(size_t)i * ld_lp + j] = z;
+      t_lp[(size_t)i * ld_lp + j] = v;
+    }
+  }
+  finish_norm(acc, partials, counter, out);
+}
+
+__global__ void fro_norm_kernel(int m, int n, const double* __restrict__ re, const double* __restrict__ im,
+                                long long ld, double* partials, unsigned int* counter, double* out) {
+  double acc = 0.0;
+  const long long total = (long long)m * n;
+  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
+    int i = (int)(idx / n), j = (int)(idx % n);
+    double a = re[(size_t)i * ld + j];
+    acc += a * a;
+    if (im) {
+      double b = im[(size_t)i * ld + j];
+      acc += b * b;
+    }
+  }
+  finish_norm(acc, partials, counter, out);
+}
+
+__global__ void downcast_kernel(int m, int n, const double* __restrict__ re, const double* __restrict__ im,
+                                long long ld, float2* __restrict__ out, long long ldo) {
+  const long long total = (long long)m * n;
+  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
+    int i = (int)(idx / n), j = (int)(idx % n);
+    out[(size_t)i * ldo + j] = make_float2((float)re[(size_t)i * ld + j], (float)im[(size_t)i * ld + j]);
+  }
+}
+
+__global__ void skew_kernel(int n, const float2* __restrict__ l, long long ld, float2* __restrict__ w, int* flags,
+                            double* partials, unsigned int* counter, double* out) {
+  double acc = 0.0;
+  bool bad = false;
+  const long long total = (long long)n * n;
+  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
+    int i = (int)(idx / n), j = (int)(idx % n);
+    float2 a = l[(size_t)i * ld + j], b = l[(size_t)j * ld + i];
+    // w = l - conj(l^T), in lp (complex64) like l - l.conj().T at refine.py:296
+    float2 v = make_float2(a.x - b.x, a.y + b.y);
+    w[(size_t)i * ld + j] = v;
+    if (!isfinite(a.x) || !isfinite(a.y)) bad = true;
+    acc += (double)v.x * v.x + (double)v.y * v.y;
+  }
+  if (bad) atomicOr(flags, SR_FLAG_NONFINITE);
+  finish_norm(acc, partials, counter, out);
+}
+
+__global__ void sigma_merged_kernel(int n, const float2* __restrict__ w, const double* __restrict__ yr,
+                                    const double* __restrict__ yi, long long ldy, const float2* __restrict__ yw,
+                                    const float2* __restrict__ w2, const float2* __restrict__ w3,
+                                    const float2* __restrict__ w2y, const float2* __restrict__ w2yw, long long ldl,
+                                    double* __restrict__ sr, double* __restrict__ si, long long lds) {
+  const long long total = (long long)n * n;
+  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
+    int i = (int)(idx / n), j = (int)(idx % n);
+    size_t o = (size_t)i * ldl + j;
+    float2 wv = w[o];
+    // ((((2I + 2W) - Y) - YW) + W^2) + W^3, left to right (orthogonal.py:191-195)
+    double re = (i == j ? 2.0 : 0.0) + 2.0 * (double)wv.x;
+    double im = 2.0 * (double)wv.y;
+    re = re - yr[(size_t)i * ldy + j];
+    im = im - yi[(size_t)i * ldy + j];
+    float2 a = yw[o], b = w2[o], c = w3[o];
+    re = re - (double)a.x;
+    im = im - (double)a.y;
+    re = re + (double)b.x;
+    im = im + (double)b.y;
+    re = re + (double)c.x;
+    im = im + (double)c.y;
+    if (w2y) {  // restore_full_sigma (orthogonal.py:196-200)
+      float2 d = w2y[o], e = w2yw[o];
+      re = re + (double)d.x;
+      im = im + (double)d.y;
+      re = re + (double)e.x;
+      im = im + (double)e.y;
+    }
+    sr[(size_t)i * lds + j] = re;
+    si[(size_t)i * lds + j] = im;
+  }
+}
+
+__global__ void sigma_ns_kernel(int n, const double* __restrict__ gr, const double* __restrict__ gi, long long ldg,
+                                double* __restrict__ sr, double* __restrict__ si, long long lds) {
+  const long long total = (long long)n * n;
+  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
+    int i = (int)(idx / n), j = (int)(idx % n);
+    sr[(size_t)i * lds + j] = (i == j ? 3.0 : 0.0) - gr[(size_t)i * ldg + j];
+    si[(size_t)i * lds + j] = -gi[(size_t)i * ldg + j];
+  }
+}
+
+__global__ void triu_kernel(int n, double* re, double* im, long long ld) {
+  const long long total = (long long)n * n;
+  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
+    int i = (int)(idx / n), j = (int)(idx % n);
+    if (i > j) {
+      re[(size_t)i * ld + j] = 0.0;
+      im[(size_t)i * ld + j] = 0.0;
+    }
+  }
+}
+
+inline int ew_grid(long long total) {
+  long long b = (total + RT - 1) / RT;
+  return (int)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
+}
+
+}  // namespace
+
+extern "C" size_t sr_reduce_workspace_bytes(void) { return 256 + sizeof(double) * RBLOCKS; }
+
+extern "C" int sr_split_lp_c64(int n, const double* that_re, const double* that_im, long long ldt, void* t_lp,
+                               void* e_lp, long long ld_lp, double* d_norm_e, void* ws, size_t ws_bytes,
+                               void* stream) {
+  if (n < 0 || !ws || ws_bytes < sr_reduce_workspace_bytes()) return SR_EINVAL;
+  RedWs r = red_ws(ws);
+  split_lp_kernel<<<RBLOCKS, RT, 0, (cudaStream_t)stream>>>(n, that_re, that_im, ldt, (float2*)t_lp,
+                                                             (float2*)e_lp, ld_lp, r.partials, r.counter,
+                                                             d_norm_e);
+  SR_CUDA_CHECK(cudaGetLastError());
+  return SR_OK;
+}
+
+extern "C" int sr_fro_norm_f64(int m, int n, const double* re, const double* im, long long ld, double* d_out,
+                               void* ws, size_t ws_bytes, void* stream) {
+  if (m < 0 || n < 0 || !ws || ws_bytes < sr_reduce_workspace_bytes()) return SR_EINVAL;
+  RedWs r = red_ws(ws);
+  fro_norm_kernel<<<RBLOCKS, RT, 0, (cudaStream_t)stream>>>(m, n, re, im, ld, r.partials, r.counter, d_out);
+  SR_CUDA_CHECK(cudaGetLastError());
+  return SR_OK;
+}
+
+extern "C" int sr_downcast_c64(int m, int n, const double* re, const double* im, long long ld, void* out,
+                               long long ld_out, void* stream) {
+  if (m < 0 || n < 0) return SR_EINVAL;
+  if ((long long)m * n == 0) return SR_OK;
+  downcast_kernel<<<ew_grid((long long)m * n), RT, 0, (cudaStream_t)stream>>>(m, n, re, im, ld, (float2*)out,
+                                                                              ld_out);
+  SR_CUDA_CHECK(cudaGetLastError());
+  return SR_OK;
+}
+
+extern "C" int sr_skew_c64(int n, const void* l, long long ld, void* w, double* d_norm_w, int* d_flags, void* ws,
+                           size_t ws_bytes, void* stream) {
+  if (n < 0 || !ws || ws_bytes < sr_reduce_workspace_bytes()) return SR_EINVAL;
+  RedWs r = red_ws(ws);
+  skew_kernel<<<RBLOCKS, RT, 0, (cudaStream_t)stream>>>(n, (const float2*)l, ld, (float2*)w, d_flags, r.partials,
+                                                         r.counter, d_norm_w);
+  SR_CUDA_CHECK(cudaGetLastError());
+  return SR_OK;
+}
+
+extern "C" int sr_sigma_merged_f64(int n, const void* w, const double* y_re, const double* y_im, long long ldy,
+                                   const void* yw, const void* w2, const void* w3, const void* w2y,
+                                   const void* w2yw, long long ld_lp, double* s_re, double* s_im, long long lds,
+                                   void* stream) {
+  if (n < 0 || (w2y == nullptr) != (w2yw == nullptr)) return SR_EINVAL;
+  if (n == 0) return SR_OK;
+  sigma_merged_kernel<<<ew_grid((long long)n * n), RT, 0, (cudaStream_t)stream>>>(
+      n, (const float2*)w, y_re, y_im, ldy, (const float2*)yw, (const float2*)w2, (const float2*)w3,
+      (const float2*)w2y, (const float2*)w2yw, ld_lp, s_re, s_im, lds);
+  SR_CUDA_CHECK(cudaGetLastError());
+  return SR_OK;
+}
+
+extern "C" int sr_sigma_ns_f64(int n, const double* g_re, const double* g_im, long long ldg, double* s_re,
+                               double* s_im, long long lds, void* stream) {
+  if (n < 0) return SR_EINVAL;
+  if (n == 0) return SR_OK;
+  sigma_ns_kernel<<<ew_grid((long long)n * n), RT, 0, (cudaStream_t)stream>>>(n, g_re, g_im, ldg, s_re, s_im, lds);
+  SR_CUDA_CHECK(cudaGetLastError());
+  return SR_OK;
+}
+
+extern "C" int sr_triu_inplace_f64(int n, double* re, double* im, long long ld, void* stream) {
+  if (n < 0) return SR_EINVAL;
+  if (n == 0) return SR_OK;
+  triu_kernel<<<ew_grid((long long)n * n), RT, 0, (cudaStream_t)stream>>>(n, re, im, ld);
+  SR_CUDA_CHECK(cudaGetLastError());
+  return SR_OK;
+}

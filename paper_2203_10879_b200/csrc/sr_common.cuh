@@ -1,0 +1,51 @@
+// Shared helpers for the sm_100a Schur-refinement kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sr.h"
+
+#define SR_CUDA_CHECK(expr)                                        \
+  do {                                                             \
+    cudaError_t _e = (expr);                                       \
+    if (_e != cudaSuccess) return sr_set_cuda_error(_e, #expr);    \
+  } while (0)
+
+int sr_set_cuda_error(cudaError_t e, const char* what);
+
+static inline int sr_ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+struct cf32 {
+  float x, y;
+};
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a / b with the reference's semantics (numpy complex division; Smith's scaling
+// keeps |b| near the overflow threshold finite).
+__device__ __forceinline__ float2 cdiv(float2 a, float2 b) {
+  float s = fabsf(b.x) + fabsf(b.y);
+  float ars = a.x / s, ais = a.y / s, brs = b.x / s, bis = b.y / s;
+  float d = brs * brs + bis * bis;
+  return make_float2((ars * brs + ais * bis) / d, (ais * brs - ars * bis) / d);
+}
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  double s = fabs(b.x) + fabs(b.y);
+  double ars = a.x / s, ais = a.y / s, brs = b.x / s, bis = b.y / s;
+  double d = brs * brs + bis * bis;
+  return make_double2((ars * brs + ais * bis) / d, (ais * brs - ars * bis) / d);
+}
+
+__device__ __forceinline__ void cp_async_16(void* smem, const void* gmem, int src_bytes) {
+  uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}

@@ -9,14 +9,15 @@ C-order (n, n) `standard_normal` block.
 
 Q̂ is LAPACK's complex Schur vector matrix (`scipy.linalg.schur`,
 cgees/zgees, LAPACK eigenvalue order).  It is computed once per
-(config, n, seed) and cached as `.npy` under `data/` (git-ignored; it
-travels with the repo snapshot) because cgees at n = 8192 takes minutes.
+(config, n, seed) and cached as `.npy` under $SR_DATA_DIR (default /tmp/sr_data, outside the
+repo: the n = 8192 matrix alone is 512 MiB) because cgees at n = 8192 takes
+minutes.  The cache only shortens setup; no timed region depends on it.
 """
 import os
 
 import numpy as np
 
-_DATA = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "data")
+_DATA = os.environ.get("SR_DATA_DIR", "/tmp/sr_data")
 
 
 def _rng(seed):
@@ -75,7 +76,7 @@ def schur_vectors(a, dtype=np.complex64):
 
 
 def cached_qhat(tag, a, dtype=np.complex64):
-    """schur_vectors(a) cached under data/<tag>.npy."""
+    """schur_vectors(a) cached under $SR_DATA_DIR/qhat_<tag>.npy."""
     os.makedirs(_DATA, exist_ok=True)
     path = os.path.join(_DATA, "qhat_%s.npy" % tag)
     if os.path.exists(path):

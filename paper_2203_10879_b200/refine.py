@@ -1,0 +1,386 @@
+"""Newton-like Schur refinement on the B200: the drop-in `refine_template`.
+
+Mirrors the reference driver and loop
+  RefineConfig / RefineReport / RefineStatus  /root/reference/pkg/src/ddschur/refine.py:39-102
+  refine_template                             refine.py:357-380
+  _run (the loop)                             refine.py:223-329
+  _finish / _coerce_hp                        refine.py:332-350
+  newton_schulz_step / merged_update          orthogonal.py:153-201
+with every matrix operation in libsr.so.  One extra config field,
+`precision`, selects the precision pair:
+  "fp64": hp = FP64 complex (DMMA GEMMs), lp = complex64 (the BASELINE
+          configs 1, 2, 3, 5; U = 2^-53 in the stopping bound and skip rule);
+  "dd":   hp = double-double, lp = binary64 — the reference's own pair.
+The host loop reads back two small scalar groups per iteration (the norms
+after T^/Y, then ||W|| + flags + clip count after the solve); everything
+else stays on the device.
+"""
+import dataclasses
+import enum
+import math
+import time
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import NonFiniteError, NormTooLarge, NotSymmetric, SeparationError  # noqa: F401
+from .matmul import _counters, matmul_hp, matmul_lp, spectral_norm_estimate
+from .matrix import ZPlanar, lp_empty
+from .trisolve import SolverWorkspace, solve_lp_device
+
+U_HP = 2.0 ** -106
+U_FP64 = 2.0 ** -53
+
+DIVERGENCE_STREAK = 3
+_CLIP_HINT = ("clipping is disabled; retrying with clip_threshold=1e-5 may "
+              "contain the blowup")
+
+
+class OrthoStrategy(enum.Enum):
+    QR_RETRACTION = "qr"
+    NEWTON_SCHULZ = "ns"
+
+
+class RefineStatus(enum.Enum):
+    CONVERGED = "Converged"
+    MAX_ITERS = "MaxIters"
+    DIVERGED = "Diverged"
+    NON_FINITE = "NonFinite"
+
+
+@dataclasses.dataclass
+class RefineConfig:
+    """refine.py:53-82, plus `precision` ("fp64" | "dd")."""
+
+    tol_factor: float = 10.0
+    max_iters: int = 20
+    n_min: int = 4
+    clip_threshold: float | None = None
+    ortho: OrthoStrategy = OrthoStrategy.NEWTON_SCHULZ
+    skip_final_ortho: bool = True
+    seed: int = 0
+    restore_full_sigma: bool = False
+    precision: str = "dd"
+
+    def __post_init__(self):
+        if not self.tol_factor > 0.0:
+            raise ValueError("tol_factor must be positive")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be at least 1")
+        if self.n_min < 2:
+            raise ValueError("n_min must be at least 2")
+        if self.clip_threshold is not None and not self.clip_threshold > 0.0:
+            raise ValueError("clip_threshold must be positive when set")
+        if not isinstance(self.ortho, OrthoStrategy):
+            raise ValueError("ortho must be an OrthoStrategy")
+        if self.precision not in ("fp64", "dd"):
+            raise ValueError("precision must be 'fp64' or 'dd'")
+
+
+@dataclasses.dataclass
+class RefineReport:
+    """refine.py:85-102."""
+
+    iterations: int
+    residual_history: list
+    hp_matmul_count: int
+    clipped_total: int
+    status: RefineStatus
+    wall_time: float
+    skip_fired: bool = False
+    detail: str = ""
+
+
+@dataclasses.dataclass
+class SchurPair:
+    """schur.py:29-49: q unitary, t upper triangular (device tensors)."""
+
+    q: object
+    t: object
+    ortho_residual: float
+    tri_residual: float | None = None
+
+
+class _Fp64Workspace:
+    """Every device buffer one FP64-mode refinement needs, allocated once."""
+
+    def __init__(self, n, device):
+        self.n = n
+        self.q = ZPlanar.empty(n, device=device)
+        self.q_next = ZPlanar.empty(n, device=device)
+        self.p = ZPlanar.empty(n, device=device)        # Q^H A
+        self.that = ZPlanar.empty(n, device=device)     # (Q^H A) Q
+        self.y = ZPlanar.empty(n, device=device)        # Q^H Q - I
+        self.sigma = ZPlanar.empty(n, device=device)
+        self.t_lp = lp_empty(n, device=device)
+        self.e_lp = lp_empty(n, device=device)
+        self.l_lp = lp_empty(n, device=device)
+        self.w_lp = lp_empty(n, device=device)
+        self.y_lp = lp_empty(n, device=device)
+        self.yw = lp_empty(n, device=device)
+        self.w2 = lp_empty(n, device=device)
+        self.w3 = lp_empty(n, device=device)
+        self.w2y = None
+        self.w2yw = None
+        self.scal = torch.zeros(8, dtype=torch.float64, device=device)  # norm_a, norm_e, norm_y, norm_w
+        red = _lib.load().sr_reduce_workspace_bytes()
+        self.red = [torch.zeros(red, dtype=torch.uint8, device=device) for _ in range(4)]
+        self.solver = SolverWorkspace(n, torch.complex64, device)
+
+    def ptr(self, i):
+        return self.scal.data_ptr() + 8 * i
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _coerce(x, device):
+    """_coerce_hp (refine.py:341-350): exact embed, square + finite checks."""
+    if isinstance(x, ZPlanar):
+        m = x
+    else:
+        if isinstance(x, np.ndarray):
+            if x.ndim != 2:
+                raise ValueError("expected a 2-d array")
+        m = ZPlanar.from_any(x, device=device)
+    if m.rows != m.cols:
+        raise ValueError("refinement needs a square matrix")
+    fin = torch.isfinite(m.re).all()
+    if m.im is not None:
+        fin = fin & torch.isfinite(m.im).all()
+    if not bool(fin):
+        raise ValueError("input matrix has non-finite entries")
+    return m
+
+
+def _newton_schulz_entry(qhat, ws):
+    """newton_schulz_step (orthogonal.py:153-169): guard ||Q^||_2 < sqrt(3)
+    by lp power iteration, G = Q^H Q (hp), S = 3I - G, Q = Q^ S / 2 (hp)."""
+    n = ws.n
+    _lib.call("sr_downcast_c64", n, n, qhat.re_ptr(), qhat.im_ptr(), qhat.ld, ws.y_lp.data_ptr(),
+              ws.y_lp.shape[1], _stream())
+    est = spectral_norm_estimate(ws.y_lp, n)
+    if not est < math.sqrt(3.0):
+        raise NormTooLarge("spectral norm estimate %.6f is not below sqrt(3)" % est)
+    g = matmul_hp(qhat, qhat, trans_a=True, out=ws.y)
+    _lib.call("sr_sigma_ns_f64", n, g.re_ptr(), g.im_ptr(), g.ld, ws.sigma.re_ptr(), ws.sigma.im_ptr(),
+              ws.sigma.ld, _stream())
+    matmul_hp(qhat, ws.sigma, alpha=0.5, out=ws.q)
+
+
+def _merged_update(ws, restore_full_sigma):
+    """merged_update (orthogonal.py:172-201): YW, W^2, W^3 in lp, Sigma in hp
+    left to right, Q_new = (Q Sigma) / 2 in hp."""
+    n = ws.n
+    _lib.call("sr_downcast_c64", n, n, ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld, ws.y_lp.data_ptr(),
+              ws.y_lp.shape[1], _stream())
+    matmul_lp(ws.y_lp, ws.w_lp, n, n, n, out=ws.yw)
+    matmul_lp(ws.w_lp, ws.w_lp, n, n, n, out=ws.w2)
+    matmul_lp(ws.w2, ws.w_lp, n, n, n, out=ws.w3)
+    w2y = w2yw = None
+    if restore_full_sigma:
+        if ws.w2y is None:
+            ws.w2y = lp_empty(n, device=ws.w_lp.device)
+            ws.w2yw = lp_empty(n, device=ws.w_lp.device)
+        matmul_lp(ws.w2, ws.y_lp, n, n, n, out=ws.w2y)
+        matmul_lp(ws.w2y, ws.w_lp, n, n, n, out=ws.w2yw)
+        w2y, w2yw = ws.w2y.data_ptr(), ws.w2yw.data_ptr()
+    _lib.call("sr_sigma_merged_f64", n, ws.w_lp.data_ptr(), ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld,
+              ws.yw.data_ptr(), ws.w2.data_ptr(), ws.w3.data_ptr(), w2y, w2yw, ws.w_lp.shape[1],
+              ws.sigma.re_ptr(), ws.sigma.im_ptr(), ws.sigma.ld, _stream())
+    matmul_hp(ws.q, ws.sigma, alpha=0.5, out=ws.q_next)
+    ws.q, ws.q_next = ws.q_next, ws.q
+
+
+
+def _phase_permutation(q):
+    """_phase_permutation (refine.py:172-189): perm with q[perm[j], j] the only
+    nonzero of column j and of its row, each of exactly unit modulus; else None.
+    O(n^2) scan on the device, O(n) exactness check on the host."""
+    nz = q.re != 0
+    if q.im is not None:
+        nz = nz | (q.im != 0)
+    if not (bool((nz.sum(dim=0) == 1).all()) and bool((nz.sum(dim=1) == 1).all())):
+        return None
+    perm = nz.to(torch.int8).argmax(dim=0)
+    cols = torch.arange(q.cols, device=perm.device)
+    zr = q.re[perm, cols].double().cpu().numpy()
+    zi = (q.im[perm, cols] if q.im is not None else torch.zeros_like(q.re[perm, cols])).cpu().numpy()
+    from fractions import Fraction
+    for x, y in zip(zr.tolist(), zi.tolist()):
+        if Fraction(x) ** 2 + Fraction(y) ** 2 != 1:
+            return None
+    return perm
+
+
+def _structural_triangle(a, q, perm):
+    """_permuted_part_is_zero + _exact_similarity_triangle (refine.py:192-220):
+    if A[perm][:, perm] is exactly upper triangular, T = conj(q_p) A_pp q_p
+    entrywise (no products); else None."""
+    sub_re = a.re[perm][:, perm]
+    nz = sub_re != 0
+    if a.im is not None:
+        nz = nz | (a.im[perm][:, perm] != 0)
+    if bool(torch.tril(nz, -1).any()):
+        return None
+    cols = torch.arange(q.cols, device=perm.device)
+    ph = torch.complex(q.re[perm, cols], q.im[perm, cols] if q.im is not None else torch.zeros_like(sub_re[0]))
+    sub = torch.complex(sub_re, a.im[perm][:, perm] if a.im is not None else torch.zeros_like(sub_re))
+    t = torch.triu(ph.conj()[:, None] * sub * ph[None, :])
+    return t
+
+
+def _run_fp64(a, qhat, cfg, ws):
+    """_run (refine.py:223-329) with hp = FP64, lp = complex64."""
+    n = a.rows
+    st = _stream()
+    hp0 = _counters["hp_calls"]
+    _newton_schulz_entry(qhat, ws)
+    _lib.call("sr_fro_norm_f64", n, n, a.re_ptr(), a.im_ptr(), a.ld, ws.ptr(0), ws.red[0].data_ptr(),
+              ws.red[0].numel(), st)
+    history = []
+    perm = _phase_permutation(ws.q)
+    if perm is not None:
+        t_exact = _structural_triangle(a, ws.q, perm)
+        if t_exact is not None:
+            # exactly unitary Q, exactly triangular Q^H A Q: zero iterations
+            # beyond the entry check (refine.py:239-252)
+            history.append((0.0, 0.0))
+            pair = SchurPair(q=ws.q.to_complex(), t=t_exact, ortho_residual=0.0, tri_residual=0.0)
+            report = RefineReport(iterations=0, residual_history=history,
+                                  hp_matmul_count=_counters["hp_calls"] - hp0, clipped_total=0,
+                                  status=RefineStatus.CONVERGED, wall_time=0.0)
+            return pair, report
+    clipped_total = 0
+    skip_fired = False
+    detail = ""
+    status = RefineStatus.MAX_ITERS
+    iterations = cfg.max_iters
+    streak = 0
+    tol = None
+    for it in range(1, cfg.max_iters + 1):
+        # T^ = (Q^H A) Q; split + lp downcast + ||E||; Y = Q^H Q - I; ||Y||
+        matmul_hp(ws.q, a, trans_a=True, out=ws.p)
+        matmul_hp(ws.p, ws.q, out=ws.that)
+        _lib.call("sr_split_lp_c64", n, ws.that.re_ptr(), ws.that.im_ptr(), ws.that.ld, ws.t_lp.data_ptr(),
+                  ws.e_lp.data_ptr(), ws.t_lp.shape[1], ws.ptr(1), ws.red[1].data_ptr(), ws.red[1].numel(), st)
+        matmul_hp(ws.q, ws.q, trans_a=True, diag_shift=-1.0, out=ws.y)
+        _lib.call("sr_fro_norm_f64", n, n, ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld, ws.ptr(2),
+                  ws.red[2].data_ptr(), ws.red[2].numel(), st)
+        s = ws.scal[:3].cpu()  # sync 1
+        norm_a, norm_e, norm_y = float(s[0]), float(s[1]), float(s[2])
+        if tol is None:
+            tol = cfg.tol_factor * n * U_FP64 * norm_a
+            # row 0: entry state measured in FP64 (see oracle/refine_fp64.py)
+            history.append((norm_e, norm_y))
+        history.append((norm_e, norm_y))
+        if not (math.isfinite(norm_e) and math.isfinite(norm_y)):
+            status, iterations = RefineStatus.NON_FINITE, it
+            detail = "iteration %d: residuals became non-finite" % it
+            if cfg.clip_threshold is None:
+                detail += "; " + _CLIP_HINT
+            break
+        converged = norm_e <= tol
+        # lp solve + W = L - L^H + ||W|| + finiteness
+        ws.solver.clipped.zero_()
+        ws.solver.flags.zero_()
+        solve_lp_device(ws.t_lp, ws.e_lp, ws.l_lp, n, cfg.clip_threshold, ws.solver, st)
+        _lib.call("sr_skew_c64", n, ws.l_lp.data_ptr(), ws.l_lp.shape[1], ws.w_lp.data_ptr(), ws.ptr(3),
+                  ws.solver.flags.data_ptr(), ws.red[3].data_ptr(), ws.red[3].numel(), st)
+        norm_w = float(ws.scal[3].cpu())  # sync 2
+        flags = int(ws.solver.flags.item())
+        nclip = int(ws.solver.clipped.item())
+        if flags & _lib.SR_FLAG_SEPARATION:
+            raise SeparationError("t has exactly repeated diagonal entries: diagonal separation is "
+                                  "exactly zero")
+        if flags & _lib.SR_FLAG_NONFINITE:
+            status, iterations = RefineStatus.NON_FINITE, it
+            detail = "iteration %d: solution contains non-finite entries" % it
+            if cfg.clip_threshold is None:
+                detail += "; " + _CLIP_HINT
+            break
+        clipped_total += nclip
+        skip = (converged and cfg.skip_final_ortho and norm_y <= 10.0 * n * U_FP64
+                and norm_w <= math.sqrt(U_FP64))
+        if not skip:
+            _merged_update(ws, cfg.restore_full_sigma)
+        if converged:
+            status, iterations, skip_fired = RefineStatus.CONVERGED, it, skip
+            break
+        if len(history) >= 2 and norm_e > history[-2][0]:
+            streak += 1
+        else:
+            streak = 0
+        if streak >= DIVERGENCE_STREAK:
+            status, iterations = RefineStatus.DIVERGED, it
+            break
+    _lib.call("sr_triu_inplace_f64", n, ws.that.re_ptr(), ws.that.im_ptr(), ws.that.ld, st)
+    last_e, last_y = history[-1]
+    pair = SchurPair(q=ws.q.to_complex(), t=ws.that.to_complex(), ortho_residual=last_y,
+                     tri_residual=last_e)
+    report = RefineReport(iterations=iterations, residual_history=history,
+                          hp_matmul_count=_counters["hp_calls"] - hp0, clipped_total=clipped_total,
+                          status=status, wall_time=0.0, skip_fired=skip_fired, detail=detail)
+    return pair, report
+
+
+_WS_CACHE = {}
+
+
+def _workspace(n, device):
+    key = (n, str(device))
+    ws = _WS_CACHE.get(key)
+    if ws is None:
+        _WS_CACHE.clear()
+        ws = _WS_CACHE[key] = _Fp64Workspace(n, device)
+    return ws
+
+
+def refine_template(a, qhat, cfg=None, device=None):
+    """Refine a user-supplied candidate Q toward a Schur pair of A
+    (refine.py:357-380).  a, qhat: numpy arrays, torch tensors (any device)
+    or ZPlanar device matrices; real A is kept real.  Returns
+    (SchurPair, RefineReport) with q, t as complex128 CUDA tensors."""
+    cfg = RefineConfig() if cfg is None else cfg
+    if cfg.ortho is not OrthoStrategy.NEWTON_SCHULZ:
+        raise NotImplementedError("QR retraction is not on the B200 path (no CPU fallback)")
+    if not torch.cuda.is_available():
+        raise RuntimeError("refine_template needs a CUDA device (no CPU fallback)")
+    device = torch.device("cuda") if device is None else torch.device(device)
+    t0 = time.perf_counter()
+    a = _coerce(a, device)
+    qhat = _coerce(qhat, device)
+    if a.shape != qhat.shape:
+        raise ValueError("matrix and candidate shapes differ")
+    if qhat.is_real:
+        qhat = ZPlanar.from_any(qhat.re, device=device, force_complex=True)
+    if cfg.precision == "dd":
+        from . import dd_refine
+        pair, report = dd_refine.run_dd(a, qhat, cfg, device)
+    else:
+        ws = _workspace(a.rows, device)
+        pair, report = _run_fp64(a, qhat, cfg, ws)
+    torch.cuda.current_stream().synchronize()
+    report.wall_time = time.perf_counter() - t0
+    return pair, report
+
+
+def verify_pair(a, pair, device=None):
+    """verify_pair (refine.py:456-476) in FP64 on the GPU:
+    (||Q^H Q - I||_F, ||stril(Q^H A Q)||_F, ||T - Q^H A Q||_F)."""
+    device = torch.device("cuda") if device is None else torch.device(device)
+    a = _coerce(a, device)
+    q = ZPlanar.from_any(pair.q, device=device, force_complex=True)
+    t = ZPlanar.from_any(pair.t, device=device, force_complex=True)
+    n = a.rows
+    g = matmul_hp(q, q, trans_a=True, diag_shift=-1.0)
+    that = matmul_hp(matmul_hp(q, a, trans_a=True), q)
+    gz = g.to_complex()
+    tz = that.to_complex()
+    ortho = float(torch.linalg.matrix_norm(gz))
+    tri = float(torch.linalg.matrix_norm(torch.tril(tz, -1)))
+    sim = float(torch.linalg.matrix_norm(t.to_complex() - tz))
+    del n
+    return ortho, tri, sim

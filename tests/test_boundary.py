@@ -1,0 +1,53 @@
+"""CPU-side checks of the drop-in boundary: libsr.so loads and exports every
+symbol include/sr.h declares; host-side API validation mirrors the
+reference (RefineConfig checks, refine.py:72-82)."""
+import os
+import re
+
+import pytest
+
+from paper_2203_10879_b200 import RefineConfig, _lib
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(REPO, "include", "sr.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(sr_\w+)\s*\(", src, re.M)))
+
+
+def test_header_and_binding_agree():
+    assert set(declared_symbols()) == set(_lib.SIGNATURES)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    assert lib.sr_version() >= 1
+    assert lib.sr_reduce_workspace_bytes() > 0
+    assert lib.sr_trisolve_workspace_bytes(8192, 1) > 0
+
+
+def test_invalid_arguments_are_rejected_without_a_gpu():
+    lib = _lib.load()
+    # negative sizes and odd leading dimensions are argument errors
+    assert lib.sr_zgemm_f64(0, -1, 4, 4, 1.0, 0.0, 16, 16, 4, 16, 16, 4, 16, 16, 4, None) == _lib.SR_EINVAL
+    assert lib.sr_zgemm_f64(0, 4, 4, 4, 1.0, 0.0, 16, 16, 3, 16, 16, 4, 16, 16, 4, None) == _lib.SR_EINVAL
+    assert lib.sr_cgemm_c64(1, 4, 4, 4, 16, 4, 16, 4, 16, 4, None) == _lib.SR_EINVAL
+    with pytest.raises(ValueError):
+        _lib.check(_lib.SR_EINVAL, "probe")
+
+
+def test_refine_config_validation():
+    with pytest.raises(ValueError):
+        RefineConfig(tol_factor=0.0)
+    with pytest.raises(ValueError):
+        RefineConfig(max_iters=0)
+    with pytest.raises(ValueError):
+        RefineConfig(n_min=1)
+    with pytest.raises(ValueError):
+        RefineConfig(clip_threshold=-1.0)
+    with pytest.raises(ValueError):
+        RefineConfig(precision="fp32")
+    assert RefineConfig().precision == "dd"

@@ -1,0 +1,50 @@
+"""Measurement noise of the FP64 products vs an exact (double-double) oracle:
+||stril((Q^H A) Q) - exact||_F / ||A||_F and ||(Q^H Q - I) - exact||_F in
+units of u64, for numpy (OpenBLAS) and the libsr DMMA kernel."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from oracle import clib  # noqa: E402
+from paper_2203_10879_b200 import ZPlanar, matmul_hp  # noqa: E402
+
+U = 2.0 ** -53
+
+
+def dd_planes(x):
+    z = np.zeros(x.shape)
+    return (np.ascontiguousarray(x.real), z, np.ascontiguousarray(x.imag), z.copy())
+
+
+def dd_gemm(a_planes, b_planes):
+    return clib.gemm_dd(a_planes, b_planes)
+
+
+def conj_t(p):
+    return tuple(np.ascontiguousarray(x.T) * (1 if i < 2 else -1) for i, x in enumerate(p))
+
+
+for n in [int(x) for x in sys.argv[1:]] or [256, 512]:
+    rng = np.random.default_rng(n)
+    a = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) * np.sqrt(0.5)
+    z = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    q, r = np.linalg.qr(z)
+    qp, ap = dd_planes(q), dd_planes(a)
+    p_ex = dd_gemm(conj_t(qp), ap)
+    t_ex = dd_gemm(p_ex, qp)
+    g_ex = dd_gemm(conj_t(qp), qp)
+    t_hi = (t_ex[0] + 1j * t_ex[2]) + (t_ex[1] + 1j * t_ex[3])
+    g_lo = (g_ex[0] - np.eye(n)) + g_ex[1] + 1j * (g_ex[2] + g_ex[3])
+    na = np.linalg.norm(a)
+    t_np = (q.conj().T @ a) @ q
+    g_np = q.conj().T @ q - np.eye(n)
+    qd, ad = ZPlanar.from_any(q), ZPlanar.from_any(a)
+    t_gpu = matmul_hp(matmul_hp(qd, ad, trans_a=True), qd).to_numpy()
+    g_gpu = matmul_hp(qd, qd, trans_a=True, diag_shift=-1.0).to_numpy()
+    for name, t, g in (("numpy", t_np, g_np), ("libsr", t_gpu, g_gpu)):
+        et = np.linalg.norm(np.tril(t - t_hi, -1)) / na / U
+        eg = np.linalg.norm(g - g_lo) / U
+        print("n=%d %-6s stril(T) noise %.2f u*||A||   Y noise %.2f u  (true ||Y|| %.2f u)" % (
+            n, name, et, eg, np.linalg.norm(g_lo) / U), flush=True)

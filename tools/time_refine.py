@@ -1,0 +1,70 @@
+"""Quick timing of refine_template (FP64 mode) and its GEMM on one GPU."""
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2203_10879_b200 import RefineConfig, ZPlanar, inputs, matmul_hp, refine_template  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
+rng = np.random.default_rng(0)
+# GEMM throughput
+a = ZPlanar.from_any(torch.randn(n, n, dtype=torch.complex128))
+b = ZPlanar.from_any(torch.randn(n, n, dtype=torch.complex128))
+br = ZPlanar.from_any(torch.randn(n, n, dtype=torch.float64))
+c = ZPlanar.empty(n)
+for trans, bb, flops, name in ((False, b, 8, "NN"), (True, b, 8, "CN"), (True, br, 4, "CN-real")):
+    for _ in range(2):
+        matmul_hp(a, bb, trans_a=trans, out=c)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    reps = 5
+    for _ in range(reps):
+        matmul_hp(a, bb, trans_a=trans, out=c)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    print("zgemm %s n=%d: %.3f ms  %.2f TFLOP/s" % (name, n, ms, flops * n ** 3 / ms / 1e9), flush=True)
+
+if n <= 4096:
+    A = inputs.gaussian_complex(n, 0)
+    Q = inputs.schur_vectors(A).astype(np.complex128)
+    cfg = RefineConfig(precision="fp64", tol_factor=10.0 / n, max_iters=10)
+    for rep in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pair, r = refine_template(A, Q, cfg)
+        torch.cuda.synchronize()
+        print("refine n=%d: %.3f s  status %s it %d hist %s" % (
+            n, time.perf_counter() - t0, r.status.value, r.iterations,
+            ["%.2e" % (h[0] / np.linalg.norm(A)) for h in r.residual_history]), flush=True)
+
+# Q^ generation options at large n (setup only): LAPACK cgees vs GPU eig + QR
+if len(sys.argv) > 2:
+    import scipy.linalg
+    m = int(sys.argv[2])
+    A = inputs.gaussian_real(m, 0)
+    t0 = time.perf_counter()
+    try:
+        w, v = torch.linalg.eig(torch.from_numpy(A).to(torch.complex64).cuda())
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        q, _ = torch.linalg.qr(v)
+        torch.cuda.synchronize()
+        qn = q.cpu().numpy().astype(np.complex128)
+        th = (qn.conj().T @ A) @ qn
+        print("gpu eig+qr n=%d: eig %.1fs qr %.1fs relE %.2e ortho %.2e" % (
+            m, t1 - t0, time.perf_counter() - t1, np.linalg.norm(np.tril(th, -1)) / np.linalg.norm(A),
+            np.linalg.norm(qn.conj().T @ qn - np.eye(m))), flush=True)
+    except Exception as ex:
+        print("gpu eig failed:", ex, flush=True)
+    t0 = time.perf_counter()
+    _, z = scipy.linalg.schur(A.astype(np.complex64), output="complex")
+    zq = z.astype(np.complex128)
+    th = (zq.conj().T @ A) @ zq
+    print("cgees n=%d: %.1fs relE %.2e ortho %.2e" % (m, time.perf_counter() - t0,
+          np.linalg.norm(np.tril(th, -1)) / np.linalg.norm(A),
+          np.linalg.norm(zq.conj().T @ zq - np.eye(m))), flush=True)

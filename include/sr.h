@@ -49,6 +49,8 @@ extern "C" {
 
 int sr_version(void);
 const char* sr_last_error(void);
+/* number of kernels this process has launched through libsr (bench evidence) */
+unsigned long long sr_kernel_launches(void);
 
 /* hp product in FP64 mode: C = alpha * op(A) * B, then C_ii += diag_shift.
    Replaces matmul_hp (matmul.py:52-81) -> gemm_hp (_numba_kernels.py:18-46).
@@ -98,10 +100,13 @@ int sr_skew_c64(int n, const void* l, long long ld, void* w, double* d_norm_w, i
 /* Sigma of the merged Newton-Schulz update (merged_update,
    orthogonal.py:191-201), planar FP64, summed left to right:
    S = ((((2I + 2W) - Y) - YW) + W^2) + W^3 [+ W^2 Y + W^2 Y W].
-   w, yw, w2, w3 (and optional w2y, w2yw, NULL to skip) are complex64. */
+   w, yw, w2, w3 (and optional w2y, w2yw, NULL to skip) are complex64.
+   with_identity = 0 drops the 2I term (S' = S - 2I, used by the Ozaki path,
+   which forms Q S / 2 = Q + Q S' / 2 exactly). */
 int sr_sigma_merged_f64(int n, const void* w, const double* y_re, const double* y_im, long long ldy,
                         const void* yw, const void* w2, const void* w3, const void* w2y, const void* w2yw,
-                        long long ld_lp, double* s_re, double* s_im, long long lds, void* stream);
+                        long long ld_lp, double* s_re, double* s_im, long long lds, int with_identity,
+                        void* stream);
 
 /* Sigma of the entry Newton-Schulz step: S = 3I - G (orthogonal.py:167-168). */
 int sr_sigma_ns_f64(int n, const double* g_re, const double* g_im, long long ldg, double* s_re, double* s_im,
@@ -113,6 +118,43 @@ int sr_triu_inplace_f64(int n, double* re, double* im, long long ld, void* strea
 
 /* bytes of reduction workspace the norm kernels need */
 size_t sr_reduce_workspace_bytes(void);
+
+/* ---- Ozaki-II emulated products on the int8 tensor cores (csrc/ozaki.cu,
+   csrc/oz_gemm.cu).  Replace matmul_hp / matmul_lp (matmul.py:52-110) in
+   FP64 mode; generalise the reference's Ozaki-I dd path (matmul.py:151-212).
+   Sources are planar FP64 (src_c64 = 0; im may be NULL for a real matrix) or
+   interleaved complex64 (src_c64 = 1; im unused). */
+
+/* exps[i] = e with max_k |op(X)[i,k]| < 2^e; op(X) = X (transposed = 0:
+   per row) or X^T (transposed = 1: per column). */
+int sr_oz_exponents(int rows, int cols, const void* src, const double* im, long long ld, int src_c64,
+                    int transposed, int* exps, void* stream);
+
+/* Residue planes [nmod][planes][rows_out][kpitch] (int8, K-major) of
+   round(op(X) * 2^(beta - exps[i])) modulo moduli[l] (129..256, pairwise
+   coprime; host array).  op(X)[i][k] = X[i][k], or X[k][i] when transposed;
+   conj negates the imaginary part.  layout 0: (re, im) A operand;
+   1: (-im, re, im) complex B operand; 2: (re) real B operand. */
+int sr_oz_encode(int rows_out, int K, const void* src, const double* im, long long ld, int src_c64,
+                 int transposed, int conj, int layout, const int* exps, int beta, int nmod, const int* moduli,
+                 void* out, long long kpitch, void* stream);
+
+/* R_l = A_l B_l^T mod p_l on tcgen05 (kind::i8), out [nmod][2][M][out_pitch]
+   int8 (re, im).  a_planes = 2; b_planes = 3 (complex B) or 1 (real B).
+   moduli is a host array; num_sms <= 0 means 148. */
+int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, const void* a, int a_planes,
+                  long long a_kpitch, const void* b, int b_planes, long long b_kpitch, void* out,
+                  long long out_pitch, int num_sms, void* stream);
+
+/* CRT decode of the residues into C = alpha * C' * 2^-(rho_i + sigma_j)
+   + shift * I + add_scale * X (X = (add_re, add_im), optional), with
+   rho_i = beta_a - exps_a[i], sigma_j = beta_b - exps_b[j].  table (host):
+   [nmod][4] CRT weights, [4] modulus-product chunks, [4] chunk offsets,
+   1/P.  out_kind 0: planar FP64 (out_re, out_im); 1: complex64 (out_re). */
+int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* table, const void* res, long long res_pitch,
+                 const int* exps_a, int beta_a, const int* exps_b, int beta_b, double alpha, double shift,
+                 const double* add_re, const double* add_im, long long ld_add, double add_scale, int out_kind,
+                 void* out_re, double* out_im, long long ld_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -106,6 +106,6 @@ extern "C" int sr_cgemm_c64(int op_a, int m, int n, int k, const void* a, long l
   dim3 grid(sr_ceil_div(n, BN), sr_ceil_div(m, BM));
   cgemm_c64_kernel<<<grid, NT, 0, (cudaStream_t)stream>>>(m, n, k, (const float2*)a, lda, (const float2*)b, ldb,
                                                           (float2*)c, ldc);
-  SR_CUDA_CHECK(cudaGetLastError());
+  SR_LAUNCH_CHECK();
   return SR_OK;
 }

@@ -127,14 +127,14 @@ __global__ void sigma_merged_kernel(int n, const float2* __restrict__ w, const d
                                     const double* __restrict__ yi, long long ldy, const float2* __restrict__ yw,
                                     const float2* __restrict__ w2, const float2* __restrict__ w3,
                                     const float2* __restrict__ w2y, const float2* __restrict__ w2yw, long long ldl,
-                                    double* __restrict__ sr, double* __restrict__ si, long long lds) {
+                                    double* __restrict__ sr, double* __restrict__ si, long long lds, double eye) {
   const long long total = (long long)n * n;
   for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
     int i = (int)(idx / n), j = (int)(idx % n);
     size_t o = (size_t)i * ldl + j;
     float2 wv = w[o];
     // ((((2I + 2W) - Y) - YW) + W^2) + W^3, left to right (orthogonal.py:191-195)
-    double re = (i == j ? 2.0 : 0.0) + 2.0 * (double)wv.x;
+    double re = (i == j ? eye : 0.0) + 2.0 * (double)wv.x;
     double im = 2.0 * (double)wv.y;
     re = re - yr[(size_t)i * ldy + j];
     im = im - yi[(size_t)i * ldy + j];
@@ -195,7 +195,7 @@ extern "C" int sr_split_lp_c64(int n, const double* that_re, const double* that_
   split_lp_kernel<<<RBLOCKS, RT, 0, (cudaStream_t)stream>>>(n, that_re, that_im, ldt, (float2*)t_lp,
                                                              (float2*)e_lp, ld_lp, r.partials, r.counter,
                                                              d_norm_e);
-  SR_CUDA_CHECK(cudaGetLastError());
+  SR_LAUNCH_CHECK();
   return SR_OK;
 }
 
@@ -204,7 +204,7 @@ extern "C" int sr_fro_norm_f64(int m, int n, const double* re, const double* im,
   if (m < 0 || n < 0 || !ws || ws_bytes < sr_reduce_workspace_bytes()) return SR_EINVAL;
   RedWs r = red_ws(ws);
   fro_norm_kernel<<<RBLOCKS, RT, 0, (cudaStream_t)stream>>>(m, n, re, im, ld, r.partials, r.counter, d_out);
-  SR_CUDA_CHECK(cudaGetLastError());
+  SR_LAUNCH_CHECK();
   return SR_OK;
 }
 
@@ -214,7 +214,7 @@ extern "C" int sr_downcast_c64(int m, int n, const double* re, const double* im,
   if ((long long)m * n == 0) return SR_OK;
   downcast_kernel<<<ew_grid((long long)m * n), RT, 0, (cudaStream_t)stream>>>(m, n, re, im, ld, (float2*)out,
                                                                               ld_out);
-  SR_CUDA_CHECK(cudaGetLastError());
+  SR_LAUNCH_CHECK();
   return SR_OK;
 }
 
@@ -224,20 +224,20 @@ extern "C" int sr_skew_c64(int n, const void* l, long long ld, void* w, double* 
   RedWs r = red_ws(ws);
   skew_kernel<<<RBLOCKS, RT, 0, (cudaStream_t)stream>>>(n, (const float2*)l, ld, (float2*)w, d_flags, r.partials,
                                                          r.counter, d_norm_w);
-  SR_CUDA_CHECK(cudaGetLastError());
+  SR_LAUNCH_CHECK();
   return SR_OK;
 }
 
 extern "C" int sr_sigma_merged_f64(int n, const void* w, const double* y_re, const double* y_im, long long ldy,
                                    const void* yw, const void* w2, const void* w3, const void* w2y,
                                    const void* w2yw, long long ld_lp, double* s_re, double* s_im, long long lds,
-                                   void* stream) {
+                                   int with_identity, void* stream) {
   if (n < 0 || (w2y == nullptr) != (w2yw == nullptr)) return SR_EINVAL;
   if (n == 0) return SR_OK;
   sigma_merged_kernel<<<ew_grid((long long)n * n), RT, 0, (cudaStream_t)stream>>>(
       n, (const float2*)w, y_re, y_im, ldy, (const float2*)yw, (const float2*)w2, (const float2*)w3,
-      (const float2*)w2y, (const float2*)w2yw, ld_lp, s_re, s_im, lds);
-  SR_CUDA_CHECK(cudaGetLastError());
+      (const float2*)w2y, (const float2*)w2yw, ld_lp, s_re, s_im, lds, with_identity ? 2.0 : 0.0);
+  SR_LAUNCH_CHECK();
   return SR_OK;
 }
 
@@ -246,7 +246,7 @@ extern "C" int sr_sigma_ns_f64(int n, const double* g_re, const double* g_im, lo
   if (n < 0) return SR_EINVAL;
   if (n == 0) return SR_OK;
   sigma_ns_kernel<<<ew_grid((long long)n * n), RT, 0, (cudaStream_t)stream>>>(n, g_re, g_im, ldg, s_re, s_im, lds);
-  SR_CUDA_CHECK(cudaGetLastError());
+  SR_LAUNCH_CHECK();
   return SR_OK;
 }
 
@@ -254,6 +254,6 @@ extern "C" int sr_triu_inplace_f64(int n, double* re, double* im, long long ld, 
   if (n < 0) return SR_EINVAL;
   if (n == 0) return SR_OK;
   triu_kernel<<<ew_grid((long long)n * n), RT, 0, (cudaStream_t)stream>>>(n, re, im, ld);
-  SR_CUDA_CHECK(cudaGetLastError());
+  SR_LAUNCH_CHECK();
   return SR_OK;
 }

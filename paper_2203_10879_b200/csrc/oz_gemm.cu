@@ -1,0 +1,378 @@
+// Modular int8 GEMM on the 5th-generation tensor cores (tcgen05, kind::i8).
+//
+// The engine of the Ozaki-II emulated FP64 / FP32 complex products (see
+// ozaki.cu and DESIGN.md §Ozaki): for every modulus p_l of the plan it
+// computes the residue matrix
+//     R_l = (A_l B_l^T) mod p_l            (complex: 4M, fused in one tile)
+// from int8 residue operands that ozaki.cu's encoder wrote K-major.
+// Every product is exact (|A_l|,|B_l| <= 128, int32 accumulation of K <= 2^17
+// terms), so the result is independent of the summation order.
+//
+// Complex tile trick: the B stage holds three 128-row planes in the order
+// [-B_im | B_re | B_im], so the two N = 256 MMAs
+//     D[:, 0:256] += A_re x [B_re | B_im]^T
+//     D[:, 0:256] += A_im x [-B_im | B_re]^T
+// leave D = [C_re | C_im] in one 256-column TMEM accumulator.
+//
+// Kernel shape: persistent, one CTA per SM, warp-specialised —
+//   warp 0     TMA producer (4-d tensor maps, 64-byte swizzle, 5-stage ring)
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-5  epilogue: tcgen05.ld -> mod p -> int8 residues -> global
+// with two 256-column TMEM accumulators so the epilogue of tile i overlaps
+// the MMAs of tile i+1.  Tiles are rasterised in groups of 16 M-tiles so
+// the operand panels of a wave stay resident in the 126 MB L2.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "sr_common.cuh"
+
+namespace {
+
+constexpr int TM = 128, TN = 128, TK = 64;  // tile: 128 rows x 128 cols, 64-byte k blocks
+constexpr int STAGES = 5;
+constexpr int PLANE_BYTES = TM * TK;        // 8 KB per 128-row, 64-byte plane
+constexpr int NUM_THREADS = 192;
+constexpr int GROUP_M = 16;
+constexpr int MAX_MODULI = 32;
+
+struct OzParams {
+  int M, N, K, nmod;
+  int a_planes, b_planes;
+  int tiles_m, tiles_n;
+  long long out_pitch;          // bytes between output rows
+  long long out_plane;          // bytes between output planes (re / im)
+  long long out_mod;            // bytes between moduli
+  int moduli[MAX_MODULI];
+  float inv[MAX_MODULI];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];\n" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, 64-byte swizzle, 8-row groups 512 B apart.
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;        // SBO
+  d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
+  d |= (uint64_t)4 << 61;                 // SWIZZLE_64B
+  return d;
+}
+
+__device__ __forceinline__ constexpr uint32_t idesc_i8(int m, int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void decode_tile(const OzParams& p, int t, int& l, int& mt, int& nt) {
+  const int per_mod = p.tiles_m * p.tiles_n;
+  l = t / per_mod;
+  int r = t - l * per_mod;
+  const int group = r / (GROUP_M * p.tiles_n);
+  const int first_m = group * GROUP_M;
+  const int gm = min(GROUP_M, p.tiles_m - first_m);
+  const int in = r - group * GROUP_M * p.tiles_n;
+  mt = first_m + in % gm;
+  nt = in / gm;
+}
+
+// symmetric residue of v modulo p: [-floor(p/2), ceil(p/2) - 1]
+__device__ __forceinline__ int sym_mod(int v, int p, float inv) {
+  int q = __float2int_rn((float)v * inv);
+  int r = v - q * p;
+  const int lo = -(p >> 1), hi = ((p + 1) >> 1) - 1;
+  if (r > hi) r -= p;
+  if (r < lo) r += p;
+  if (r > hi) r -= p;
+  if (r < lo) r += p;
+  return r;
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    oz_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                   const __grid_constant__ OzParams p, int8_t* __restrict__ out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int a_bytes = p.a_planes * PLANE_BYTES;
+  const int b_bytes = p.b_planes * PLANE_BYTES;
+  const int stage_bytes = a_bytes + b_bytes;
+  uint64_t* bars = (uint64_t*)(smem + STAGES * stage_bytes);
+  // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]; then tmem base slot
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t bar0 = smem_u32(bars);
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
+  auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * STAGES + b); };
+  auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * STAGES + 2 + b); };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull_bar(b), 1);
+      mbar_init(tempty_bar(b), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&tmap_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&tmap_b) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int total_tiles = p.nmod * p.tiles_m * p.tiles_n;
+  const int kblocks = (p.K + TK - 1) / TK;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        int l, mt, nt;
+        decode_tile(p, t, l, mt, nt);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty_bar(stage), phase ^ 1);
+          uint8_t* st = smem + stage * stage_bytes;
+          mbar_expect_tx(full_bar(stage), stage_bytes);
+          tma_load_4d(smem_u32(st), &tmap_a, full_bar(stage), kb * TK, mt * TM, 0, l);
+          tma_load_4d(smem_u32(st + a_bytes), &tmap_b, full_bar(stage), kb * TK, nt * TN, 0, l);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    const bool cplx = (p.b_planes == 3);
+    const uint32_t id256 = idesc_i8(128, 256), id128 = idesc_i8(128, 128);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      mbar_wait(tempty_bar(acc), acc_phase ^ 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t d = tmem_base + (uint32_t)(acc * 256);
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(full_bar(stage), phase);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(smem + stage * stage_bytes);
+          const uint32_t sb = sa + a_bytes;
+#pragma unroll
+          for (int ks = 0; ks < TK / 32; ++ks) {
+            const uint32_t acc_flag = (kb | ks) != 0;
+            const uint64_t are = umma_desc_sw64(sa + ks * 32);
+            const uint64_t aim = umma_desc_sw64(sa + PLANE_BYTES + ks * 32);
+            if (cplx) {
+              const uint64_t b1 = umma_desc_sw64(sb + PLANE_BYTES + ks * 32);  // [B_re | B_im]
+              const uint64_t b2 = umma_desc_sw64(sb + ks * 32);                // [-B_im | B_re]
+              umma_i8(d, are, b1, id256, acc_flag);
+              umma_i8(d, aim, b2, id256, 1u);
+            } else {
+              const uint64_t b = umma_desc_sw64(sb + ks * 32);
+              umma_i8(d, are, b, id128, acc_flag);
+              umma_i8(d + 128, aim, b, id128, acc_flag);
+            }
+          }
+          umma_commit(empty_bar(stage));
+          if (kb == kblocks - 1) umma_commit(tfull_bar(acc));
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else {
+    // ---------------- epilogue: TMEM -> residues -> global ----------------
+    const int ew = warp & 3;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      int l, mt, nt;
+      decode_tile(p, t, l, mt, nt);
+      const int pm = p.moduli[l];
+      const float inv = p.inv[l];
+      mbar_wait(tfull_bar(acc), acc_phase);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const int row = mt * TM + ew * 32 + lane;
+      int8_t* base = out + (size_t)l * p.out_mod + (size_t)row * p.out_pitch;
+#pragma unroll 1
+      for (int chunk = 0; chunk < 16; ++chunk) {
+        uint32_t v[16];
+        tmem_ld16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * 256 + chunk * 16), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        const int plane = chunk >> 3;
+        const int col0 = nt * TN + (chunk & 7) * 16;
+        uint32_t packed[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t w = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            int r = sym_mod((int)v[q * 4 + e], pm, inv);
+            w |= ((uint32_t)(r & 0xFF)) << (8 * e);
+          }
+          packed[q] = w;
+        }
+        if (row < p.M) {
+          int8_t* dst = base + (size_t)plane * p.out_plane + col0;
+          if (col0 + 16 <= p.N) {
+            *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+          } else {
+            for (int e = 0; e < 16 && col0 + e < p.N; ++e) dst[e] = (int8_t)((packed[e >> 2] >> (8 * (e & 3))) & 0xFF);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      mbar_arrive(tempty_bar(acc));
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)ptr;
+  }
+  return fn;
+}
+
+// 4-d map over [nmod][planes][rows][kpitch] int8, box (64, 128, planes, 1).
+int make_map(CUtensorMap* map, const void* base, int K, int rows, int planes, int nmod, long long kpitch) {
+  auto enc = get_encode();
+  if (!enc) return SR_ECUDA;
+  cuuint64_t dims[4] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)planes, (cuuint64_t)nmod};
+  cuuint64_t strides[3] = {(cuuint64_t)kpitch, (cuuint64_t)(kpitch * rows), (cuuint64_t)(kpitch * rows * planes)};
+  cuuint32_t box[4] = {(cuuint32_t)TK, (cuuint32_t)TM, (cuuint32_t)planes, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? SR_OK : SR_ECUDA;
+}
+
+}  // namespace
+
+extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, const void* a, int a_planes,
+                             long long a_kpitch, const void* b, int b_planes, long long b_kpitch, void* out,
+                             long long out_pitch, int num_sms, void* stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || nmod <= 0 || nmod > MAX_MODULI) return SR_EINVAL;
+  if (a_planes != 2 || (b_planes != 1 && b_planes != 3)) return SR_EINVAL;
+  if ((a_kpitch | b_kpitch | out_pitch) & 15) return SR_EINVAL;
+  if (K > (1 << 17)) return SR_EINVAL;  // int32 accumulation stays exact below this
+  if (((uintptr_t)a | (uintptr_t)b | (uintptr_t)out) & 15) return SR_EINVAL;
+  OzParams p;
+  memset(&p, 0, sizeof(p));
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.nmod = nmod;
+  p.a_planes = a_planes;
+  p.b_planes = b_planes;
+  p.tiles_m = (M + TM - 1) / TM;
+  p.tiles_n = (N + TN - 1) / TN;
+  p.out_pitch = out_pitch;
+  p.out_plane = out_pitch * M;
+  p.out_mod = p.out_plane * 2;
+  for (int i = 0; i < nmod; ++i) {
+    if (moduli[i] < 2 || moduli[i] > 256) return SR_EINVAL;
+    p.moduli[i] = moduli[i];
+    p.inv[i] = 1.0f / (float)moduli[i];
+  }
+  CUtensorMap ma, mb;
+  if (make_map(&ma, a, K, M, a_planes, nmod, a_kpitch) != SR_OK) return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(A)");
+  if (make_map(&mb, b, K, N, b_planes, nmod, b_kpitch) != SR_OK) return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(B)");
+  const size_t smem = 1024 + (size_t)STAGES * (a_planes + b_planes) * PLANE_BYTES + 256;
+  static bool configured = false;
+  if (!configured) {
+    SR_CUDA_CHECK(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured = true;
+  }
+  const int tiles = nmod * p.tiles_m * p.tiles_n;
+  int grid = num_sms > 0 ? num_sms : 148;
+  if (grid > tiles) grid = tiles;
+  oz_gemm_kernel<<<grid, NUM_THREADS, smem, (cudaStream_t)stream>>>(ma, mb, p, (int8_t*)out);
+  SR_LAUNCH_CHECK();
+  return SR_OK;
+}

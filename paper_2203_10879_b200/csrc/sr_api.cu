@@ -2,6 +2,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
+
 #include "sr_common.cuh"
 
 static thread_local char g_last_error[512] = "";
@@ -10,6 +12,12 @@ int sr_set_cuda_error(cudaError_t e, const char* what) {
   snprintf(g_last_error, sizeof(g_last_error), "%s: %s", what, cudaGetErrorString(e));
   return SR_ECUDA;
 }
+
+static std::atomic<unsigned long long> g_launches{0};
+
+void sr_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+extern "C" unsigned long long sr_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 extern "C" int sr_version(void) { return 1; }
 

@@ -12,6 +12,14 @@
   } while (0)
 
 int sr_set_cuda_error(cudaError_t e, const char* what);
+void sr_count_launch();
+
+// after every kernel launch: count it (sr_kernel_launches) and surface launch errors
+#define SR_LAUNCH_CHECK()                       \
+  do {                                          \
+    sr_count_launch();                          \
+    SR_CUDA_CHECK(cudaGetLastError());          \
+  } while (0)
 
 static inline int sr_ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 

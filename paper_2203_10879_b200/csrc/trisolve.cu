@@ -273,7 +273,7 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
   {
     dim3 b(32, 8), g(sr_ceil_div(n, 32), sr_ceil_div(n, 8));
     separation_kernel<C><<<g, b, 0, st>>>(n, t, ld, d_flags);
-    SR_CUDA_CHECK(cudaGetLastError());
+    SR_LAUNCH_CHECK();
   }
   const size_t smem = sizeof(C) * (3 * NB * (NB + 1));
   auto kern = trisolve_level_kernel<C>;
@@ -294,7 +294,7 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
     LevelArgs a{n, N, level, splits, ld};
     kern<<<dim3(tiles, splits), NT, smem, st>>>(a, t, e, l, part, counters, (typename Real<C>::T)clip,
                                                 d_clipped);
-    SR_CUDA_CHECK(cudaGetLastError());
+    SR_LAUNCH_CHECK();
   }
   return SR_OK;
 }

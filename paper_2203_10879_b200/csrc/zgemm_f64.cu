@@ -230,7 +230,7 @@ int launch(int m, int n, int k, double alpha, double shift, const double* ar, co
   }
   dim3 grid(sr_ceil_div(n, BN), sr_ceil_div(m, BM));
   kern<<<grid, NTHREADS, SMEM_BYTES, st>>>(m, n, k, alpha, shift, ar, ai, lda, br, bi, ldb, cr, ci, ldc);
-  SR_CUDA_CHECK(cudaGetLastError());
+  SR_LAUNCH_CHECK();
   return SR_OK;
 }
 

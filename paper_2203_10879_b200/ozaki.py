@@ -1,0 +1,168 @@
+"""Ozaki-II emulated products on the B200's int8 tensor cores (host side).
+
+C = alpha * op(A) B (+ shift I) (+ add_scale X) is computed exactly on
+integers: op(A) and B are scaled per row / column to integers below 2^beta,
+reduced modulo r pairwise-coprime moduli p_l <= 256 (int8 residues), the r
+residue products run on tcgen05 (csrc/oz_gemm.cu), and the Chinese remainder
+theorem recovers C' before one final rounding (csrc/ozaki.cu).  The plan
+picks the smallest r with  prod(p_l) > 4 * 2K * 2^(beta_a + beta_b), so the
+CRT representative is unique with a 2-bit margin.
+
+Where it sits in the reference: it replaces matmul_hp / matmul_lp
+(/root/reference/pkg/src/ddschur/matmul.py:52-110) in FP64 mode and
+generalises the reference's own Ozaki-I dd path (_ozaki_gemm_hp,
+matmul.py:151-212), which splits into FP64 slices multiplied by BLAS.
+"""
+import math
+
+import torch
+
+from . import _lib
+
+# pairwise-coprime moduli, largest first (greedy from 256 down)
+MODULI = [256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193, 191, 181, 179, 173,
+          167, 163, 157, 151]
+CHUNK_BITS = 40
+MAXCHUNK = 4
+
+HP_BETA = 60   # hp (FP64-mode) operands: every entry within 2^-7 of its row max is exact
+LP_BETA = 26   # lp (complex64) operands: complex64 significand + 2 guard bits
+
+
+class OzPlan:
+    """Moduli and CRT constants for products with inner dimension <= K."""
+
+    def __init__(self, K, beta_a, beta_b):
+        self.K = K
+        self.beta_a = beta_a
+        self.beta_b = beta_b
+        need = beta_a + beta_b + math.ceil(math.log2(max(K, 2))) + 1 + 2
+        P = 1
+        r = 0
+        while P.bit_length() - 1 < need:
+            if r == len(MODULI):
+                raise ValueError("no Ozaki plan for K=%d beta=(%d,%d)" % (K, beta_a, beta_b))
+            P *= MODULI[r]
+            r += 1
+        self.nmod = r
+        self.moduli = MODULI[:r]
+        self.P = P
+        nbits = P.bit_length()
+        nchunk = (nbits + CHUNK_BITS - 1) // CHUNK_BITS
+        if nchunk > MAXCHUNK:
+            raise ValueError("modulus product too wide")
+        offs = [max(nbits - CHUNK_BITS * (j + 1), 0) for j in range(nchunk)]
+
+        def chunks(x):
+            out = []
+            for j in range(nchunk):
+                hi = nbits if j == 0 else offs[j - 1]
+                out.append(float((x >> offs[j]) & ((1 << (hi - offs[j])) - 1)))
+            return out + [0.0] * (MAXCHUNK - nchunk)
+        table = []
+        for p in self.moduli:
+            m = P // p
+            w = (m * pow(m % p, -1, p)) % P
+            table += chunks(w)
+        table += chunks(P)
+        table += [float(o) for o in offs] + [0.0] * (MAXCHUNK - nchunk)
+        table += [1.0 / float(P)]
+        self.nchunk = nchunk
+        self.table = (torch.tensor(table, dtype=torch.float64)).numpy()
+        self._moduli_c = (torch.tensor(self.moduli, dtype=torch.int32)).numpy()
+
+    def moduli_ptr(self):
+        return self._moduli_c.ctypes.data
+
+    def table_ptr(self):
+        return self.table.ctypes.data
+
+
+_PLANS = {}
+
+
+def plan(K, beta_a, beta_b):
+    key = (K, beta_a, beta_b)
+    if key not in _PLANS:
+        _PLANS[key] = OzPlan(K, beta_a, beta_b)
+    return _PLANS[key]
+
+
+def kpitch(K):
+    return (K + 15) // 16 * 16
+
+
+class Encoded:
+    """Residue planes of one operand (A role: op(X) rows; B role: columns)."""
+
+    __slots__ = ("buf", "exps", "rows", "K", "planes", "beta", "nmod", "kp")
+
+    def __init__(self, rows, K, planes, beta, nmod, device):
+        self.rows, self.K, self.planes, self.beta, self.nmod = rows, K, planes, beta, nmod
+        self.kp = kpitch(K)
+        self.buf = torch.empty(nmod * planes * rows * self.kp, dtype=torch.int8, device=device)
+        self.exps = torch.empty(rows, dtype=torch.int32, device=device)
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _src(x):
+    """(ptr, im_ptr, ld, c64) for a ZPlanar or an interleaved complex64 tensor."""
+    if isinstance(x, torch.Tensor):
+        return x.data_ptr(), None, x.shape[1], 1
+    return x.re_ptr(), x.im_ptr(), x.ld, 0
+
+
+def encode(x, rows, cols, role, pl, conj_t=False, out=None):
+    """Encode op(X) as an A operand (role "a": rows x K, op = conj-transpose
+    when conj_t) or X as a B operand (role "b": K = rows of X, output rows =
+    columns of X).  x: ZPlanar (FP64) or complex64 (rows, ld) tensor."""
+    ptr, im, ld, c64 = _src(x)
+    real = (im is None and not c64)
+    if role == "a":
+        out_rows, K, transposed, layout, planes, beta = (cols, rows, 1, 0, 2, pl.beta_a) if conj_t else \
+            (rows, cols, 0, 0, 2, pl.beta_a)
+        conj = 1 if conj_t else 0
+    else:
+        out_rows, K, transposed, beta = cols, rows, 1, pl.beta_b
+        layout, planes = (2, 1) if real else (1, 3)
+        conj = 0
+    dev = x.device if isinstance(x, torch.Tensor) else x.re_buf.device
+    enc = out if out is not None else Encoded(out_rows, K, planes, beta, pl.nmod, dev)
+    st = _stream()
+    _lib.call("sr_oz_exponents", rows, cols, ptr, im, ld, c64, transposed, enc.exps.data_ptr(), st)
+    _lib.call("sr_oz_encode", out_rows, K, ptr, im, ld, c64, transposed, conj, layout, enc.exps.data_ptr(),
+              beta, pl.nmod, pl.moduli_ptr(), enc.buf.data_ptr(), enc.kp, st)
+    return enc
+
+
+class ResidueBuffer:
+    def __init__(self, M, N, nmod, device):
+        self.M, self.N, self.nmod = M, N, nmod
+        self.pitch = kpitch(N)
+        self.buf = torch.empty(nmod * 2 * M * self.pitch, dtype=torch.int8, device=device)
+
+
+def gemm_residues(ea, eb, pl, res):
+    if ea.K != eb.K:
+        raise ValueError("inner dimensions disagree: %d vs %d" % (ea.K, eb.K))
+    _lib.call("sr_oz_gemm_i8", ea.rows, eb.rows, ea.K, pl.nmod, pl.moduli_ptr(), ea.buf.data_ptr(), ea.planes,
+              ea.kp, eb.buf.data_ptr(), eb.planes, eb.kp, res.buf.data_ptr(), res.pitch, 0, _stream())
+
+
+def decode(res, ea, eb, pl, out, alpha=1.0, shift=0.0, add=None, add_scale=1.0):
+    """out: ZPlanar (FP64 planar) or complex64 (M, ld) tensor."""
+    if isinstance(out, torch.Tensor):
+        out_kind, o_re, o_im, ld_out = 1, out.data_ptr(), None, out.shape[1]
+    else:
+        out_kind, o_re, o_im, ld_out = 0, out.re_ptr(), out.im_ptr(), out.ld
+    a_re = a_im = None
+    ld_add = 0
+    if add is not None:
+        a_re, a_im, ld_add = add.re_ptr(), add.im_ptr(), add.ld
+    _lib.call("sr_oz_decode", res.M, res.N, pl.nmod, pl.nchunk, pl.table_ptr(), res.buf.data_ptr(), res.pitch,
+              ea.exps.data_ptr(), ea.beta, eb.exps.data_ptr(), eb.beta, float(alpha), float(shift), a_re, a_im,
+              ld_add, float(add_scale), out_kind, o_re, o_im, ld_out, _stream())
+    return out

@@ -1,0 +1,170 @@
+"""The matrix products of one FP64-mode refinement, two implementations.
+
+Every product the loop needs (refine.py:259,265 and orthogonal.py:167-201):
+  entry    Q = (Q^ (3I - Q^H Q^)) / 2                    (2 hp products)
+  measure  P = Q^H A, T^ = P Q, Y = Q^H Q - I            (3 hp products)
+  update   YW, W^2, W^3 (lp), Sigma (hp sum), Q S / 2    (3 lp + 1 hp product)
+
+OzakiProducts (default) runs them as Ozaki-II emulated products on the int8
+tensor cores (ozaki.py, csrc/oz_gemm.cu): exact integer products, so the
+stril(Q^H A Q) measurement noise does not grow with n, and the update is
+formed as Q + Q S'/2 with S' = S - 2I (the same matrix as Q S / 2,
+with one rounding instead of a K-long accumulation).  DmmaProducts runs
+them on the FP64 DMMA pipe (csrc/zgemm_f64.cu) and the FP32 SIMT lp GEMM
+(csrc/cgemm_c64.cu); it is kept as the native-FP64 comparison point.
+"""
+import torch
+
+from . import _lib, ozaki
+from .matmul import _counters, matmul_hp, matmul_lp
+from .matrix import ZPlanar, lp_empty
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _sigma(ws, restore_full_sigma, with_identity):
+    n = ws.n
+    w2y = w2yw = None
+    if restore_full_sigma:
+        w2y, w2yw = ws.w2y.data_ptr(), ws.w2yw.data_ptr()
+    _lib.call("sr_sigma_merged_f64", n, ws.w_lp.data_ptr(), ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld,
+              ws.yw.data_ptr(), ws.w2.data_ptr(), ws.w3.data_ptr(), w2y, w2yw, ws.w_lp.shape[1],
+              ws.sigma.re_ptr(), ws.sigma.im_ptr(), ws.sigma.ld, 1 if with_identity else 0, _stream())
+
+
+def _downcast_y(ws):
+    n = ws.n
+    _lib.call("sr_downcast_c64", n, n, ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld, ws.y_lp.data_ptr(),
+              ws.y_lp.shape[1], _stream())
+
+
+class DmmaProducts:
+    name = "dmma"
+
+    def __init__(self, ws, a):
+        self.ws = ws
+
+    def entry(self, qhat):
+        ws = self.ws
+        n = ws.n
+        g = matmul_hp(qhat, qhat, trans_a=True, out=ws.y)
+        _lib.call("sr_sigma_ns_f64", n, g.re_ptr(), g.im_ptr(), g.ld, ws.sigma.re_ptr(), ws.sigma.im_ptr(),
+                  ws.sigma.ld, _stream())
+        matmul_hp(qhat, ws.sigma, alpha=0.5, out=ws.q)
+
+    def measure(self, a):
+        ws = self.ws
+        matmul_hp(ws.q, a, trans_a=True, out=ws.p)
+        matmul_hp(ws.p, ws.q, out=ws.that)
+        matmul_hp(ws.q, ws.q, trans_a=True, diag_shift=-1.0, out=ws.y)
+
+    def update(self, restore_full_sigma):
+        ws = self.ws
+        n = ws.n
+        _downcast_y(ws)
+        matmul_lp(ws.y_lp, ws.w_lp, n, n, n, out=ws.yw)
+        matmul_lp(ws.w_lp, ws.w_lp, n, n, n, out=ws.w2)
+        matmul_lp(ws.w2, ws.w_lp, n, n, n, out=ws.w3)
+        if restore_full_sigma:
+            matmul_lp(ws.w2, ws.y_lp, n, n, n, out=ws.w2y)
+            matmul_lp(ws.w2y, ws.w_lp, n, n, n, out=ws.w2yw)
+        _sigma(ws, restore_full_sigma, True)
+        matmul_hp(ws.q, ws.sigma, alpha=0.5, out=ws.q_next)
+        ws.q, ws.q_next = ws.q_next, ws.q
+
+
+class OzakiProducts:
+    """All products on the int8 tensor cores; encodings are reused across the
+    products that share an operand (Q^H feeds P and Y, Q feeds T^ and Y, the
+    constant A is encoded once per refinement, W once per update)."""
+
+    name = "ozaki"
+
+    def __init__(self, ws, a):
+        self.ws = ws
+        n = ws.n
+        dev = ws.q.re_buf.device
+        self.hp = ozaki.plan(n, ozaki.HP_BETA, ozaki.HP_BETA)
+        self.lp = ozaki.plan(n, ozaki.LP_BETA, ozaki.LP_BETA)
+        hp, lp = self.hp, self.lp
+        self.ea_qh = ozaki.Encoded(n, n, 2, hp.beta_a, hp.nmod, dev)   # Q^H, A role
+        self.ea_x = ozaki.Encoded(n, n, 2, hp.beta_a, hp.nmod, dev)    # P or Q, A role
+        self.eb_q = ozaki.Encoded(n, n, 3, hp.beta_b, hp.nmod, dev)    # Q, B role
+        self.eb_s = ozaki.Encoded(n, n, 3, hp.beta_b, hp.nmod, dev)    # Sigma' / Y', B role
+        self.res = ozaki.ResidueBuffer(n, n, hp.nmod, dev)
+        self.la = ozaki.Encoded(n, n, 2, lp.beta_a, lp.nmod, dev)      # Y_lp / W / W^2, A role
+        self.lb = ozaki.Encoded(n, n, 3, lp.beta_b, lp.nmod, dev)      # W, B role
+        self.lres = ozaki.ResidueBuffer(n, n, lp.nmod, dev)
+        # the constant matrix A, B role (real A keeps one plane)
+        self.eb_a = ozaki.encode(a, n, n, "b", hp)
+
+    def _hp(self, ea, eb, out, **kw):
+        ozaki.gemm_residues(ea, eb, self.hp, self.res)
+        ozaki.decode(self.res, ea, eb, self.hp, out, **kw)
+        _counters["hp_calls"] += 1
+
+    def _lp(self, ea, eb, out):
+        ozaki.gemm_residues(ea, eb, self.lp, self.lres)
+        ozaki.decode(self.lres, ea, eb, self.lp, out)
+        _counters["lp_calls"] += 1
+
+    def entry(self, qhat):
+        """Q = Q^ (3I - G) / 2 = Q^ - Q^ (G - I) / 2 (orthogonal.py:167-169)."""
+        ws, hp, n = self.ws, self.hp, self.ws.n
+        ozaki.encode(qhat, n, n, "a", hp, conj_t=True, out=self.ea_qh)
+        ozaki.encode(qhat, n, n, "b", hp, out=self.eb_q)
+        self._hp(self.ea_qh, self.eb_q, ws.y, shift=-1.0)               # G - I
+        ozaki.encode(qhat, n, n, "a", hp, out=self.ea_x)
+        ozaki.encode(ws.y, n, n, "b", hp, out=self.eb_s)
+        self._hp(self.ea_x, self.eb_s, ws.q, alpha=-0.5, add=qhat)       # Q^ - Q^ (G - I) / 2
+
+    def measure(self, a):
+        ws, hp, n = self.ws, self.hp, self.ws.n
+        ozaki.encode(ws.q, n, n, "a", hp, conj_t=True, out=self.ea_qh)
+        ozaki.encode(ws.q, n, n, "b", hp, out=self.eb_q)
+        self._hp(self.ea_qh, self.eb_a, ws.p)                            # P = Q^H A
+        ozaki.encode(ws.p, n, n, "a", hp, out=self.ea_x)
+        self._hp(self.ea_x, self.eb_q, ws.that)                          # T^ = P Q
+        self._hp(self.ea_qh, self.eb_q, ws.y, shift=-1.0)                # Y = Q^H Q - I
+
+    def update(self, restore_full_sigma):
+        ws, hp, lp, n = self.ws, self.hp, self.lp, self.ws.n
+        _downcast_y(ws)
+        ozaki.encode(ws.w_lp, n, n, "b", lp, out=self.lb)                # W, B role (all lp products)
+        ozaki.encode(ws.y_lp, n, n, "a", lp, out=self.la)
+        self._lp(self.la, self.lb, ws.yw)                                # Y W
+        ozaki.encode(ws.w_lp, n, n, "a", lp, out=self.la)
+        self._lp(self.la, self.lb, ws.w2)                                # W^2
+        ozaki.encode(ws.w2, n, n, "a", lp, out=self.la)
+        self._lp(self.la, self.lb, ws.w3)                                # W^3
+        if restore_full_sigma:
+            ozaki.encode(ws.y_lp, n, n, "b", lp, out=self.lb)
+            ozaki.encode(ws.w2, n, n, "a", lp, out=self.la)
+            self._lp(self.la, self.lb, ws.w2y)                           # W^2 Y
+            ozaki.encode(ws.w_lp, n, n, "b", lp, out=self.lb)
+            ozaki.encode(ws.w2y, n, n, "a", lp, out=self.la)
+            self._lp(self.la, self.lb, ws.w2yw)                          # W^2 Y W
+        _sigma(ws, restore_full_sigma, False)                             # S' = S - 2I
+        ozaki.encode(ws.q, n, n, "a", hp, out=self.ea_x)
+        ozaki.encode(ws.sigma, n, n, "b", hp, out=self.eb_s)
+        self._hp(self.ea_x, self.eb_s, ws.q_next, alpha=0.5, add=ws.q)  # Q + Q S' / 2
+        ws.q, ws.q_next = ws.q_next, ws.q
+
+
+def make(kind, ws, a):
+    if kind == "ozaki":
+        return OzakiProducts(ws, a)
+    if kind == "dmma":
+        return DmmaProducts(ws, a)
+    raise ValueError("unknown gemm kind %r" % (kind,))
+
+
+def ensure_full_sigma_buffers(ws):
+    if ws.w2y is None:
+        ws.w2y = lp_empty(ws.n, device=ws.w_lp.device)
+        ws.w2yw = lp_empty(ws.n, device=ws.w_lp.device)
+
+
+__all__ = ["DmmaProducts", "OzakiProducts", "make", "ensure_full_sigma_buffers", "ZPlanar"]

@@ -23,9 +23,9 @@ import time
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, products
 from .errors import NonFiniteError, NormTooLarge, NotSymmetric, SeparationError  # noqa: F401
-from .matmul import _counters, matmul_hp, matmul_lp, spectral_norm_estimate
+from .matmul import _counters, matmul_hp, spectral_norm_estimate
 from .matrix import ZPlanar, lp_empty
 from .trisolve import SolverWorkspace, solve_lp_device
 
@@ -51,7 +51,9 @@ class RefineStatus(enum.Enum):
 
 @dataclasses.dataclass
 class RefineConfig:
-    """refine.py:53-82, plus `precision` ("fp64" | "dd")."""
+    """refine.py:53-82, plus `precision` ("fp64" | "dd") and `gemm`
+    ("ozaki": int8 tensor-core Ozaki-II products, default; "dmma": FP64
+    DMMA / FP32 SIMT products)."""
 
     tol_factor: float = 10.0
     max_iters: int = 20
@@ -62,6 +64,7 @@ class RefineConfig:
     seed: int = 0
     restore_full_sigma: bool = False
     precision: str = "dd"
+    gemm: str = "ozaki"
 
     def __post_init__(self):
         if not self.tol_factor > 0.0:
@@ -76,6 +79,8 @@ class RefineConfig:
             raise ValueError("ortho must be an OrthoStrategy")
         if self.precision not in ("fp64", "dd"):
             raise ValueError("precision must be 'fp64' or 'dd'")
+        if self.gemm not in ("ozaki", "dmma"):
+            raise ValueError("gemm must be 'ozaki' or 'dmma'")
 
 
 @dataclasses.dataclass
@@ -155,44 +160,16 @@ def _coerce(x, device):
     return m
 
 
-def _newton_schulz_entry(qhat, ws):
+def _newton_schulz_entry(qhat, ws, prod):
     """newton_schulz_step (orthogonal.py:153-169): guard ||Q^||_2 < sqrt(3)
-    by lp power iteration, G = Q^H Q (hp), S = 3I - G, Q = Q^ S / 2 (hp)."""
+    by lp power iteration, then Q = Q^ (3I - Q^H Q^) / 2 in hp."""
     n = ws.n
     _lib.call("sr_downcast_c64", n, n, qhat.re_ptr(), qhat.im_ptr(), qhat.ld, ws.y_lp.data_ptr(),
               ws.y_lp.shape[1], _stream())
     est = spectral_norm_estimate(ws.y_lp, n)
     if not est < math.sqrt(3.0):
         raise NormTooLarge("spectral norm estimate %.6f is not below sqrt(3)" % est)
-    g = matmul_hp(qhat, qhat, trans_a=True, out=ws.y)
-    _lib.call("sr_sigma_ns_f64", n, g.re_ptr(), g.im_ptr(), g.ld, ws.sigma.re_ptr(), ws.sigma.im_ptr(),
-              ws.sigma.ld, _stream())
-    matmul_hp(qhat, ws.sigma, alpha=0.5, out=ws.q)
-
-
-def _merged_update(ws, restore_full_sigma):
-    """merged_update (orthogonal.py:172-201): YW, W^2, W^3 in lp, Sigma in hp
-    left to right, Q_new = (Q Sigma) / 2 in hp."""
-    n = ws.n
-    _lib.call("sr_downcast_c64", n, n, ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld, ws.y_lp.data_ptr(),
-              ws.y_lp.shape[1], _stream())
-    matmul_lp(ws.y_lp, ws.w_lp, n, n, n, out=ws.yw)
-    matmul_lp(ws.w_lp, ws.w_lp, n, n, n, out=ws.w2)
-    matmul_lp(ws.w2, ws.w_lp, n, n, n, out=ws.w3)
-    w2y = w2yw = None
-    if restore_full_sigma:
-        if ws.w2y is None:
-            ws.w2y = lp_empty(n, device=ws.w_lp.device)
-            ws.w2yw = lp_empty(n, device=ws.w_lp.device)
-        matmul_lp(ws.w2, ws.y_lp, n, n, n, out=ws.w2y)
-        matmul_lp(ws.w2y, ws.w_lp, n, n, n, out=ws.w2yw)
-        w2y, w2yw = ws.w2y.data_ptr(), ws.w2yw.data_ptr()
-    _lib.call("sr_sigma_merged_f64", n, ws.w_lp.data_ptr(), ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld,
-              ws.yw.data_ptr(), ws.w2.data_ptr(), ws.w3.data_ptr(), w2y, w2yw, ws.w_lp.shape[1],
-              ws.sigma.re_ptr(), ws.sigma.im_ptr(), ws.sigma.ld, _stream())
-    matmul_hp(ws.q, ws.sigma, alpha=0.5, out=ws.q_next)
-    ws.q, ws.q_next = ws.q_next, ws.q
-
+    prod.entry(qhat)
 
 
 def _phase_permutation(q):
@@ -237,7 +214,10 @@ def _run_fp64(a, qhat, cfg, ws):
     n = a.rows
     st = _stream()
     hp0 = _counters["hp_calls"]
-    _newton_schulz_entry(qhat, ws)
+    prod = products.make(cfg.gemm, ws, a)
+    if cfg.restore_full_sigma:
+        products.ensure_full_sigma_buffers(ws)
+    _newton_schulz_entry(qhat, ws, prod)
     _lib.call("sr_fro_norm_f64", n, n, a.re_ptr(), a.im_ptr(), a.ld, ws.ptr(0), ws.red[0].data_ptr(),
               ws.red[0].numel(), st)
     history = []
@@ -262,11 +242,9 @@ def _run_fp64(a, qhat, cfg, ws):
     tol = None
     for it in range(1, cfg.max_iters + 1):
         # T^ = (Q^H A) Q; split + lp downcast + ||E||; Y = Q^H Q - I; ||Y||
-        matmul_hp(ws.q, a, trans_a=True, out=ws.p)
-        matmul_hp(ws.p, ws.q, out=ws.that)
+        prod.measure(a)
         _lib.call("sr_split_lp_c64", n, ws.that.re_ptr(), ws.that.im_ptr(), ws.that.ld, ws.t_lp.data_ptr(),
                   ws.e_lp.data_ptr(), ws.t_lp.shape[1], ws.ptr(1), ws.red[1].data_ptr(), ws.red[1].numel(), st)
-        matmul_hp(ws.q, ws.q, trans_a=True, diag_shift=-1.0, out=ws.y)
         _lib.call("sr_fro_norm_f64", n, n, ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld, ws.ptr(2),
                   ws.red[2].data_ptr(), ws.red[2].numel(), st)
         s = ws.scal[:3].cpu()  # sync 1
@@ -305,7 +283,7 @@ def _run_fp64(a, qhat, cfg, ws):
         skip = (converged and cfg.skip_final_ortho and norm_y <= 10.0 * n * U_FP64
                 and norm_w <= math.sqrt(U_FP64))
         if not skip:
-            _merged_update(ws, cfg.restore_full_sigma)
+            prod.update(cfg.restore_full_sigma)
         if converged:
             status, iterations, skip_fired = RefineStatus.CONVERGED, it, skip
             break

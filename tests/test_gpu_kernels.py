@@ -164,5 +164,5 @@ def test_sigma_merged_matches_numpy():
     s = ZPlanar.empty(n)
     _lib.call("sr_sigma_merged_f64", n, wd.data_ptr(), yz.re_ptr(), yz.im_ptr(), yz.ld, ywd.data_ptr(),
               w2d.data_ptr(), w3d.data_ptr(), None, None, wd.shape[1], s.re_ptr(), s.im_ptr(), s.ld,
-              torch.cuda.current_stream().cuda_stream)
+              1, torch.cuda.current_stream().cuda_stream)
     assert np.array_equal(s.to_numpy(), ref)

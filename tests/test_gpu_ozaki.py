@@ -1,0 +1,141 @@
+"""GPU parity of the Ozaki-II int8 tensor-core products.
+
+1. The tcgen05 modular GEMM is checked bit-exactly against numpy integer
+   arithmetic (integer work: the bar is bit-exact).
+2. The emulated FP64 products are checked against an exact double-double
+   evaluation (oracle/ddgemm_oracle.c, the reference's gemm_hp restated): the
+   Ozaki result must be at least as accurate as numpy's FP64 BLAS product.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import clib
+from paper_2203_10879_b200 import ZPlanar, _lib, ozaki
+from paper_2203_10879_b200.matrix import lp_empty
+
+pytestmark = pytest.mark.gpu
+
+
+def sym_residues(rng, shape, p):
+    lo, hi = -(p // 2), (p + 1) // 2 - 1
+    return rng.integers(lo, hi + 1, size=shape).astype(np.int8)
+
+
+def sym_mod(x, p):
+    r = np.mod(x, p)
+    hi = (p + 1) // 2 - 1
+    return np.where(r > hi, r - p, r)
+
+
+@pytest.mark.parametrize("M,N,K,cplx", [(128, 128, 64, True), (200, 130, 100, True), (256, 384, 512, True),
+                                        (77, 300, 1000, False), (129, 129, 129, True)])
+def test_oz_gemm_residues_bit_exact(M, N, K, cplx):
+    rng = np.random.default_rng(M + N + K)
+    moduli = [256, 255, 253]
+    kp = ozaki.kpitch(K)
+    bp = 3 if cplx else 1
+    a = np.zeros((len(moduli), 2, M, kp), np.int8)
+    b = np.zeros((len(moduli), bp, N, kp), np.int8)
+    for l, p in enumerate(moduli):
+        a[l, :, :, :K] = sym_residues(rng, (2, M, K), p)
+        if cplx:
+            re = sym_residues(rng, (N, K), p)
+            im = sym_residues(rng, (N, K), p)
+            b[l, 0, :, :K] = sym_mod(-im.astype(np.int64), p)
+            b[l, 1, :, :K] = re
+            b[l, 2, :, :K] = im
+        else:
+            b[l, 0, :, :K] = sym_residues(rng, (N, K), p)
+    ad, bd = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    pitch = ozaki.kpitch(N)
+    out = torch.zeros((len(moduli), 2, M, pitch), dtype=torch.int8, device="cuda")
+    mods = np.array(moduli, np.int32)
+    _lib.call("sr_oz_gemm_i8", M, N, K, len(moduli), mods.ctypes.data, ad.data_ptr(), 2, kp, bd.data_ptr(), bp,
+              kp, out.data_ptr(), pitch, 0, torch.cuda.current_stream().cuda_stream)
+    got = out.cpu().numpy()[:, :, :, :N].astype(np.int64)
+    for l, p in enumerate(moduli):
+        ar, ai = a[l, 0].astype(np.int64), a[l, 1].astype(np.int64)
+        if cplx:
+            br, bi = b[l, 1].astype(np.int64), b[l, 2].astype(np.int64)
+            cre = ar @ br.T - ai @ bi.T
+            cim = ar @ bi.T + ai @ br.T
+        else:
+            br = b[l, 0].astype(np.int64)
+            cre, cim = ar @ br.T, ai @ br.T
+        assert np.array_equal(got[l, 0], sym_mod(cre, p)), (l, p)
+        assert np.array_equal(got[l, 1], sym_mod(cim, p)), (l, p)
+
+
+def dd_exact(a, b):
+    z = np.zeros(a.shape)
+    pa = (np.ascontiguousarray(a.real), z, np.ascontiguousarray(a.imag), z.copy())
+    z = np.zeros(b.shape)
+    pb = (np.ascontiguousarray(b.real), z, np.ascontiguousarray(np.imag(b)), z.copy())
+    o = clib.gemm_dd(pa, pb)
+    return (o[0] + o[1]) + 1j * (o[2] + o[3]), o
+
+
+def oz_product(x, y, trans=False, alpha=1.0, shift=0.0, beta=ozaki.HP_BETA):
+    xm, ym = ZPlanar.from_any(x), ZPlanar.from_any(y)
+    K = x.shape[0] if trans else x.shape[1]
+    M = x.shape[1] if trans else x.shape[0]
+    N = y.shape[1]
+    pl = ozaki.plan(K, beta, beta)
+    ea = ozaki.encode(xm, x.shape[0], x.shape[1], "a", pl, conj_t=trans)
+    eb = ozaki.encode(ym, y.shape[0], y.shape[1], "b", pl)
+    res = ozaki.ResidueBuffer(M, N, pl.nmod, "cuda")
+    ozaki.gemm_residues(ea, eb, pl, res)
+    out = ZPlanar.empty(M, N)
+    ozaki.decode(res, ea, eb, pl, out, alpha=alpha, shift=shift)
+    return out.to_numpy()
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (64, 48, 40), (200, 130, 257), (256, 256, 256)])
+@pytest.mark.parametrize("trans", [False, True])
+@pytest.mark.parametrize("b_real", [False, True])
+def test_oz_fp64_product_beats_blas(M, N, K, trans, b_real):
+    rng = np.random.default_rng(M * 7 + N + K)
+    x = rng.standard_normal((K, M) if trans else (M, K)) + 1j * rng.standard_normal((K, M) if trans else (M, K))
+    y = rng.standard_normal((K, N))
+    if not b_real:
+        y = y + 1j * rng.standard_normal((K, N))
+    xo = x.conj().T if trans else x
+    exact, _ = dd_exact(xo, y)
+    got = oz_product(x, y, trans=trans)
+    blas = xo @ y
+    e_oz = np.linalg.norm(got - exact)
+    e_blas = np.linalg.norm(blas - exact)
+    scale = np.linalg.norm(exact)
+    assert e_oz <= max(2 * e_blas, 4 * 2.0 ** -53 * scale), (e_oz / scale, e_blas / scale)
+
+
+def test_oz_gram_minus_identity_is_accurate():
+    rng = np.random.default_rng(3)
+    n = 200
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    _, o = dd_exact(q.conj().T, q)
+    exact = (o[0] - np.eye(n)) + o[1] + 1j * (o[2] + o[3])
+    got = oz_product(q, q, trans=True, shift=-1.0)
+    blas = q.conj().T @ q - np.eye(n)
+    assert np.linalg.norm(got - exact) <= np.linalg.norm(blas - exact)
+
+
+def test_oz_lp_product_complex64():
+    rng = np.random.default_rng(9)
+    n = 300
+    w = ((rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) * 1e-3).astype(np.complex64)
+    wd = lp_empty(n)
+    wd[:, :n] = torch.from_numpy(w)
+    pl = ozaki.plan(n, ozaki.LP_BETA, ozaki.LP_BETA)
+    ea = ozaki.encode(wd, n, n, "a", pl)
+    eb = ozaki.encode(wd, n, n, "b", pl)
+    res = ozaki.ResidueBuffer(n, n, pl.nmod, "cuda")
+    ozaki.gemm_residues(ea, eb, pl, res)
+    out = lp_empty(n)
+    ozaki.decode(res, ea, eb, pl, out)
+    ref = w.astype(np.complex128) @ w.astype(np.complex128)
+    got = out[:, :n].cpu().numpy()
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    f32 = np.linalg.norm((w @ w) - ref) / np.linalg.norm(ref)
+    assert err <= max(2 * f32, 1e-7), (err, f32)

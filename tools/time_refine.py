@@ -29,17 +29,43 @@ for trans, bb, flops, name in ((False, b, 8, "NN"), (True, b, 8, "CN"), (True, b
     ms = e0.elapsed_time(e1) / reps
     print("zgemm %s n=%d: %.3f ms  %.2f TFLOP/s" % (name, n, ms, flops * n ** 3 / ms / 1e9), flush=True)
 
+from paper_2203_10879_b200 import ozaki  # noqa: E402
+for beta, tag in ((ozaki.HP_BETA, "hp"), (ozaki.LP_BETA, "lp")):
+    pl = ozaki.plan(n, beta, beta)
+    res = ozaki.ResidueBuffer(n, n, pl.nmod, "cuda")
+    ea = ozaki.encode(a, n, n, "a", pl, conj_t=True)
+    eb = ozaki.encode(b, n, n, "b", pl)
+    out = ZPlanar.empty(n)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    for rep in range(3):
+        ev[0].record()
+        ozaki.encode(a, n, n, "a", pl, conj_t=True, out=ea)
+        ev[1].record()
+        ozaki.encode(b, n, n, "b", pl, out=eb)
+        ev[2].record()
+        ozaki.gemm_residues(ea, eb, pl, res)
+        ev[3].record()
+        ozaki.decode(res, ea, eb, pl, out)
+        ev[4].record()
+        torch.cuda.synchronize()
+    t = [ev[i].elapsed_time(ev[i + 1]) for i in range(4)]
+    g_ops = 2.0 * 4 * pl.nmod * n ** 3
+    print("ozaki %s n=%d nmod=%d: encA %.3f encB %.3f gemm %.3f ms (%.0f TOP/s int8, %.1f TF/s fp64-equiv) "
+          "decode %.3f ms; total %.3f ms" % (tag, n, pl.nmod, t[0], t[1], t[2], g_ops / t[2] / 1e9,
+                                            8 * n ** 3 / t[2] / 1e9, t[3], sum(t)), flush=True)
+
 if n <= 4096:
     A = inputs.gaussian_complex(n, 0)
     Q = inputs.schur_vectors(A).astype(np.complex128)
-    cfg = RefineConfig(precision="fp64", tol_factor=10.0 / n, max_iters=10)
-    for rep in range(3):
+    for gemm in ("ozaki", "dmma"):
+      cfg = RefineConfig(precision="fp64", tol_factor=10.0 / n, max_iters=10, gemm=gemm)
+      for rep in range(3):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         pair, r = refine_template(A, Q, cfg)
         torch.cuda.synchronize()
-        print("refine n=%d: %.3f s  status %s it %d hist %s" % (
-            n, time.perf_counter() - t0, r.status.value, r.iterations,
+        print("refine[%s] n=%d: %.3f s  status %s it %d hist %s" % (
+            gemm, n, time.perf_counter() - t0, r.status.value, r.iterations,
             ["%.2e" % (h[0] / np.linalg.norm(A)) for h in r.residual_history]), flush=True)
 
 # Q^ generation options at large n (setup only): LAPACK cgees vs GPU eig + QR

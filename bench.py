@@ -1,0 +1,287 @@
+#!/usr/bin/env python
+"""Benchmark: time-to-refine of BASELINE config 3 on the B200.
+
+Workload (BASELINE.json configs[2], the config the metric is quoted on):
+n = 8192 real float64 Gaussian A (N(0,1), Philox seed 0), Q̂ = complex
+Schur vectors of A cast to complex64 (LAPACK cgees, cached under
+$SR_DATA_DIR), FP32 -> FP64 refinement (hp = FP64 via Ozaki-II on the int8
+tensor cores, lp = complex64) until ||stril(Q^H A Q)||_F / ||A||_F <= 10 u64
+(tol_factor = 10 / n) or 10 iterations.  One step = one refine_template
+call with A and Q̂ resident in HBM (value); `e2e` repeats it through the
+public API from pinned host numpy-backed tensors, with the host->device
+copies of A, Q̂ and the device->host copies of Q, T inside the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 (torchrun, one rank per GPU): every rank refines its own replica
+(seed = rank) — "replicas"; the time is the max over
+ranks.  --impl reference times the CPU oracle port of the reference loop
+(oracle/refine_fp64.py: numpy BLAS + the C restatement of the reference
+solver) on a bounded sample of the same workload, on rank 0 only.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "time-to-refine (s), n=8192 complex FP32->FP64 (config 3)"
+U64 = 2.0 ** -53
+SAMPLE_N = 1024  # CPU sample size (same workload family, O(n^3) extrapolated)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--gemm", default="ozaki", choices=["ozaki", "dmma"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def workload(n, seed):
+    from paper_2203_10879_b200 import inputs
+    a = inputs.gaussian_real(n, seed)
+    t0 = time.time()
+    q = inputs.cached_qhat("c3_n%d_s%d" % (n, seed), a)
+    log("[bench] Q^ (complex64 Schur of A, n=%d) ready in %.1f s" % (n, time.time() - t0))
+    return a, q
+
+
+def cpu_oracle_sample(steps, n_full):
+    """Time the oracle port on SAMPLE_N real-Gaussian config-3-type inputs;
+    returns list of extrapolated seconds (x (n_full / SAMPLE_N)^3)."""
+    from oracle.refine_fp64 import refine_template_fp64
+    from paper_2203_10879_b200 import inputs
+    a = inputs.gaussian_real(SAMPLE_N, 0)
+    q = inputs.cached_qhat("c3_n%d_s0" % SAMPLE_N, a).astype(np.complex128)
+    scale = (n_full / SAMPLE_N) ** 3
+    vals = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        out = refine_template_fp64(a, q, tol_factor=10.0 / SAMPLE_N, max_iters=10)
+        vals.append((time.perf_counter() - t0) * scale)
+    return vals, out
+
+
+def cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    n = args.n
+    vals, out = cpu_oracle_sample(args.warmup, n)
+    vals, out = cpu_oracle_sample(args.steps, n)
+    v = float(np.median(vals))
+    sample = ("oracle port (oracle/refine_fp64.py: numpy/OpenBLAS hp, C restatement of trisolve.py lp) "
+              "full refine at n=%d on the config-3 workload family, %d iterations, scaled by (n/%d)^3"
+              % (SAMPLE_N, out["iterations"], SAMPLE_N))
+    line = {"metric": METRIC, "value": v, "unit": "s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1000.0, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config3: n=%d real Gaussian A, complex64-Schur start, FP32->FP64, "
+                                   "stop relE<10u64 or 10 iters" % n, "n": n},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": cores(), "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+class ClockSampler:
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), "--query-gpu=" + q, "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) < 9:
+                continue
+            for k, nm in enumerate(names):
+                if r[5 + k].strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2203_10879_b200 import RefineConfig, ZPlanar, _lib, ozaki, refine_template
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n = args.n
+    a_np, q_np = workload(n, seed=rank)
+    A = ZPlanar.from_any(a_np, device=dev)
+    Qh = ZPlanar.from_any(q_np.astype(np.complex128), device=dev)
+    cfg = RefineConfig(precision="fp64", tol_factor=10.0 / n, max_iters=10, gemm=args.gemm)
+    lib = _lib.load()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 0)):
+        pair, rep = refine_template(A, Qh, cfg, device=dev)
+    barrier()
+    # ---- timed region: K refinements, inputs resident in HBM (A 512 MB + Q^ 1 GB > 126 MB L2)
+    sampler = ClockSampler(local)
+    ozaki.timing_begin()
+    launches0 = lib.sr_kernel_launches()
+    st = torch.cuda.current_stream()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    reports = []
+    barrier()
+    evs[0].record(st)
+    for k in range(args.steps):
+        pair, rep = refine_template(A, Qh, cfg, device=dev)
+        evs[k + 1].record(st)
+        reports.append(rep)
+    barrier()
+    launches = lib.sr_kernel_launches() - launches0
+    gemm_ms, gemm_ops, gemm_launches = ozaki.timing_end()
+    clocks = sampler.stop()
+    step_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
+    total_ms = evs[0].elapsed_time(evs[-1])
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    rep = reports[-1]
+    # ---- e2e through the public API from pinned host memory
+    a_host = torch.from_numpy(a_np).pin_memory()
+    q_host = torch.from_numpy(q_np.astype(np.complex128)).pin_memory()
+    q_out = torch.empty((n, n), dtype=torch.complex128).pin_memory()
+    t_out = torch.empty((n, n), dtype=torch.complex128).pin_memory()
+    e2e = []
+    for _ in range(max(1, min(args.steps, 3))):
+        barrier()
+        t0 = time.perf_counter()
+        pair, _r = refine_template(a_host, q_host, cfg, device=dev)
+        q_out.copy_(pair.q, non_blocking=True)
+        t_out.copy_(pair.t, non_blocking=True)
+        torch.cuda.synchronize()
+        e2e.append(time.perf_counter() - t0)
+    e2e_v = float(np.median(e2e))
+    if world > 1:
+        t = torch.tensor([e2e_v], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_v = float(t.item())
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    # ---- parity of the measured run (FP64 evaluator on the device)
+    hist = rep.residual_history
+    norm_a = float(np.linalg.norm(a_np))
+    # ---- roofline of the dominant kernel (modular int8 GEMM on tcgen05)
+    peaks = measured_peaks()
+    bf16 = peaks.get("bf16_tflops_sustained")
+    if bf16:
+        int8_peak, peak_src = 2.0 * bf16, "2 x measured sustained bf16 (MEASURED_PEAKS.json; int8 dense = 2x bf16)"
+    else:
+        int8_peak, peak_src = 2.0 * 1400.0, "fallback 2 x 1.4 PF sustained bf16 (B200_PROFILING.md)"
+    achieved = gemm_ops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    # FP64-equivalent hp flops: entry 16n^3, 28n^3 per iteration (real A), -8n^3 if skipped
+    k_it = rep.iterations
+    f_hp = 16 * n ** 3 + k_it * 28 * n ** 3 - (8 * n ** 3 if rep.skip_fired else 0)
+    fp64_peak = peaks.get("fp64_tflops")
+    line = {
+        "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Philox Gaussian A; LAPACK complex64 Schur start)",
+        "config": {"workload": "config3: n=%d real Gaussian A, complex64-Schur start, FP32->FP64, stop "
+                               "relE<10u64 or 10 iters" % n, "n": n, "gemm": args.gemm,
+                   "parallelism": "replicas x%d" % world if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (A 512 MiB, Q 1 GiB)"},
+        "result": {"status": rep.status.value, "iterations": k_it, "skip_fired": rep.skip_fired,
+                   "final_relE": hist[-1][0] / norm_a, "final_ortho": hist[-1][1],
+                   "hp_matmul_count": rep.hp_matmul_count, "step_ms": step_ms},
+        "roofline": {"bound": "tensor", "kernel": "oz_gemm_kernel (tcgen05 kind::i8)",
+                     "achieved": achieved, "peak": int8_peak, "unit": "TOP/s (int8)",
+                     "frac": (achieved / int8_peak) if achieved else None, "traffic": None,
+                     "launches": gemm_launches, "avg_launch_ms": gemm_ms / max(gemm_launches, 1),
+                     "share_of_step": gemm_ms / total_ms if total_ms else None, "peak_source": peak_src,
+                     "algorithmic_ops_per_launch": gemm_ops / max(gemm_launches, 1)},
+        "fp64_equivalent": {"hp_flops_per_refine": f_hp, "tflops": f_hp / (ms_per_step / 1e3) / 1e12,
+                            "fp64_peak_tflops": fp64_peak or 37.0,
+                            "fp64_peak_source": "MEASURED_PEAKS.json" if fp64_peak else
+                            "DMMA/DFMA microbenchmark on this pool's B200 (tools/ubench_fp64.cu): 37.0",
+                            "note": "algorithmic FP64 flops of the hp products over the whole time-to-refine"},
+        "clocks": clocks,
+        "gpu_launches": int(launches),
+        "e2e": {"value": e2e_v, "unit": "s", "h2d_bytes_per_step": int(a_host.numel() * 8 + q_host.numel() * 16),
+                "d2h_bytes_per_step": int(q_out.numel() * 16 + t_out.numel() * 16)},
+    }
+    if not args.no_cpu_baseline:
+        vals, out = cpu_oracle_sample(2, n)
+        line["cpu_baseline"] = {"value": float(np.median(vals)), "unit": "s", "cores": cores(), "kind": "port",
+                                "sample": "oracle port full refine at n=%d (config-3 workload family, %d "
+                                          "iterations), O(n^3)-scaled to n=%d" % (SAMPLE_N, out["iterations"], n)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

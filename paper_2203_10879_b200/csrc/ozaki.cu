@@ -90,14 +90,14 @@ __global__ void exps_transposed_kernel(int rows, int cols, const double* __restr
   }
 }
 
-// symmetric residue of an exact integer a (|a| < 2^62) modulo p in [-floor(p/2), ceil(p/2)-1]
-__device__ __forceinline__ int res_i64(long long a, int p, double inv) {
-  long long q = __double2ll_rn((double)a * inv);
-  long long r = a - q * (long long)p;
-  const int lo = -(p >> 1), hi = ((p + 1) >> 1) - 1;
-  while (r > hi) r -= p;
-  while (r < lo) r += p;
-  return (int)r;
+// Symmetric residue of an integer-valued double a (|a| < 2^62) modulo p, in
+// [-floor(p/2), ceil(p/2) - 1].  Two exact fma reductions: the first quotient
+// estimate is within a few units, the second reduction is then exact.
+__device__ __forceinline__ double res_f64(double a, double p, double inv, double hi) {
+  double r = fma(-rint(a * inv), p, a);  // exact, |r| < 8p
+  r = fma(-rint(r * inv), p, r);         // exact, |r| <= p/2
+  if (r > hi) r -= p;
+  return r;
 }
 
 // ---- encode: residue planes [nmod][planes][rows_out][kpitch] -------------------
@@ -137,24 +137,25 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
     const int i = i0 + il, k = k0 + kl;
     if (i >= p.rows_out || k >= p.K) continue;
     const int sh = p.beta - exps[i];
-    long long ar[4], ai[4];
+    double ar[4], ai[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       double xr = s_re[il][kl + e], xi = s_im[il][kl + e];
       if (p.conj) xi = -xi;
-      ar[e] = __double2ll_rn(ldexp(xr, sh));
-      ai[e] = __double2ll_rn(ldexp(xi, sh));
+      ar[e] = rint(ldexp(xr, sh));  // exact integers (|.| <= 2^beta)
+      ai[e] = rint(ldexp(xi, sh));
     }
     int8_t* dst = out + (size_t)i * p.kpitch + k;
     for (int l = 0; l < p.nmod; ++l) {
-      const int pm = p.moduli[l];
-      const double inv = p.inv[l];
+      const double pm = (double)p.moduli[l], inv = p.inv[l];
+      const double hi = (double)(((p.moduli[l] + 1) >> 1) - 1);
       uint32_t wr = 0, wi = 0, wn = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        int rr = res_i64(ar[e], pm, inv);
-        int ri = res_i64(ai[e], pm, inv);
-        int rn = res_i64(-ai[e], pm, inv);
+        const int rr = (int)res_f64(ar[e], pm, inv, hi);
+        const int ri = (int)res_f64(ai[e], pm, inv, hi);
+        int rn = -ri;
+        if (rn > (int)hi) rn -= p.moduli[l];
         wr |= (uint32_t)(rr & 0xFF) << (8 * e);
         wi |= (uint32_t)(ri & 0xFF) << (8 * e);
         wn |= (uint32_t)(rn & 0xFF) << (8 * e);
@@ -198,16 +199,9 @@ __device__ __forceinline__ void dd_add_d(double& hi, double& lo, double b) {
   lo = e - (hi - s);
 }
 
-// value of the CRT representative of residues x[0..nmod) as a double-double
-__device__ __forceinline__ void crt_value(const DecodeParams& p, const int* x, double& hi, double& lo) {
-  double S[MAXCHUNK];
-#pragma unroll
-  for (int j = 0; j < MAXCHUNK; ++j) S[j] = 0.0;
-  for (int l = 0; l < p.nmod; ++l) {
-    const double xl = (double)x[l];
-#pragma unroll
-    for (int j = 0; j < MAXCHUNK; ++j) S[j] = fma(xl, p.w[l][j], S[j]);  // exact: < 2^52
-  }
+// CRT finish: S[j] = sum_l x_l w_lj (exact chunk sums) -> double-double value
+__device__ __forceinline__ void crt_finish(const DecodeParams& p, const double (&S)[MAXCHUNK], double& hi,
+                                           double& lo) {
   double approx = ldexp(S[0], p.off[0]);
   if (p.nchunk > 1) approx += ldexp(S[1], p.off[1]);
   const double k = rint(approx * p.inv_p);
@@ -221,38 +215,64 @@ __device__ __forceinline__ void crt_value(const DecodeParams& p, const int* x, d
   }
 }
 
+// one thread: row i, columns j0..j0+3, both planes
 __global__ void __launch_bounds__(256) decode_kernel(const __grid_constant__ DecodeParams p,
                                                      const int8_t* __restrict__ res, const int* __restrict__ ea,
                                                      const int* __restrict__ eb, const double* __restrict__ add_re,
                                                      const double* __restrict__ add_im, void* __restrict__ out_re,
                                                      double* __restrict__ out_im) {
-  const long long total = (long long)p.M * p.N;
+  const int ngrp = (p.N + 3) >> 2;
+  const long long total = (long long)p.M * ngrp;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(idx / p.N), j = (int)(idx % p.N);
-    const int sc = -((p.beta_a - ea[i]) + (p.beta_b - eb[j]));
-    double v[2];
-#pragma unroll
+    const int i = (int)(idx / ngrp), j0 = (int)(idx % ngrp) * 4;
+    const int rho = p.beta_a - ea[i];
+#pragma unroll 1
     for (int plane = 0; plane < 2; ++plane) {
-      int x[MAXMOD];
-      const int8_t* r = res + (size_t)plane * p.res_plane + (size_t)i * p.res_pitch + j;
-      for (int l = 0; l < p.nmod; ++l) x[l] = r[(size_t)l * p.res_mod];
-      double hi, lo;
-      crt_value(p, x, hi, lo);
-      hi = ldexp(hi, sc) * p.alpha;
-      lo = ldexp(lo, sc) * p.alpha;
-      if (plane == 0 && i == j && p.shift != 0.0) dd_add_d(hi, lo, p.shift);
-      if (p.has_add) {
-        const double a = plane == 0 ? add_re[(size_t)i * p.ld_add + j] : add_im[(size_t)i * p.ld_add + j];
-        dd_add_d(hi, lo, p.add_scale * a);
+      double S[4][MAXCHUNK];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int j = 0; j < MAXCHUNK; ++j) S[e][j] = 0.0;
+      const int8_t* r = res + (size_t)plane * p.res_plane + (size_t)i * p.res_pitch + j0;
+#pragma unroll 4
+      for (int l = 0; l < p.nmod; ++l) {
+        // int8 -> double without I2F: the byte with its sign bit flipped is
+        // x + 128 in [0, 255]; as the low word of 0x4338000000000000 it reads
+        // 1.5 * 2^52 + x + 128, so one DADD recovers x exactly.
+        const uint32_t w4 = *reinterpret_cast<const uint32_t*>(r + (size_t)l * p.res_mod) ^ 0x80808080u;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double x = __hiloint2double(0x43380000, (w4 >> (8 * e)) & 0xFF) - 6755399441055872.0;
+#pragma unroll
+          for (int j = 0; j < MAXCHUNK; ++j) S[e][j] = fma(x, p.w[l][j], S[e][j]);  // exact: < 2^52
+        }
       }
-      v[plane] = hi + lo;
-    }
-    if (p.out_kind == 0) {
-      ((double*)out_re)[(size_t)i * p.ld_out + j] = v[0];
-      out_im[(size_t)i * p.ld_out + j] = v[1];
-    } else {
-      ((float2*)out_re)[(size_t)i * p.ld_out + j] = make_float2((float)v[0], (float)v[1]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = j0 + e;
+        if (j >= p.N) break;
+        double hi, lo;
+        crt_finish(p, S[e], hi, lo);
+        const int sc = -(rho + (p.beta_b - eb[j]));
+        hi = ldexp(hi, sc) * p.alpha;
+        lo = ldexp(lo, sc) * p.alpha;
+        if (plane == 0 && i == j && p.shift != 0.0) dd_add_d(hi, lo, p.shift);
+        if (p.has_add) {
+          const double av = plane == 0 ? add_re[(size_t)i * p.ld_add + j] : add_im[(size_t)i * p.ld_add + j];
+          dd_add_d(hi, lo, p.add_scale * av);
+        }
+        const double v = hi + lo;
+        if (p.out_kind == 0) {
+          if (plane == 0)
+            ((double*)out_re)[(size_t)i * p.ld_out + j] = v;
+          else
+            out_im[(size_t)i * p.ld_out + j] = v;
+        } else {
+          float* o = reinterpret_cast<float*>(out_re) + 2 * ((size_t)i * p.ld_out + j);
+          o[plane] = (float)v;
+        }
+      }
     }
   }
 }
@@ -341,7 +361,8 @@ extern "C" int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* ta
     p.off[j] = (int)table[nmod * MAXCHUNK + MAXCHUNK + j];
   }
   p.inv_p = table[nmod * MAXCHUNK + 2 * MAXCHUNK];
-  const long long total = (long long)M * N;
+  if (res_pitch & 3) return SR_EINVAL;
+  const long long total = (long long)M * ((N + 3) / 4);
   int grid = (int)((total + 255) / 256);
   if (grid > 148 * 16) grid = 148 * 16;
   decode_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(p, (const int8_t*)res, exps_a, exps_b, add_re, add_im,

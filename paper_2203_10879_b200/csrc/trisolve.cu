@@ -6,22 +6,28 @@
 //   _sylvester_tri        trisolve.py:164-196
 //   _scalar_solve_inplace trisolve.py:121-145
 //   _check_separation     trisolve.py:104-113
-// with a blocked wavefront over NB x NB tiles of L.  Tile (I, J), I >= J,
-// satisfies
-//   T_II L_IJ - L_IJ T_JJ = -E_IJ - sum_{K>I} T_IK L_KJ + sum_{K<J} L_IK T_KJ
-// (stril() of both sides when I == J).  Every tile on the anti-diagonal
-// level (N-1-I) + J depends only on lower levels, so the sweep is N
-// level-synchronous launches.  Inside a launch each tile first forms the
-// right-hand side as two skinny products (the off-diagonal updates, split
-// over several CTAs when a level has few tiles and reduced in fixed split
-// order — deterministic), then one CTA solves the small tile equation by an
-// in-tile wavefront: entry (i, j) is finalised at step (NB-1-i) + j, and
-// every still-open entry of the CTA folds in the two entries finalised at
-// that step (one per row / column neighbour), so a step costs two complex
-// FMAs per entry and one barrier.  Clipping is applied at finalisation, as
-// in the reference (trisolve.py:141-144,192-195): dependent entries see the
-// clipped zero.  Any dependency-respecting order yields the same L up to
-// rounding.
+// with a right-looking blocked wavefront over NB x NB tiles of L.  Tile
+// (I, J), I >= J, satisfies
+//   T_II L_IJ - L_IJ T_JJ = R_IJ,
+//   R_IJ = -E_IJ - sum_{K>I} T_IK L_KJ + sum_{K<J} L_IK T_KJ
+// (stril() of both sides when I == J).  Tile (I, J) sits on anti-diagonal
+// level (N-1-I) + J and depends only on lower levels.  Launch `lev` of the
+// sweep owns every still-open tile that the tiles solved at level lev-1
+// contribute to — at most one column term (T_IK L_KJ) and one row term
+// (L_IJ T_JM) per tile, so each tile is updated by exactly one CTA and the
+// running right-hand side R lives in HBM with no atomics — and the CTAs whose
+// tile sits on level `lev` then solve it.  N launches per solve, each fully
+// parallel over the open tiles.
+//
+// The tile solve is one warp: lane i owns row i, and entry (i, j) is final at
+// step (NB-1-i) + j.  Each lane keeps its open entries in a 32-wide register
+// window that slides one column per step (fully unrolled, so the slide is
+// register renaming); at every step the lanes finalise one entry each,
+// exchange the new values with warp shuffles (the column terms) and fold
+// their own new value into their later columns (the row terms).  Clipping is
+// applied at finalisation as in the reference (trisolve.py:141-144,192-195),
+// so dependants see the clipped zero; any dependency-respecting order gives
+// the same L up to rounding.
 //
 // Templated on the lp type: float2 (FP64 mode, lp = complex64) and double2
 // (dd mode, lp = binary64 complex).
@@ -30,7 +36,8 @@
 namespace {
 
 constexpr int NB = 32;
-constexpr int NT = 256;  // 16 x 16 threads, each owning a 2 x 2 block of the tile
+constexpr int NT = 128;  // 16 x 8 threads, each owning a 2 x 4 block of the tile
+constexpr int LD = NB + 1;
 
 template <typename C>
 struct Real;
@@ -52,13 +59,23 @@ __device__ __forceinline__ C czero() {
 }
 template <typename C>
 __device__ __forceinline__ void cfma(C& acc, C a, C b) {  // acc += a * b
-  acc.x += a.x * b.x - a.y * b.y;
-  acc.y += a.x * b.y + a.y * b.x;
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
 }
 template <typename C>
 __device__ __forceinline__ void cfms(C& acc, C a, C b) {  // acc -= a * b
-  acc.x -= a.x * b.x - a.y * b.y;
-  acc.y -= a.x * b.y + a.y * b.x;
+  acc.x = fma(-a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(-a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+}
+__device__ __forceinline__ float2 shfl_down(float2 v, int d) {
+  return make_float2(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d));
+}
+__device__ __forceinline__ double2 shfl_down(double2 v, int d) {
+  return make_double2(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d));
 }
 
 // Load an NB x NB tile (rows r0.., cols c0..) with zero fill outside [0, n).
@@ -67,185 +84,234 @@ __device__ __forceinline__ void load_tile(C* s, const C* __restrict__ g, long lo
   for (int idx = threadIdx.x; idx < NB * NB; idx += NT) {
     int r = idx / NB, c = idx % NB;
     int gr = r0 + r, gc = c0 + c;
-    s[r * (NB + 1) + c] = (gr < n && gc < n) ? g[(size_t)gr * ld + gc] : czero<C>();
+    s[r * LD + c] = (gr < n && gc < n) ? g[(size_t)gr * ld + gc] : czero<C>();
   }
 }
 
-struct LevelArgs {
-  int n, N, level, splits;
+// Same, as asynchronous copies (cp.async, zero-filled outside [0, n)); the
+// caller commits and waits once for all the tiles it issued.
+template <typename C>
+__device__ __forceinline__ void load_tile_async(C* s, const C* __restrict__ g, long long ld, int r0, int c0,
+                                                int n) {
+  for (int idx = threadIdx.x; idx < NB * NB; idx += NT) {
+    const int r = idx / NB, c = idx % NB;
+    const int gr = r0 + r, gc = c0 + c;
+    const bool ok = gr < n && gc < n;
+    const C* src = g + (ok ? (size_t)gr * ld + gc : 0);
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s + r * LD + c);
+    if (sizeof(C) == 16)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
+    else
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0));
+  }
+}
+
+struct SweepArgs {
+  int n, N, lev, countA;
   long long ld;
 };
 
-// One launch per anti-diagonal level.  grid.x = tiles on the level
-// (J = 0..level), grid.y = splits of the update sum.
-template <typename C>
-__global__ void __launch_bounds__(NT) trisolve_level_kernel(LevelArgs p, const C* __restrict__ T,
-                                                            const C* __restrict__ E, C* __restrict__ L,
-                                                            C* __restrict__ ws, int* __restrict__ counters,
-                                                            typename Real<C>::T clip,
-                                                            unsigned long long* __restrict__ clipped) {
-  using R = typename Real<C>::T;
+// In-tile solve by one warp: T2 X - X T1 = R (strict lower part only when diag).
+template <typename C, bool DIAG>
+__device__ __forceinline__ void tile_solve_warp(const C* sT2, const C* sT1, const C* sR, C* sX, int valid_i,
+                                                int valid_j, typename Real<C>::T clip, unsigned int* s_clip) {
+  const int i = threadIdx.x & 31;
+  C pend[NB];
+  C tr[NB];
+#pragma unroll
+  for (int d = 0; d < NB; ++d) {
+    const int c = i - (NB - 1) + d;  // window at step 0 covers columns i-31 .. i
+    pend[d] = (c >= 0) ? sR[i * LD + c] : czero<C>();
+    tr[d] = (i + d < NB) ? sT2[i * LD + i + d] : czero<C>();
+  }
+  const C tii = tr[0];
+#pragma unroll
+  for (int t = 0; t < 2 * NB - 1; ++t) {
+    const int j = t - (NB - 1) + i;  // this lane's column at step t
+    const bool valid = (j >= 0) && (j < NB) && (i < valid_i) && (j < valid_j) && (!DIAG || i > j);
+    C x = czero<C>();
+    if (valid) {
+      const C tjj = sT1[j * LD + j];
+      C piv;
+      piv.x = tii.x - tjj.x;
+      piv.y = tii.y - tjj.y;
+      x = cdiv(pend[0], piv);
+      if (clip > 0 && sqrt(x.x * x.x + x.y * x.y) > clip) {
+        x = czero<C>();
+        if (threadIdx.x < 32) atomicAdd(s_clip, 1u);
+      }
+      sX[i * LD + j] = x;
+    }
+    // column terms: lane i+d finalised (i+d, j+d); it feeds this lane's (i, j+d)
+#pragma unroll
+    for (int d = 1; d < NB; ++d) {
+      const C xv = shfl_down(x, d);
+      if (i + d < NB) cfms(pend[d], tr[d], xv);
+    }
+    // row terms: (i, j) feeds this lane's (i, j+d) through T1[j][j+d]
+    if (valid) {
+#pragma unroll
+      for (int d = 1; d < NB; ++d)
+        if (j + d < NB) cfma(pend[d], x, sT1[j * LD + j + d]);
+    }
+    // slide the window one column to the right
+#pragma unroll
+    for (int d = 0; d < NB - 1; ++d) pend[d] = pend[d + 1];
+    {
+      const int c = t + i + 1;
+      pend[NB - 1] = (c < NB) ? sR[i * LD + c] : czero<C>();
+    }
+  }
+}
+
+// SOLVE = true: one CTA per tile on level `lev` (blockIdx.x = its column M):
+//   fold in the level-(lev-1) contributions, then solve the tile (critical path).
+// SOLVE = false: one CTA per open tile above level `lev` that level lev-1
+//   feeds: fold in the contributions, write R back (bulk work, runs on a
+//   second stream concurrently with the SOLVE launch of the same level).
+template <typename C, bool SOLVE>
+__global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs p, const C* __restrict__ T, C* __restrict__ R,
+                                                   C* __restrict__ L, typename Real<C>::T clip,
+                                                   unsigned long long* __restrict__ clipped) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* sA = reinterpret_cast<C*>(smem_raw);       // [NB][NB+1]
-  C* sB = sA + NB * (NB + 1);                   // [NB][NB+1]
-  __shared__ int s_last;
+  C* s0 = reinterpret_cast<C*>(smem_raw);  // 5 tiles of NB x LD
+  C* s1 = s0 + NB * LD;
+  C* s2 = s1 + NB * LD;
+  C* s3 = s2 + NB * LD;
+  C* s4 = s3 + NB * LD;
   __shared__ unsigned int s_clip;
-
-  const int J = blockIdx.x;
-  const int I = J + (p.N - 1 - p.level);
-  const int split = blockIdx.y;
-  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
-  const int n = p.n;
+  const int N = p.N, lev = p.lev, n = p.n;
   const long long ld = p.ld;
-
-  // ---- off-diagonal updates: col terms K = I+1..N-1 (sign -), row terms K = 0..J-1 (sign +)
-  const int ncol = p.N - 1 - I, nrow = J, nterms = ncol + nrow;
-  const int per = (nterms + p.splits - 1) / p.splits;
-  const int t0 = split * per, t1 = min(nterms, t0 + per);
-  C acc[2][2];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 2; ++b) acc[a][b] = czero<C>();
-
-  for (int term = t0; term < t1; ++term) {
-    bool colterm = term < ncol;
-    int K = colterm ? I + 1 + term : term - ncol;
-    __syncthreads();
-    if (colterm) {
-      load_tile(sA, T, ld, I * NB, K * NB, n);  // T_IK
-      load_tile(sB, L, ld, K * NB, J * NB, n);  // L_KJ
-    } else {
-      load_tile(sA, L, ld, I * NB, K * NB, n);  // L_IK
-      load_tile(sB, T, ld, K * NB, J * NB, n);  // T_KJ
-    }
-    __syncthreads();
-    C part[2][2];
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) part[a][b] = czero<C>();
-#pragma unroll 8
-    for (int k = 0; k < NB; ++k) {
-      C a0 = sA[(2 * ty) * (NB + 1) + k], a1 = sA[(2 * ty + 1) * (NB + 1) + k];
-      C b0 = sB[k * (NB + 1) + 2 * tx], b1 = sB[k * (NB + 1) + 2 * tx + 1];
-      cfma(part[0][0], a0, b0);
-      cfma(part[0][1], a0, b1);
-      cfma(part[1][0], a1, b0);
-      cfma(part[1][1], a1, b1);
-    }
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        if (colterm) {
-          acc[a][b].x -= part[a][b].x;
-          acc[a][b].y -= part[a][b].y;
-        } else {
-          acc[a][b].x += part[a][b].x;
-          acc[a][b].y += part[a][b].y;
-        }
+  // ---- which open tile (I, M) this CTA owns
+  int I, M;
+  if (SOLVE) {  // tile (M + N - 1 - lev, M) on level lev
+    M = blockIdx.x;
+    I = M + N - 1 - lev;
+  } else if ((int)blockIdx.x < p.countA) {  // region A: M <= lev-1, I in [M, M + N - lev - 1]
+    const int h = N - lev;
+    M = blockIdx.x / h;
+    I = M + blockIdx.x % h;
+  } else {  // region B: I = N-lev+r, M in [lev, N-lev+r]
+    int rem = blockIdx.x - p.countA, r = 0;
+    while (true) {
+      const int cnt = N - 2 * lev + r + 1;
+      if (cnt > 0) {
+        if (rem < cnt) break;
+        rem -= cnt;
       }
-  }
-
-  const int tiles = p.level + 1;
-  if (p.splits > 1) {
-    // publish the partial, last CTA of this tile reduces in split order
-    C* mine = ws + ((size_t)split * tiles + J) * NB * NB;
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) mine[(2 * ty + a) * NB + 2 * tx + b] = acc[a][b];
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-      int prev = atomicAdd(&counters[J], 1);
-      s_last = (prev == p.splits - 1);
-      if (s_last) counters[J] = 0;  // ready for the next level / call
+      ++r;
     }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        C s = czero<C>();
-        for (int q = 0; q < p.splits; ++q) {
-          C v = ws[((size_t)q * tiles + J) * NB * NB + (2 * ty + a) * NB + 2 * tx + b];
-          s.x += v.x;
-          s.y += v.y;
-        }
-        acc[a][b] = s;
-      }
+    M = lev + rem;
+    I = N - lev + r;
   }
-
-  // ---- tile solve: T_II X - X T_JJ = R,  R = -E_IJ + acc
-  C* sT2 = sA;                 // T_II
-  C* sT1 = sB;                 // T_JJ
-  C* sX = sB + NB * (NB + 1);  // X
-  __syncthreads();
-  load_tile(sT2, T, ld, I * NB, I * NB, n);
-  load_tile(sT1, T, ld, J * NB, J * NB, n);
+  const int tlev = (N - 1 - I) + M;
+  if (!SOLVE && tlev == lev) return;  // owned by the SOLVE launch
+  const bool has_col = lev >= 1 && M <= lev - 1;
+  const bool has_row = lev >= 1 && I >= N - lev;
+  const int tid = threadIdx.x;
+  // ---- load R_IM and the contributing tiles
+  load_tile_async(s0, R, ld, I * NB, M * NB, n);
+  if (has_col) {
+    const int K = M + N - lev;
+    load_tile_async(s1, T, ld, I * NB, K * NB, n);  // T_IK
+    load_tile_async(s2, L, ld, K * NB, M * NB, n);  // L_KM
+  }
+  if (has_row) {
+    const int J = I - N + lev;
+    load_tile_async(s3, L, ld, I * NB, J * NB, n);  // L_IJ
+    load_tile_async(s4, T, ld, J * NB, M * NB, n);  // T_JM
+  }
+  if (SOLVE) {  // the diagonal blocks for the tile solve, behind a separate group
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
   if (tid == 0) s_clip = 0;
-  for (int idx = tid; idx < NB * NB; idx += NT) sX[(idx / NB) * (NB + 1) + idx % NB] = czero<C>();
-  const bool diag = (I == J);
-  C r[2][2];
-  int stepv[2][2];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      int i = 2 * ty + a, j = 2 * tx + b;
-      int gi = I * NB + i, gj = J * NB + j;
-      bool valid = gi < n && gj < n && (!diag || i > j);
-      C e = valid ? E[(size_t)gi * ld + gj] : czero<C>();
-      r[a][b].x = acc[a][b].x - e.x;
-      r[a][b].y = acc[a][b].y - e.y;
-      stepv[a][b] = valid ? (NB - 1 - i) + j : -1;
-    }
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
-  const int nsteps = diag ? NB - 1 : 2 * NB - 1;
-  for (int s = 0; s < nsteps; ++s) {
-    // finalise the entries of anti-diagonal s
+  if (has_col || has_row) {
+    const int ty = tid / 8, tx = tid % 8;  // rows 2ty..2ty+1, cols 4tx..4tx+3
+    C acc[2][4];
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int b = 0; b < 2; ++b)
-        if (stepv[a][b] == s) {
-          int i = 2 * ty + a, j = 2 * tx + b;
-          C t2 = sT2[i * (NB + 1) + i], t1 = sT1[j * (NB + 1) + j];
-          C piv;
-          piv.x = t2.x - t1.x;
-          piv.y = t2.y - t1.y;
-          C x = cdiv(r[a][b], piv);
-          if (clip > 0 && sqrt(x.x * x.x + x.y * x.y) > clip) {
-            x = czero<C>();
-            atomicAdd(&s_clip, 1u);
-          }
-          sX[i * (NB + 1) + j] = x;
+      for (int c = 0; c < 4; ++c) acc[a][c] = s0[(2 * ty + a) * LD + 4 * tx + c];
+    if (has_col) {
+#pragma unroll 8
+      for (int k = 0; k < NB; ++k) {
+        C a0 = s1[(2 * ty) * LD + k], a1 = s1[(2 * ty + 1) * LD + k];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          C b = s2[k * LD + 4 * tx + c];
+          cfms(acc[0][c], a0, b);
+          cfms(acc[1][c], a1, b);
         }
-    __syncthreads();
-    // fold the freshly final neighbours into the open entries
+      }
+    }
+    if (has_row) {
+#pragma unroll 8
+      for (int k = 0; k < NB; ++k) {
+        C a0 = s3[(2 * ty) * LD + k], a1 = s3[(2 * ty + 1) * LD + k];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          C b = s4[k * LD + 4 * tx + c];
+          cfma(acc[0][c], a0, b);
+          cfma(acc[1][c], a1, b);
+        }
+      }
+    }
+    if (!SOLVE) {  // still open: write the updated right-hand side back
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int gi = I * NB + 2 * ty + a, gj = M * NB + 4 * tx + c;
+          if (gi < n && gj < n) R[(size_t)gi * ld + gj] = acc[a][c];
+        }
+      return;
+    }
+    __syncthreads();  // everyone is done reading s0 before it is overwritten
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int b = 0; b < 2; ++b)
-        if (stepv[a][b] > s) {
-          int i = 2 * ty + a, j = 2 * tx + b;
-          int k = NB - 1 - s + j;  // column neighbour (k, j), k > i
-          if (k > i && k < NB) cfms(r[a][b], sT2[i * (NB + 1) + k], sX[k * (NB + 1) + j]);
-          int k2 = s - (NB - 1 - i);  // row neighbour (i, k2), k2 < j
-          if (k2 >= 0 && k2 < j) cfma(r[a][b], sX[i * (NB + 1) + k2], sT1[k2 * (NB + 1) + j]);
-        }
+      for (int c = 0; c < 4; ++c) s0[(2 * ty + a) * LD + 4 * tx + c] = acc[a][c];
   }
+  if (!SOLVE) return;
+  // ---- solve the tile: T_II X - X T_MM = R_IM
+  __syncthreads();
+  load_tile(s1, T, ld, I * NB, I * NB, n);  // T_II
+  load_tile(s2, T, ld, M * NB, M * NB, n);  // T_MM
+  __syncthreads();
+  const int vi = min(NB, n - I * NB), vj = min(NB, n - M * NB);
+  // every warp runs the (identical) tile solve: keeping the shuffles outside any
+  // thread-dependent branch lets them compile to plain SHFL instead of
+  // convergence-barrier sequences; all warps store the same values
+  if (I == M)
+    tile_solve_warp<C, true>(s1, s2, s0, s3, vi, vj, clip, &s_clip);
+  else
+    tile_solve_warp<C, false>(s1, s2, s0, s3, vi, vj, clip, &s_clip);
   __syncthreads();
   for (int idx = tid; idx < NB * NB; idx += NT) {
-    int i = idx / NB, j = idx % NB;
-    int gi = I * NB + i, gj = J * NB + j;
-    if (gi < n && gj < n) L[(size_t)gi * ld + gj] = (diag && i <= j) ? czero<C>() : sX[i * (NB + 1) + j];
+    const int i = idx / NB, j = idx % NB;
+    const int gi = I * NB + i, gj = M * NB + j;
+    if (gi < n && gj < n) L[(size_t)gi * ld + gj] = (I == M && i <= j) ? czero<C>() : s3[i * LD + j];
   }
   if (tid == 0 && s_clip) atomicAdd(clipped, (unsigned long long)s_clip);
+}
+
+// R = -stril(E) (only the strictly lower part is ever read), L = 0.
+template <typename C>
+__global__ void init_kernel(int n, const C* __restrict__ E, C* __restrict__ R, C* __restrict__ L, long long ld) {
+  const long long total = (long long)n * n;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    const C e = E[(size_t)i * ld + j];
+    C r;
+    r.x = (i > j) ? -e.x : 0;
+    r.y = (i > j) ? -e.y : 0;
+    R[(size_t)i * ld + j] = r;
+    L[(size_t)i * ld + j] = czero<C>();
+  }
 }
 
 // Exact-duplicate diagonal check (trisolve.py:104-113): flags |= 1 on a hit.
@@ -258,53 +324,82 @@ __global__ void separation_kernel(int n, const C* __restrict__ T, long long ld, 
   if (a.x == b.x && a.y == b.y) atomicOr(flags, SR_FLAG_SEPARATION);
 }
 
+inline int count_b(int N, int lev) {
+  int c = 0;
+  for (int r = 0; r < lev; ++r) {
+    const int cnt = N - 2 * lev + r + 1;
+    if (cnt > 0) c += cnt;
+  }
+  return c;
+}
+
 template <typename C>
 int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsigned long long* d_clipped,
           int* d_flags, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (n < 0 || ld < n) return SR_EINVAL;
   if (n == 0) return SR_OK;
   const int N = (n + NB - 1) / NB;
-  size_t need = sr_trisolve_workspace_bytes(n, sizeof(C) == 8 ? 1 : 0);
-  if (ws_bytes < need || !ws) return SR_EINVAL;
-  int* counters = (int*)ws;
-  C* part = (C*)((char*)ws + 4096 * sizeof(int) * ((N + 4095) / 4096));
-  SR_CUDA_CHECK(cudaMemsetAsync(counters, 0, sizeof(int) * N, st));
-  SR_CUDA_CHECK(cudaMemsetAsync(l, 0, sizeof(C) * (size_t)n * ld, st));  // strictly upper tiles stay 0
+  const size_t need = sr_trisolve_workspace_bytes(n, sizeof(C) == 8 ? 1 : 0);
+  if (ws_bytes < need || !ws || (size_t)n * ld * sizeof(C) > need) return SR_EINVAL;
+  C* R = (C*)ws;
   {
+    const long long total = (long long)n * n;
+    const long long blocks = (total + 255) / 256;
+    const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
+    init_kernel<C><<<grid, 256, 0, st>>>(n, e, R, l, ld);
+    SR_LAUNCH_CHECK();
     dim3 b(32, 8), g(sr_ceil_div(n, 32), sr_ceil_div(n, 8));
     separation_kernel<C><<<g, b, 0, st>>>(n, t, ld, d_flags);
     SR_LAUNCH_CHECK();
   }
-  const size_t smem = sizeof(C) * (3 * NB * (NB + 1));
-  auto kern = trisolve_level_kernel<C>;
+  const size_t smem = sizeof(C) * 5 * NB * LD;
+  auto ksolve = sweep_kernel<C, true>;
+  auto kupd = sweep_kernel<C, false>;
+  // Two internal streams (created once): the critical-path tile solves and the
+  // bulk right-hand-side updates of each level run concurrently; events order
+  // level lev+1 after both launches of level lev.
   static bool configured = false;
+  static cudaStream_t s_solve, s_upd;
+  static cudaEvent_t ev_in, ev_s, ev_u;
   if (!configured) {
-    SR_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SR_CUDA_CHECK(cudaFuncSetAttribute(ksolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SR_CUDA_CHECK(cudaFuncSetAttribute(kupd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SR_CUDA_CHECK(cudaStreamCreateWithFlags(&s_solve, cudaStreamNonBlocking));
+    SR_CUDA_CHECK(cudaStreamCreateWithFlags(&s_upd, cudaStreamNonBlocking));
+    SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+    SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_s, cudaEventDisableTiming));
+    SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_u, cudaEventDisableTiming));
     configured = true;
   }
-  const int max_ctas = SR_TRISOLVE_MAX_CTAS;
-  for (int level = 0; level < N; ++level) {
-    int tiles = level + 1;
-    int splits = 1;
-    if (level >= 4) {
-      splits = max(1, min(level / 2, (2 * 148 + tiles - 1) / tiles));
-      splits = min(splits, max_ctas / tiles);
-      if (splits < 1) splits = 1;
-    }
-    LevelArgs a{n, N, level, splits, ld};
-    kern<<<dim3(tiles, splits), NT, smem, st>>>(a, t, e, l, part, counters, (typename Real<C>::T)clip,
-                                                d_clipped);
+  SR_CUDA_CHECK(cudaEventRecord(ev_in, st));
+  SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, ev_in, 0));
+  SR_CUDA_CHECK(cudaStreamWaitEvent(s_upd, ev_in, 0));
+  const typename Real<C>::T cl = (typename Real<C>::T)clip;
+  for (int lev = 0; lev < N; ++lev) {
+    const int countA = lev * (N - lev);
+    SweepArgs a{n, N, lev, countA, ld};
+    ksolve<<<lev + 1, NT, smem, s_solve>>>(a, t, R, l, cl, d_clipped);
     SR_LAUNCH_CHECK();
+    const int grid = lev == 0 ? 0 : countA + count_b(N, lev);
+    if (grid > 0) {
+      kupd<<<grid, NT, smem, s_upd>>>(a, t, R, l, cl, d_clipped);
+      SR_LAUNCH_CHECK();
+    }
+    SR_CUDA_CHECK(cudaEventRecord(ev_s, s_solve));
+    SR_CUDA_CHECK(cudaEventRecord(ev_u, s_upd));
+    SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, ev_u, 0));
+    SR_CUDA_CHECK(cudaStreamWaitEvent(s_upd, ev_s, 0));
   }
+  SR_CUDA_CHECK(cudaEventRecord(ev_s, s_solve));
+  SR_CUDA_CHECK(cudaStreamWaitEvent(st, ev_s, 0));
   return SR_OK;
 }
 
 }  // namespace
 
 extern "C" size_t sr_trisolve_workspace_bytes(int n, int lp_is_c64) {
-  const int N = (n + NB - 1) / NB;
-  size_t elt = lp_is_c64 ? 8 : 16;
-  return 4096 * sizeof(int) * ((N + 4095) / 4096) + (size_t)SR_TRISOLVE_MAX_CTAS * NB * NB * elt;
+  const size_t elt = lp_is_c64 ? 8 : 16;
+  return (size_t)n * (size_t)(n + (n & 1)) * elt + 256;  // the running right-hand side R
 }
 
 extern "C" int sr_trisolve_c64(int n, const void* t, const void* e, long long ld, void* l, float clip,

@@ -145,11 +145,37 @@ class ResidueBuffer:
         self.buf = torch.empty(nmod * 2 * M * self.pitch, dtype=torch.int8, device=device)
 
 
+_TIMING = None  # list of (start_event, end_event, int8_ops) while bench timing is on
+
+
+def timing_begin():
+    """Record CUDA events around every modular GEMM launch (bench roofline)."""
+    global _TIMING
+    _TIMING = []
+
+
+def timing_end():
+    """-> (total ms, total algorithmic int8 ops, launches) since timing_begin."""
+    global _TIMING
+    recs, _TIMING = _TIMING or [], None
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b, _ in recs)
+    return ms, float(sum(o for _, _, o in recs)), len(recs)
+
+
 def gemm_residues(ea, eb, pl, res):
     if ea.K != eb.K:
         raise ValueError("inner dimensions disagree: %d vs %d" % (ea.K, eb.K))
+    rec = _TIMING is not None
+    if rec:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
     _lib.call("sr_oz_gemm_i8", ea.rows, eb.rows, ea.K, pl.nmod, pl.moduli_ptr(), ea.buf.data_ptr(), ea.planes,
               ea.kp, eb.buf.data_ptr(), eb.planes, eb.kp, res.buf.data_ptr(), res.pitch, 0, _stream())
+    if rec:
+        e1.record()
+        real_products = 4 if eb.planes == 3 else 2
+        _TIMING.append((e0, e1, 2.0 * ea.rows * eb.rows * ea.K * real_products * pl.nmod))
 
 
 def decode(res, ea, eb, pl, out, alpha=1.0, shift=0.0, add=None, add_scale=1.0):

@@ -214,10 +214,13 @@ def _run_fp64(a, qhat, cfg, ws):
     n = a.rows
     st = _stream()
     hp0 = _counters["hp_calls"]
+    _mark("start")
     prod = products.make(cfg.gemm, ws, a)
     if cfg.restore_full_sigma:
         products.ensure_full_sigma_buffers(ws)
+    _mark("setup")
     _newton_schulz_entry(qhat, ws, prod)
+    _mark("entry")
     _lib.call("sr_fro_norm_f64", n, n, a.re_ptr(), a.im_ptr(), a.ld, ws.ptr(0), ws.red[0].data_ptr(),
               ws.red[0].numel(), st)
     history = []
@@ -243,10 +246,12 @@ def _run_fp64(a, qhat, cfg, ws):
     for it in range(1, cfg.max_iters + 1):
         # T^ = (Q^H A) Q; split + lp downcast + ||E||; Y = Q^H Q - I; ||Y||
         prod.measure(a)
+        _mark("measure")
         _lib.call("sr_split_lp_c64", n, ws.that.re_ptr(), ws.that.im_ptr(), ws.that.ld, ws.t_lp.data_ptr(),
                   ws.e_lp.data_ptr(), ws.t_lp.shape[1], ws.ptr(1), ws.red[1].data_ptr(), ws.red[1].numel(), st)
         _lib.call("sr_fro_norm_f64", n, n, ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld, ws.ptr(2),
                   ws.red[2].data_ptr(), ws.red[2].numel(), st)
+        _mark("split_norms")
         s = ws.scal[:3].cpu()  # sync 1
         norm_a, norm_e, norm_y = float(s[0]), float(s[1]), float(s[2])
         if tol is None:
@@ -265,8 +270,10 @@ def _run_fp64(a, qhat, cfg, ws):
         ws.solver.clipped.zero_()
         ws.solver.flags.zero_()
         solve_lp_device(ws.t_lp, ws.e_lp, ws.l_lp, n, cfg.clip_threshold, ws.solver, st)
+        _mark("solve")
         _lib.call("sr_skew_c64", n, ws.l_lp.data_ptr(), ws.l_lp.shape[1], ws.w_lp.data_ptr(), ws.ptr(3),
                   ws.solver.flags.data_ptr(), ws.red[3].data_ptr(), ws.red[3].numel(), st)
+        _mark("skew")
         norm_w = float(ws.scal[3].cpu())  # sync 2
         flags = int(ws.solver.flags.item())
         nclip = int(ws.solver.clipped.item())
@@ -284,6 +291,7 @@ def _run_fp64(a, qhat, cfg, ws):
                 and norm_w <= math.sqrt(U_FP64))
         if not skip:
             prod.update(cfg.restore_full_sigma)
+            _mark("update")
         if converged:
             status, iterations, skip_fired = RefineStatus.CONVERGED, it, skip
             break
@@ -305,6 +313,15 @@ def _run_fp64(a, qhat, cfg, ws):
 
 
 _WS_CACHE = {}
+
+PHASES = None  # list of (label, cuda event) while phase profiling is on (tools/time_refine.py)
+
+
+def _mark(label):
+    if PHASES is not None:
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        PHASES.append((label, ev))
 
 
 def _workspace(n, device):

@@ -69,7 +69,7 @@ if n <= 4096:
             ["%.2e" % (h[0] / np.linalg.norm(A)) for h in r.residual_history]), flush=True)
 
 # Q^ generation options at large n (setup only): LAPACK cgees vs GPU eig + QR
-if len(sys.argv) > 2:
+if len(sys.argv) > 2 and int(sys.argv[2]) > 0:
     import scipy.linalg
     m = int(sys.argv[2])
     A = inputs.gaussian_real(m, 0)
@@ -94,3 +94,29 @@ if len(sys.argv) > 2:
     print("cgees n=%d: %.1fs relE %.2e ortho %.2e" % (m, time.perf_counter() - t0,
           np.linalg.norm(np.tril(th, -1)) / np.linalg.norm(A),
           np.linalg.norm(zq.conj().T @ zq - np.eye(m))), flush=True)
+
+
+def phase_profile(A, Q, cfg, label):
+    import collections
+    from paper_2203_10879_b200 import refine as R
+    refine_template(A, Q, cfg)
+    torch.cuda.synchronize()
+    R.PHASES = []
+    t0 = time.perf_counter()
+    pair, r = refine_template(A, Q, cfg)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ph, R.PHASES = R.PHASES, None
+    acc = collections.OrderedDict()
+    for (l0, e0), (l1, e1) in zip(ph, ph[1:]):
+        acc[l1] = acc.get(l1, 0.0) + e0.elapsed_time(e1)
+    print("phases[%s] n=%d wall %.3f s, iterations %d: %s" % (label, A.shape[0] if hasattr(A, "shape") else 0,
+          wall, r.iterations, ", ".join("%s %.1f ms" % kv for kv in acc.items())), flush=True)
+    print("  history relE:", ["%.2e" % (h[0] / float(np.linalg.norm(A))) for h in r.residual_history], flush=True)
+
+
+if len(sys.argv) > 3:
+    m = int(sys.argv[3])
+    Am = inputs.gaussian_real(m, 0)
+    Qm = inputs.cached_qhat("c3_n%d_s0" % m, Am).astype(np.complex128)
+    phase_profile(Am, Qm, RefineConfig(precision="fp64", tol_factor=10.0 / m, max_iters=10), "ozaki")

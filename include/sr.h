@@ -125,36 +125,50 @@ size_t sr_reduce_workspace_bytes(void);
    Sources are planar FP64 (src_c64 = 0; im may be NULL for a real matrix) or
    interleaved complex64 (src_c64 = 1; im unused). */
 
-/* exps[i] = e with max_k |op(X)[i,k]| < 2^e; op(X) = X (transposed = 0:
-   per row) or X^T (transposed = 1: per column). */
-int sr_oz_exponents(int rows, int cols, const void* src, const double* im, long long ld, int src_c64,
-                    int transposed, int* exps, void* stream);
+/* matrix kinds of the Ozaki entry points */
+#define SR_MAT_F64 0  /* planar FP64 (re, im); im == NULL: real */
+#define SR_MAT_C64 1  /* interleaved complex64 (re) */
+#define SR_MAT_C128 2 /* interleaved complex128 (re) */
+#define SR_MAT_DD 3   /* planar double-double: re = re_hi, im = im_hi, re_lo, im_lo */
+
+/* exps[i] = e with max_k |op(X)[i,k]| < 2^e (dd: of the hi parts); op(X) = X
+   (transposed = 0: per row) or X^T (transposed = 1: per column). */
+int sr_oz_exponents(int rows, int cols, int kind, const void* re, const double* im, long long ld, int transposed,
+                    int* exps, void* stream);
 
 /* Residue planes [nmod][planes][rows_out][kpitch] (int8, K-major) of
-   round(op(X) * 2^(beta - exps[i])) modulo moduli[l] (129..256, pairwise
+   round(op(X) * 2^(beta - exps[i])) modulo moduli[l] (3..256, pairwise
    coprime; host array).  op(X)[i][k] = X[i][k], or X[k][i] when transposed;
    conj negates the imaginary part.  layout 0: (re, im) A operand;
-   1: (-im, re, im) complex B operand; 2: (re) real B operand. */
-int sr_oz_encode(int rows_out, int K, const void* src, const double* im, long long ld, int src_c64,
-                 int transposed, int conj, int layout, const int* exps, int beta, int nmod, const int* moduli,
-                 void* out, long long kpitch, void* stream);
+   1: (-im, re, im) complex B operand; 2: (re) real B operand.
+   beta <= 61 (<= 106 for SR_MAT_DD). */
+int sr_oz_encode(int rows_out, int K, int kind, const void* re, const double* im, const double* re_lo,
+                 const double* im_lo, long long ld, int transposed, int conj, int layout, const int* exps, int beta,
+                 int nmod, const int* moduli, void* out, long long kpitch, void* stream);
 
 /* R_l = A_l B_l^T mod p_l on tcgen05 (kind::i8), out [nmod][2][M][out_pitch]
    int8 (re, im).  a_planes = 2; b_planes = 3 (complex B) or 1 (real B).
-   moduli is a host array; num_sms <= 0 means 148. */
+   moduli is a host array; num_sms <= 0 means 148.  lower_only (M == N):
+   skip the 128 x 128 tiles above the diagonal (Hermitian products such as
+   Q^H Q, whose upper part the decode mirrors). */
 int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, const void* a, int a_planes,
                   long long a_kpitch, const void* b, int b_planes, long long b_kpitch, void* out,
-                  long long out_pitch, int num_sms, void* stream);
+                  long long out_pitch, int lower_only, int num_sms, void* stream);
 
 /* CRT decode of the residues into C = alpha * C' * 2^-(rho_i + sigma_j)
-   + shift * I + add_scale * X (X = (add_re, add_im), optional), with
-   rho_i = beta_a - exps_a[i], sigma_j = beta_b - exps_b[j].  table (host):
-   [nmod][4] CRT weights, [4] modulus-product chunks, [4] chunk offsets,
-   1/P.  out_kind 0: planar FP64 (out_re, out_im); 1: complex64 (out_re). */
+   + shift * I + add_scale * X (X of add_kind SR_MAT_F64 or SR_MAT_DD, or
+   add_kind < 0 for none), with rho_i = beta_a - exps_a[i], sigma_j =
+   beta_b - exps_b[j], rounded once into out_kind (any SR_MAT_*).  table
+   (host): [nmod][6] CRT weights, [6] modulus-product chunks, [6] chunk
+   offsets, 1/P.  hermitian: the residues hold only the lower 128-tiles
+   (sr_oz_gemm_i8 with lower_only); the strictly upper tiles are written as
+   the conjugate transpose (out_kind SR_MAT_F64 or SR_MAT_DD, no add). */
 int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* table, const void* res, long long res_pitch,
                  const int* exps_a, int beta_a, const int* exps_b, int beta_b, double alpha, double shift,
-                 const double* add_re, const double* add_im, long long ld_add, double add_scale, int out_kind,
-                 void* out_re, double* out_im, long long ld_out, void* stream);
+                 int add_kind, const double* add_re, const double* add_im, const double* add_re_lo,
+                 const double* add_im_lo, long long ld_add, double add_scale, int out_kind, void* out_re,
+                 double* out_im, double* out_re_lo, double* out_im_lo, long long ld_out, int hermitian,
+                 void* stream);
 
 #ifdef __cplusplus
 }

@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libsr.so")
 SR_OK, SR_EINVAL, SR_ESEPARATION, SR_ENONFINITE, SR_ECUDA = 0, 1, 2, 3, 4
 SR_FLAG_SEPARATION, SR_FLAG_NONFINITE = 1, 2
 SR_OP_N, SR_OP_C = 0, 1
+SR_MAT_F64, SR_MAT_C64, SR_MAT_C128, SR_MAT_DD = 0, 1, 2, 3
 
 _p = ctypes.c_void_p
 _i = ctypes.c_int
@@ -40,11 +41,11 @@ SIGNATURES = {
     "sr_sigma_ns_f64": (_i, [_i, _p, _p, _ll, _p, _p, _ll, _p]),
     "sr_triu_inplace_f64": (_i, [_i, _p, _p, _ll, _p]),
     "sr_reduce_workspace_bytes": (_sz, []),
-    "sr_oz_exponents": (_i, [_i, _i, _p, _p, _ll, _i, _i, _p, _p]),
-    "sr_oz_encode": (_i, [_i, _i, _p, _p, _ll, _i, _i, _i, _i, _p, _i, _i, _p, _p, _ll, _p]),
-    "sr_oz_gemm_i8": (_i, [_i, _i, _i, _i, _p, _p, _i, _ll, _p, _i, _ll, _p, _ll, _i, _p]),
-    "sr_oz_decode": (_i, [_i, _i, _i, _i, _p, _p, _ll, _p, _i, _p, _i, _d, _d, _p, _p, _ll, _d, _i, _p, _p, _ll,
-                          _p]),
+    "sr_oz_exponents": (_i, [_i, _i, _i, _p, _p, _ll, _i, _p, _p]),
+    "sr_oz_encode": (_i, [_i, _i, _i, _p, _p, _p, _p, _ll, _i, _i, _i, _p, _i, _i, _p, _p, _ll, _p]),
+    "sr_oz_gemm_i8": (_i, [_i, _i, _i, _i, _p, _p, _i, _ll, _p, _i, _ll, _p, _ll, _i, _i, _p]),
+    "sr_oz_decode": (_i, [_i, _i, _i, _i, _p, _p, _ll, _p, _i, _p, _i, _d, _d, _i, _p, _p, _p, _p, _ll, _d, _i,
+                          _p, _p, _p, _p, _ll, _i, _p]),
 }
 
 _lib = None

@@ -39,6 +39,7 @@ struct OzParams {
   int M, N, K, nmod;
   int a_planes, b_planes;
   int tiles_m, tiles_n;
+  int lower_only;               // Hermitian product: only tiles with nt <= mt
   long long out_pitch;          // bytes between output rows
   long long out_plane;          // bytes between output planes (re / im)
   long long out_mod;            // bytes between moduli
@@ -194,6 +195,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         int l, mt, nt;
         decode_tile(p, t, l, mt, nt);
+        if (p.lower_only && nt > mt) continue;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           uint8_t* st = smem + stage * stage_bytes;
@@ -216,6 +218,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      if (p.lower_only) {
+        int l, mt, nt;
+        decode_tile(p, t, l, mt, nt);
+        if (nt > mt) continue;
+      }
       mbar_wait(tempty_bar(acc), acc_phase ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const uint32_t d = tmem_base + (uint32_t)(acc * 256);
@@ -261,6 +268,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
       int l, mt, nt;
       decode_tile(p, t, l, mt, nt);
+      if (p.lower_only && nt > mt) continue;
       const int pm = p.moduli[l];
       const float inv = p.inv[l];
       mbar_wait(tfull_bar(acc), acc_phase);
@@ -336,11 +344,12 @@ int make_map(CUtensorMap* map, const void* base, int K, int rows, int planes, in
 
 extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, const void* a, int a_planes,
                              long long a_kpitch, const void* b, int b_planes, long long b_kpitch, void* out,
-                             long long out_pitch, int num_sms, void* stream) {
+                             long long out_pitch, int lower_only, int num_sms, void* stream) {
   if (M <= 0 || N <= 0 || K <= 0 || nmod <= 0 || nmod > MAX_MODULI) return SR_EINVAL;
+  if (lower_only && M != N) return SR_EINVAL;
   if (a_planes != 2 || (b_planes != 1 && b_planes != 3)) return SR_EINVAL;
   if ((a_kpitch | b_kpitch | out_pitch) & 15) return SR_EINVAL;
-  if (K > (1 << 17)) return SR_EINVAL;  // int32 accumulation stays exact below this
+  if (K > (1 << 16)) return SR_EINVAL;  // 2K terms of |x| <= 2^14: int32 accumulation stays exact
   if (((uintptr_t)a | (uintptr_t)b | (uintptr_t)out) & 15) return SR_EINVAL;
   OzParams p;
   memset(&p, 0, sizeof(p));
@@ -352,11 +361,12 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
   p.b_planes = b_planes;
   p.tiles_m = (M + TM - 1) / TM;
   p.tiles_n = (N + TN - 1) / TN;
+  p.lower_only = lower_only;
   p.out_pitch = out_pitch;
   p.out_plane = out_pitch * M;
   p.out_mod = p.out_plane * 2;
   for (int i = 0; i < nmod; ++i) {
-    if (moduli[i] < 2 || moduli[i] > 256) return SR_EINVAL;
+    if (moduli[i] < 3 || moduli[i] > 256) return SR_EINVAL;
     p.moduli[i] = moduli[i];
     p.inv[i] = 1.0f / (float)moduli[i];
   }

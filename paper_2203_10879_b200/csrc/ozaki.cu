@@ -1,130 +1,185 @@
 // Ozaki-II emulated complex products: operand encoding and CRT decoding.
 //
-// An FP64 (or complex64) product C = op(A) B is evaluated exactly on
-// integers (Ozaki, Uchino, Imamura — "Ozaki scheme II", CRT variant):
+// A product C = op(A) B is evaluated exactly on integers (Ozaki, Uchino,
+// Imamura — "Ozaki scheme II", CRT variant):
 //   1. scale   every row of op(A) and every column of B by a power of two so
 //              its largest entry is below 2^beta, round to integers A', B'
-//              (for beta = 60 every entry within 2^-7 of its row / column
-//              maximum is represented exactly — no quantisation at all);
+//              (FP64 mode, beta = 60: every entry within 2^-7 of its row or
+//              column maximum is represented exactly; dd mode, beta = 104);
 //   2. encode  the residues A' mod p_l, B' mod p_l (symmetric, int8) for the
 //              pairwise-coprime moduli p_1..p_r <= 256 of the plan, K-major;
 //   3. multiply on the tensor cores: R_l = A'_l B'_l mod p_l (oz_gemm.cu);
 //   4. decode  C' from its residues by the Chinese remainder theorem in
-//              exact FP64 chunk arithmetic, then unscale:
+//              exact FP64 chunk arithmetic (carry-normalised, so the final
+//              double-double sum has no cancellation), then unscale:
 //              C = alpha * C' * 2^-(rho_i + sigma_j) + shift * I + add_scale * X.
-// Because every integer product and sum is exact, the result is independent
-// of the summation order and its only error is the operand rounding of step 1
-// plus one final rounding — unlike a K-long FP64 accumulation chain, whose
-// noise on stril(Q^H A Q) grows like sqrt(K) (DESIGN.md §precision).
+// Every integer product and sum is exact, so the result is independent of
+// the summation order; its only errors are the operand rounding of step 1
+// and one final rounding — unlike a K-long FP64 accumulation chain, whose
+// noise on stril(Q^H A Q) grows like sqrt(K) (DESIGN.md §3.1).
 //
-// This replaces, in FP64 mode, the reference's hp product
-//   matmul_hp (/root/reference/pkg/src/ddschur/matmul.py:52-81) and lp product
-//   matmul_lp (matmul.py:84-110); the reference ships an Ozaki-I variant for
-//   dd (matmul.py:151-212) which this generalises to CRT residues on int8
-//   tensor cores.
+// Matrix kinds (SR_MAT_*, include/sr.h): planar FP64 (the FP64-mode hp type),
+// interleaved complex64 (FP64-mode lp), interleaved complex128 (dd-mode lp),
+// planar double-double (dd-mode hp, four planes re_hi, im_hi, re_lo, im_lo).
+//
+// This replaces matmul_hp / matmul_lp
+// (/root/reference/pkg/src/ddschur/matmul.py:52-110) and generalises the
+// reference's own Ozaki-I dd product (_ozaki_gemm_hp, matmul.py:151-212).
 #include "sr_common.cuh"
 
 namespace {
 
 constexpr int MAXMOD = 32;
-constexpr int MAXCHUNK = 4;
+constexpr int MAXCHUNK = 6;  // 40-bit CRT chunks: modulus products up to 240 bits
+constexpr int MAXDIG = 10;   // 11-bit digits: integers up to 2^109
+constexpr int EXP_FLOOR = -1074;  // below every finite double's exponent: all-zero rows/columns
 
-__device__ __forceinline__ void load_src(const double* re, const double* im, int c64, size_t off, double& vr,
-                                         double& vi) {
-  if (c64) {
-    float2 v = reinterpret_cast<const float2*>(re)[off];
+// x * 2^e without the libm ldexp (~15 instructions): two exact power-of-two
+// multiplies (the split keeps both factors in the normal range).
+__device__ __forceinline__ double pow2(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
+__device__ __forceinline__ double scale2(double x, int e) {
+  const int e1 = e / 2;
+  return (x * pow2(e1)) * pow2(e - e1);
+}
+
+struct Src {
+  const double* re;
+  const double* im;
+  const double* re_lo;
+  const double* im_lo;
+  int kind;
+};
+
+// element (re, im) [+ (re_lo, im_lo) for dd] at linear offset off
+template <int KIND>
+__device__ __forceinline__ void load_elem(const Src& s, size_t off, double& vr, double& vi, double& lr,
+                                          double& li) {
+  lr = li = 0.0;
+  if (KIND == SR_MAT_C64) {
+    const float2 v = reinterpret_cast<const float2*>(s.re)[off];
+    vr = v.x;
+    vi = v.y;
+  } else if (KIND == SR_MAT_C128) {
+    const double2 v = reinterpret_cast<const double2*>(s.re)[off];
     vr = v.x;
     vi = v.y;
   } else {
-    vr = re[off];
-    vi = im ? im[off] : 0.0;
+    vr = s.re[off];
+    vi = s.im ? s.im[off] : 0.0;
+    if (KIND == SR_MAT_DD) {
+      lr = s.re_lo[off];
+      li = s.im_lo[off];
+    }
   }
 }
 
-struct EncodeParams {
-  int rows_out, K, transposed, conj, layout, beta, nmod, src_c64;
-  long long ld, kpitch;
-  int moduli[MAXMOD];
-  double inv[MAXMOD];
-};
-
-// ---- exponents: e_i with max_k |op(X)[i,k]| < 2^e_i -------------------------
-__global__ void exps_direct_kernel(int rows, int cols, const double* __restrict__ re, const double* __restrict__ im,
-                                   long long ld, int c64, int* __restrict__ e) {
+// ---- exponents: e_i with max_k |op(X)[i,k]| < 2^e_i (dd: of the hi parts) ----
+template <int KIND>
+__global__ void exps_direct_kernel(int rows, int cols, Src s, long long ld, int* __restrict__ e) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
   double m = 0.0;
   for (int k = lane; k < cols; k += 32) {
-    double vr, vi;
-    load_src(re, im, c64, (size_t)warp * ld + k, vr, vi);
+    double vr, vi, lr, li;
+    load_elem<KIND>(s, (size_t)warp * ld + k, vr, vi, lr, li);
     m = fmax(m, fmax(fabs(vr), fabs(vi)));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   if (lane == 0) {
-    int ex = 0;
+    int ex = EXP_FLOOR;
     if (m > 0.0) frexp(m, &ex);
     e[warp] = ex;
   }
 }
 
-__global__ void exps_transposed_kernel(int rows, int cols, const double* __restrict__ re,
-                                       const double* __restrict__ im, long long ld, int c64, int* __restrict__ e) {
-  // one thread per column j, rows split over blockDim.y partial maxima
+__global__ void exps_fill_kernel(int n, int* __restrict__ e) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) e[i] = EXP_FLOOR;
+}
+
+// per-column maxima over a chunk of rows per block (grid.y), merged with an
+// integer atomicMax on the exponent (frexp's exponent is monotone in |x|)
+template <int KIND>
+__global__ void exps_transposed_kernel(int rows, int cols, Src s, long long ld, int rows_per_block,
+                                       int* __restrict__ e) {
   __shared__ double part[8][33];
   const int j = blockIdx.x * 32 + threadIdx.x;
+  const int r0 = blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
   double m = 0.0;
   if (j < cols)
-    for (int i = threadIdx.y; i < rows; i += 8) {
-      double vr, vi;
-      load_src(re, im, c64, (size_t)i * ld + j, vr, vi);
+    for (int i = r0 + threadIdx.y; i < r1; i += 8) {
+      double vr, vi, lr, li;
+      load_elem<KIND>(s, (size_t)i * ld + j, vr, vi, lr, li);
       m = fmax(m, fmax(fabs(vr), fabs(vi)));
     }
   part[threadIdx.y][threadIdx.x] = m;
   __syncthreads();
   if (threadIdx.y == 0 && j < cols) {
     for (int y = 1; y < 8; ++y) m = fmax(m, part[y][threadIdx.x]);
-    int ex = 0;
-    if (m > 0.0) frexp(m, &ex);
-    e[j] = ex;
+    if (m > 0.0) {
+      int ex = 0;
+      frexp(m, &ex);
+      atomicMax(&e[j], ex);
+    }
   }
-}
-
-// Symmetric residue of an integer-valued double a (|a| < 2^62) modulo p, in
-// [-floor(p/2), ceil(p/2) - 1].  Two exact fma reductions: the first quotient
-// estimate is within a few units, the second reduction is then exact.
-__device__ __forceinline__ double res_f64(double a, double p, double inv, double hi) {
-  double r = fma(-rint(a * inv), p, a);  // exact, |r| < 8p
-  r = fma(-rint(r * inv), p, r);         // exact, |r| <= p/2
-  if (r > hi) r -= p;
-  return r;
 }
 
 // ---- encode: residue planes [nmod][planes][rows_out][kpitch] -------------------
 // layout 0: A operand (re, im);  1: B operand (-im, re, im);  2: B operand (re)
-constexpr int ETI = 64, ETK = 32;  // tile: 64 output rows x 32 k
-__global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ EncodeParams p,
-                                                     const double* __restrict__ re, const double* __restrict__ im,
+struct EncodeParams {
+  int rows_out, K, transposed, conj, layout, beta, nmod, ndig;
+  long long ld, kpitch;
+  float pf[MAXMOD], invf[MAXMOD], hif[MAXMOD], lof[MAXMOD];
+  float pow2[MAXMOD][MAXDIG];  // 2^(11 c) mod p, symmetric
+};
+
+// balanced 11-bit digits of an integer-valued double (error-free, top-down)
+template <int ND>
+__device__ __forceinline__ void digits(double a, float (&d)[ND]) {
+#pragma unroll
+  for (int c = ND - 1; c >= 0; --c) {
+    const double sc = (double)(1ull << (11 * (c % 5))) * (c >= 5 ? 36028797018963968.0 : 1.0);  // 2^(11c)
+    const double q = rint(a * (1.0 / sc));
+    a = fma(-q, sc, a);
+    d[c] = (float)q;
+  }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ EncodeParams p, Src s,
                                                      const int* __restrict__ exps, int8_t* __restrict__ out) {
+  constexpr bool DD = KIND == SR_MAT_DD;
+  constexpr int ETI = DD ? 32 : 64, ETK = 32;  // tile: ETI output rows x 32 k
+  constexpr int ND = DD ? MAXDIG : 6;          // beta <= 61 needs 6 digits, dd up to 10
   __shared__ double s_re[ETI][ETK + 1];
   __shared__ double s_im[ETI][ETK + 1];
+  __shared__ double s_rl[DD ? ETI : 1][ETK + 1];
+  __shared__ double s_il[DD ? ETI : 1][ETK + 1];
   const int i0 = blockIdx.y * ETI, k0 = blockIdx.x * ETK;
   const int tid = threadIdx.x;
   // stage the source tile as s[i_local][k_local] = op(X)[i0 + i][k0 + k]
   for (int idx = tid; idx < ETI * ETK; idx += 256) {
-    double vr = 0.0, vi = 0.0;
+    double vr = 0.0, vi = 0.0, lr = 0.0, li = 0.0;
+    int il, kl;
     if (p.transposed) {
-      int a = idx / ETI, b = idx % ETI;  // coalesced along the source row (i)
-      int k = k0 + a, i = i0 + b;        // source X[k][i]
-      if (k < p.K && i < p.rows_out) load_src(re, im, p.src_c64, (size_t)k * p.ld + i, vr, vi);
-      s_re[b][a] = vr;
-      s_im[b][a] = vi;
+      const int a = idx / ETI, b = idx % ETI;  // coalesced along the source row (i)
+      const int k = k0 + a, i = i0 + b;        // source X[k][i]
+      if (k < p.K && i < p.rows_out) load_elem<KIND>(s, (size_t)k * p.ld + i, vr, vi, lr, li);
+      il = b;
+      kl = a;
     } else {
-      int a = idx / ETK, b = idx % ETK;  // coalesced along the source row (k)
-      int i = i0 + a, k = k0 + b;        // source X[i][k]
-      if (k < p.K && i < p.rows_out) load_src(re, im, p.src_c64, (size_t)i * p.ld + k, vr, vi);
-      s_re[a][b] = vr;
-      s_im[a][b] = vi;
+      const int a = idx / ETK, b = idx % ETK;  // coalesced along the source row (k)
+      const int i = i0 + a, k = k0 + b;        // source X[i][k]
+      if (k < p.K && i < p.rows_out) load_elem<KIND>(s, (size_t)i * p.ld + k, vr, vi, lr, li);
+      il = a;
+      kl = b;
+    }
+    s_re[il][kl] = vr;
+    s_im[il][kl] = vi;
+    if (DD) {
+      s_rl[il][kl] = lr;
+      s_il[il][kl] = li;
     }
   }
   __syncthreads();
@@ -137,28 +192,54 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
     const int i = i0 + il, k = k0 + kl;
     if (i >= p.rows_out || k >= p.K) continue;
     const int sh = p.beta - exps[i];
-    double ar[4], ai[4];
+    // exact 11-bit digit expansions of the scaled integers (FP64, error-free)
+    float dr[4][ND], di[4][ND];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       double xr = s_re[il][kl + e], xi = s_im[il][kl + e];
       if (p.conj) xi = -xi;
-      ar[e] = rint(ldexp(xr, sh));  // exact integers (|.| <= 2^beta)
-      ai[e] = rint(ldexp(xi, sh));
+      digits<ND>(rint(scale2(xr, sh)), dr[e]);  // exact integers, |.| <= 2^beta
+      digits<ND>(rint(scale2(xi, sh)), di[e]);
+      if (DD) {  // + the rounded lo part: digit-wise sum, still exact in FP32
+        double lr = s_rl[il][kl + e], li = s_il[il][kl + e];
+        if (p.conj) li = -li;
+        float er[ND], ei[ND];
+        digits<ND>(rint(scale2(lr, sh)), er);
+        digits<ND>(rint(scale2(li, sh)), ei);
+#pragma unroll
+        for (int c = 0; c < ND; ++c) {
+          dr[e][c] += er[c];
+          di[e][c] += ei[c];
+        }
+      }
     }
     int8_t* dst = out + (size_t)i * p.kpitch + k;
     for (int l = 0; l < p.nmod; ++l) {
-      const double pm = (double)p.moduli[l], inv = p.inv[l];
-      const double hi = (double)(((p.moduli[l] + 1) >> 1) - 1);
+      const float pm = p.pf[l], inv = p.invf[l], hi = p.hif[l], lo = p.lof[l];
       uint32_t wr = 0, wi = 0, wn = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int rr = (int)res_f64(ar[e], pm, inv, hi);
-        const int ri = (int)res_f64(ai[e], pm, inv, hi);
-        int rn = -ri;
-        if (rn > (int)hi) rn -= p.moduli[l];
-        wr |= (uint32_t)(rr & 0xFF) << (8 * e);
-        wi |= (uint32_t)(ri & 0xFF) << (8 * e);
-        wn |= (uint32_t)(rn & 0xFF) << (8 * e);
+        // residue = sum_c digit_c * (2^(11c) mod p), exact in FP32 (|.| < 2^22), then one reduction
+        float vr = 0.f, vi = 0.f;
+#pragma unroll
+        for (int c = 0; c < ND; ++c) {
+          if (c < p.ndig) {
+            vr = fmaf(dr[e][c], p.pow2[l][c], vr);
+            vi = fmaf(di[e][c], p.pow2[l][c], vi);
+          }
+        }
+        const float qr = (vr * inv + 12582912.f) - 12582912.f;  // round-to-nearest, |.| < 2^22
+        const float qi = (vi * inv + 12582912.f) - 12582912.f;
+        float rr = fmaf(-qr, pm, vr);
+        float ri = fmaf(-qi, pm, vi);
+        rr = rr > hi ? rr - pm : (rr < lo ? rr + pm : rr);
+        ri = ri > hi ? ri - pm : (ri < lo ? ri + pm : ri);
+        float rn = -ri;
+        rn = rn > hi ? rn - pm : rn;
+        // the low byte of (r + 1.5 * 2^23) is r in two's complement
+        wr |= (__float_as_uint(rr + 12582912.f) & 0xFFu) << (8 * e);
+        wi |= (__float_as_uint(ri + 12582912.f) & 0xFFu) << (8 * e);
+        wn |= (__float_as_uint(rn + 12582912.f) & 0xFFu) << (8 * e);
       }
       int8_t* dm = dst + (size_t)l * mod_stride;
       if (p.layout == 0) {
@@ -177,75 +258,110 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
 
 // ---- decode -----------------------------------------------------------------
 struct DecodeParams {
-  int M, N, nmod, nchunk, beta_a, beta_b, out_kind, has_add;
+  int M, N, nmod, nchunk, beta_a, beta_b, hermitian;
   long long res_pitch, res_plane, res_mod, ld_out, ld_add;
   double alpha, shift, add_scale;
   double w[MAXMOD][MAXCHUNK];  // CRT weights, chunk j in units of 2^off[j]
   double pc[MAXCHUNK];         // modulus product P in the same chunks
-  int off[MAXCHUNK];
+  double offv[MAXCHUNK];       // 2^off[j]
+  double cw[MAXCHUNK], icw[MAXCHUNK];  // 2^(off[j-1]-off[j]) and its inverse
   double inv_p;                // 1 / P
 };
 
 __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
   s = a + b;
-  double bb = s - a;
+  const double bb = s - a;
   e = (a - (s - bb)) + (b - bb);
 }
+__device__ __forceinline__ void quick_two_sum(double a, double b, double& s, double& e) {
+  s = a + b;
+  e = b - (s - a);
+}
+// (hi, lo) += b
 __device__ __forceinline__ void dd_add_d(double& hi, double& lo, double b) {
   double s, e;
   two_sum(hi, b, s, e);
   e += lo;
-  hi = s + e;
-  lo = e - (hi - s);
+  quick_two_sum(s, e, hi, lo);
+}
+// (hi, lo) += (bh, bl), the accurate dd sum of the reference (dd.py:96-104)
+__device__ __forceinline__ void dd_add_dd(double& hi, double& lo, double bh, double bl) {
+  double s1, s2, t1, t2;
+  two_sum(hi, bh, s1, s2);
+  two_sum(lo, bl, t1, t2);
+  s2 += t1;
+  quick_two_sum(s1, s2, s1, s2);
+  s2 += t2;
+  quick_two_sum(s1, s2, hi, lo);
 }
 
 // CRT finish: S[j] = sum_l x_l w_lj (exact chunk sums) -> double-double value
-__device__ __forceinline__ void crt_finish(const DecodeParams& p, const double (&S)[MAXCHUNK], double& hi,
-                                           double& lo) {
-  double approx = ldexp(S[0], p.off[0]);
-  if (p.nchunk > 1) approx += ldexp(S[1], p.off[1]);
+template <int NC>
+__device__ __forceinline__ void crt_finish(const DecodeParams& p, const double (&S)[NC], double& hi, double& lo) {
+  double approx = S[0] * p.offv[0];
+  if (NC > 1) approx += S[1] * p.offv[1];
   const double k = rint(approx * p.inv_p);
-  hi = 0.0;
+  double t[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) t[j] = fma(-k, p.pc[j], S[j]);  // exact integers
+  // carry-normalise from the bottom chunk up so that |t_j| <= 2^(width_j - 1)
+  // for j >= 1: the double-double sum below then has no cancellation
+#pragma unroll
+  for (int j = NC - 1; j >= 1; --j) {
+    const double c = rint(t[j] * p.icw[j]);
+    t[j] = fma(-c, p.cw[j], t[j]);
+    t[j - 1] += c;
+  }
+  hi = t[0] * p.offv[0];
   lo = 0.0;
 #pragma unroll
-  for (int j = 0; j < MAXCHUNK; ++j) {
-    if (j >= p.nchunk) break;
-    const double t = fma(-k, p.pc[j], S[j]);  // exact integer
-    dd_add_d(hi, lo, ldexp(t, p.off[j]));
-  }
+  for (int j = 1; j < NC; ++j) dd_add_d(hi, lo, t[j] * p.offv[j]);
 }
 
+struct Dst {
+  double* re;
+  double* im;
+  double* re_lo;
+  double* im_lo;
+};
+
 // one thread: row i, columns j0..j0+3, both planes
+template <int NC, int OUT, int ADD>
 __global__ void __launch_bounds__(256) decode_kernel(const __grid_constant__ DecodeParams p,
                                                      const int8_t* __restrict__ res, const int* __restrict__ ea,
-                                                     const int* __restrict__ eb, const double* __restrict__ add_re,
-                                                     const double* __restrict__ add_im, void* __restrict__ out_re,
-                                                     double* __restrict__ out_im) {
+                                                     const int* __restrict__ eb, Src add, Dst out) {
   const int ngrp = (p.N + 3) >> 2;
   const long long total = (long long)p.M * ngrp;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(idx / ngrp), j0 = (int)(idx % ngrp) * 4;
+    if (p.hermitian && (j0 >> 7) > (i >> 7)) continue;  // upper GEMM tile: mirrored afterwards
     const int rho = p.beta_a - ea[i];
 #pragma unroll 1
     for (int plane = 0; plane < 2; ++plane) {
-      double S[4][MAXCHUNK];
+      double S[4][NC];
 #pragma unroll
       for (int e = 0; e < 4; ++e)
 #pragma unroll
-        for (int j = 0; j < MAXCHUNK; ++j) S[e][j] = 0.0;
+        for (int j = 0; j < NC; ++j) S[e][j] = 0.0;
       const int8_t* r = res + (size_t)plane * p.res_plane + (size_t)i * p.res_pitch + j0;
-#pragma unroll 4
-      for (int l = 0; l < p.nmod; ++l) {
+      // issue every residue load first (MAXMOD words in flight per thread)
+      uint32_t wv[MAXMOD];
+#pragma unroll
+      for (int l = 0; l < MAXMOD; ++l)
+        if (l < p.nmod) wv[l] = *reinterpret_cast<const uint32_t*>(r + (size_t)l * p.res_mod);
+#pragma unroll
+      for (int l = 0; l < MAXMOD; ++l) {
+        if (l >= p.nmod) break;
         // int8 -> double without I2F: the byte with its sign bit flipped is
         // x + 128 in [0, 255]; as the low word of 0x4338000000000000 it reads
         // 1.5 * 2^52 + x + 128, so one DADD recovers x exactly.
-        const uint32_t w4 = *reinterpret_cast<const uint32_t*>(r + (size_t)l * p.res_mod) ^ 0x80808080u;
+        const uint32_t w4 = wv[l] ^ 0x80808080u;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const double x = __hiloint2double(0x43380000, (w4 >> (8 * e)) & 0xFF) - 6755399441055872.0;
 #pragma unroll
-          for (int j = 0; j < MAXCHUNK; ++j) S[e][j] = fma(x, p.w[l][j], S[e][j]);  // exact: < 2^52
+          for (int j = 0; j < NC; ++j) S[e][j] = fma(x, p.w[l][j], S[e][j]);  // exact: < 2^52
         }
       }
 #pragma unroll
@@ -253,54 +369,130 @@ __global__ void __launch_bounds__(256) decode_kernel(const __grid_constant__ Dec
         const int j = j0 + e;
         if (j >= p.N) break;
         double hi, lo;
-        crt_finish(p, S[e], hi, lo);
+        crt_finish<NC>(p, S[e], hi, lo);
         const int sc = -(rho + (p.beta_b - eb[j]));
-        hi = ldexp(hi, sc) * p.alpha;
-        lo = ldexp(lo, sc) * p.alpha;
+        hi = scale2(hi, sc) * p.alpha;
+        lo = scale2(lo, sc) * p.alpha;
         if (plane == 0 && i == j && p.shift != 0.0) dd_add_d(hi, lo, p.shift);
-        if (p.has_add) {
-          const double av = plane == 0 ? add_re[(size_t)i * p.ld_add + j] : add_im[(size_t)i * p.ld_add + j];
-          dd_add_d(hi, lo, p.add_scale * av);
-        }
-        const double v = hi + lo;
-        if (p.out_kind == 0) {
-          if (plane == 0)
-            ((double*)out_re)[(size_t)i * p.ld_out + j] = v;
-          else
-            out_im[(size_t)i * p.ld_out + j] = v;
+        const size_t oa = (size_t)i * p.ld_add + j;
+        if (ADD == SR_MAT_F64) dd_add_d(hi, lo, p.add_scale * (plane == 0 ? add.re[oa] : add.im[oa]));
+        if (ADD == SR_MAT_DD)
+          dd_add_dd(hi, lo, p.add_scale * (plane == 0 ? add.re[oa] : add.im[oa]),
+                    p.add_scale * (plane == 0 ? add.re_lo[oa] : add.im_lo[oa]));
+        const size_t o = (size_t)i * p.ld_out + j;
+        if (OUT == SR_MAT_F64) {
+          (plane == 0 ? out.re : out.im)[o] = hi + lo;
+        } else if (OUT == SR_MAT_DD) {
+          quick_two_sum(hi, lo, hi, lo);
+          (plane == 0 ? out.re : out.im)[o] = hi;
+          (plane == 0 ? out.re_lo : out.im_lo)[o] = lo;
+        } else if (OUT == SR_MAT_C64) {
+          reinterpret_cast<float*>(out.re)[2 * o + plane] = (float)(hi + lo);
         } else {
-          float* o = reinterpret_cast<float*>(out_re) + 2 * ((size_t)i * p.ld_out + j);
-          o[plane] = (float)v;
+          out.re[2 * o + plane] = hi + lo;
         }
       }
     }
   }
 }
 
+// Hermitian products are computed on the lower 128 x 128 tiles only; fill the
+// strictly-upper tiles with the conjugate transpose (smem-tiled, coalesced).
+// planes: (re, im) or dd (re, im, re_lo, im_lo); imaginary planes are negated.
+__global__ void __launch_bounds__(256) mirror_kernel(int n, Dst d, int nplanes, long long ld) {
+  __shared__ double t[32][33];
+  const int bi = blockIdx.y, bj = blockIdx.x;  // destination 32-tile (bi, bj), bj > bi
+  if ((bj >> 2) <= (bi >> 2)) return;           // only strictly-upper 128-tiles
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int q = 0; q < nplanes; ++q) {
+    double* pl = q == 0 ? d.re : (q == 1 ? d.im : (q == 2 ? d.re_lo : d.im_lo));
+    const double sgn = (q & 1) ? -1.0 : 1.0;
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {  // read source tile (bj, bi), coalesced
+      const int si = bj * 32 + r, sj = bi * 32 + tx;
+      if (si < n && sj < n) t[r][tx] = pl[(size_t)si * ld + sj];
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+      const int di = bi * 32 + r, dj = bj * 32 + tx;
+      if (di < n && dj < n) pl[(size_t)di * ld + dj] = sgn * t[tx][r];
+    }
+  }
+}
+
+template <int NC, int OUT, int ADD>
+void launch_decode(int grid, cudaStream_t st, const DecodeParams& p, const int8_t* res, const int* ea,
+                   const int* eb, Src add, Dst out) {
+  decode_kernel<NC, OUT, ADD><<<grid, 256, 0, st>>>(p, res, ea, eb, add, out);
+}
+
+template <int NC, int OUT>
+int dispatch_add(int add_kind, int grid, cudaStream_t st, const DecodeParams& p, const int8_t* res, const int* ea,
+                 const int* eb, Src add, Dst out) {
+  if (add_kind < 0)
+    launch_decode<NC, OUT, -1>(grid, st, p, res, ea, eb, add, out);
+  else if (add_kind == SR_MAT_F64)
+    launch_decode<NC, OUT, SR_MAT_F64>(grid, st, p, res, ea, eb, add, out);
+  else if (add_kind == SR_MAT_DD)
+    launch_decode<NC, OUT, SR_MAT_DD>(grid, st, p, res, ea, eb, add, out);
+  else
+    return SR_EINVAL;
+  return SR_OK;
+}
+
+template <int NC>
+int dispatch_out(int out_kind, int add_kind, int grid, cudaStream_t st, const DecodeParams& p, const int8_t* res,
+                 const int* ea, const int* eb, Src add, Dst out) {
+  switch (out_kind) {
+    case SR_MAT_F64:
+      return dispatch_add<NC, SR_MAT_F64>(add_kind, grid, st, p, res, ea, eb, add, out);
+    case SR_MAT_C64:
+      return dispatch_add<NC, SR_MAT_C64>(add_kind, grid, st, p, res, ea, eb, add, out);
+    case SR_MAT_C128:
+      return dispatch_add<NC, SR_MAT_C128>(add_kind, grid, st, p, res, ea, eb, add, out);
+    case SR_MAT_DD:
+      return dispatch_add<NC, SR_MAT_DD>(add_kind, grid, st, p, res, ea, eb, add, out);
+  }
+  return SR_EINVAL;
+}
+
 }  // namespace
 
-extern "C" int sr_oz_exponents(int rows, int cols, const void* src, const double* im, long long ld, int src_c64,
+extern "C" int sr_oz_exponents(int rows, int cols, int kind, const void* re, const double* im, long long ld,
                                int transposed, int* exps, void* stream) {
-  const double* re = (const double*)src;
-  if (rows < 0 || cols < 0 || !re || !exps) return SR_EINVAL;
+  if (rows < 0 || cols < 0 || !re || !exps || kind < 0 || kind > SR_MAT_DD) return SR_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  Src s{(const double*)re, im, nullptr, nullptr, kind};
+  if (kind == SR_MAT_DD) kind = SR_MAT_F64;  // the hi parts decide the scale
   if (!transposed) {
     if (rows == 0) return SR_OK;
-    exps_direct_kernel<<<sr_ceil_div((long long)rows * 32, 256), 256, 0, st>>>(rows, cols, re, im, ld, src_c64, exps);
+    const int grid = sr_ceil_div((long long)rows * 32, 256);
+    if (kind == SR_MAT_F64) exps_direct_kernel<SR_MAT_F64><<<grid, 256, 0, st>>>(rows, cols, s, ld, exps);
+    if (kind == SR_MAT_C64) exps_direct_kernel<SR_MAT_C64><<<grid, 256, 0, st>>>(rows, cols, s, ld, exps);
+    if (kind == SR_MAT_C128) exps_direct_kernel<SR_MAT_C128><<<grid, 256, 0, st>>>(rows, cols, s, ld, exps);
   } else {
     if (cols == 0) return SR_OK;
-    exps_transposed_kernel<<<sr_ceil_div(cols, 32), dim3(32, 8), 0, st>>>(rows, cols, re, im, ld, src_c64, exps);
+    exps_fill_kernel<<<sr_ceil_div(cols, 256), 256, 0, st>>>(cols, exps);
+    SR_LAUNCH_CHECK();
+    const int rpb = 256;
+    dim3 g(sr_ceil_div(cols, 32), sr_ceil_div(rows, rpb));
+    if (kind == SR_MAT_F64) exps_transposed_kernel<SR_MAT_F64><<<g, dim3(32, 8), 0, st>>>(rows, cols, s, ld, rpb, exps);
+    if (kind == SR_MAT_C64) exps_transposed_kernel<SR_MAT_C64><<<g, dim3(32, 8), 0, st>>>(rows, cols, s, ld, rpb, exps);
+    if (kind == SR_MAT_C128)
+      exps_transposed_kernel<SR_MAT_C128><<<g, dim3(32, 8), 0, st>>>(rows, cols, s, ld, rpb, exps);
   }
   SR_LAUNCH_CHECK();
   return SR_OK;
 }
 
-extern "C" int sr_oz_encode(int rows_out, int K, const void* src, const double* im, long long ld, int src_c64,
-                            int transposed, int conj, int layout, const int* exps, int beta, int nmod,
-                            const int* moduli, void* out, long long kpitch, void* stream) {
-  const double* re = (const double*)src;
+extern "C" int sr_oz_encode(int rows_out, int K, int kind, const void* re, const double* im, const double* re_lo,
+                            const double* im_lo, long long ld, int transposed, int conj, int layout,
+                            const int* exps, int beta, int nmod, const int* moduli, void* out, long long kpitch,
+                            void* stream) {
   if (rows_out <= 0 || K <= 0 || nmod <= 0 || nmod > MAXMOD || layout < 0 || layout > 2) return SR_EINVAL;
-  if (beta < 1 || beta > 61 || (kpitch & 15) || kpitch < K) return SR_EINVAL;
+  if (kind < 0 || kind > SR_MAT_DD || (kind == SR_MAT_DD && (!re_lo || !im_lo || !im))) return SR_EINVAL;
+  const int max_beta = kind == SR_MAT_DD ? 106 : 61;
+  if (beta < 1 || beta > max_beta || (kpitch & 15) || kpitch < K) return SR_EINVAL;
   EncodeParams p;
   memset(&p, 0, sizeof(p));
   p.rows_out = rows_out;
@@ -312,30 +504,63 @@ extern "C" int sr_oz_encode(int rows_out, int K, const void* src, const double* 
   p.nmod = nmod;
   p.ld = ld;
   p.kpitch = kpitch;
-  p.src_c64 = src_c64;
+  p.ndig = (beta + 2 + 10) / 11;  // digits covering |a| <= 2^beta plus a carry
+  if (p.ndig > MAXDIG) p.ndig = MAXDIG;
   for (int l = 0; l < nmod; ++l) {
-    if (moduli[l] < 129 || moduli[l] > 256) return SR_EINVAL;
-    p.moduli[l] = moduli[l];
-    p.inv[l] = 1.0 / moduli[l];
+    const int m = moduli[l];
+    if (m < 3 || m > 256) return SR_EINVAL;
+    p.pf[l] = (float)m;
+    p.invf[l] = 1.0f / (float)m;
+    p.hif[l] = (float)(((m + 1) >> 1) - 1);
+    p.lof[l] = (float)(-(m >> 1));
+    long long pw = 1;
+    for (int c = 0; c < MAXDIG; ++c) {
+      long long r = pw % m;
+      if (r > ((m + 1) >> 1) - 1) r -= m;
+      p.pow2[l][c] = (float)r;
+      pw = (pw << 11) % m;
+    }
   }
   // K padding columns of the residue planes must read as zero
   const int planes = layout == 0 ? 2 : (layout == 1 ? 3 : 1);
-  if (kpitch > K)
-    SR_CUDA_CHECK(cudaMemsetAsync(out, 0, (size_t)nmod * planes * rows_out * kpitch, (cudaStream_t)stream));
-  dim3 grid(sr_ceil_div(K, ETK), sr_ceil_div(rows_out, ETI));
-  encode_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(p, re, im, exps, (int8_t*)out);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (kpitch > K) SR_CUDA_CHECK(cudaMemsetAsync(out, 0, (size_t)nmod * planes * rows_out * kpitch, st));
+  Src s{(const double*)re, im, re_lo, im_lo, kind};
+  const int eti = kind == SR_MAT_DD ? 32 : 64;
+  dim3 grid(sr_ceil_div(K, 32), sr_ceil_div(rows_out, eti));
+  switch (kind) {
+    case SR_MAT_F64:
+      encode_kernel<SR_MAT_F64><<<grid, 256, 0, st>>>(p, s, exps, (int8_t*)out);
+      break;
+    case SR_MAT_C64:
+      encode_kernel<SR_MAT_C64><<<grid, 256, 0, st>>>(p, s, exps, (int8_t*)out);
+      break;
+    case SR_MAT_C128:
+      encode_kernel<SR_MAT_C128><<<grid, 256, 0, st>>>(p, s, exps, (int8_t*)out);
+      break;
+    default:
+      encode_kernel<SR_MAT_DD><<<grid, 256, 0, st>>>(p, s, exps, (int8_t*)out);
+  }
   SR_LAUNCH_CHECK();
   return SR_OK;
 }
 
-// table: [nmod][4] weights, [4] P chunks, [4] offsets (as doubles), inv_p  (9 + 4*nmod doubles)
+// table (host): [nmod][6] CRT weights, [6] modulus-product chunks, [6] chunk
+// offsets (as doubles), 1/P
 extern "C" int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* table, const void* res,
                             long long res_pitch, const int* exps_a, int beta_a, const int* exps_b, int beta_b,
-                            double alpha, double shift, const double* add_re, const double* add_im, long long ld_add,
-                            double add_scale, int out_kind, void* out_re, double* out_im, long long ld_out,
-                            void* stream) {
+                            double alpha, double shift, int add_kind, const double* add_re, const double* add_im,
+                            const double* add_re_lo, const double* add_im_lo, long long ld_add, double add_scale,
+                            int out_kind, void* out_re, double* out_im, double* out_re_lo, double* out_im_lo,
+                            long long ld_out, int hermitian, void* stream) {
   if (M <= 0 || N <= 0 || nmod <= 0 || nmod > MAXMOD || nchunk < 1 || nchunk > MAXCHUNK) return SR_EINVAL;
-  if (out_kind == 0 && !out_im) return SR_EINVAL;
+  if (res_pitch & 3) return SR_EINVAL;
+  if (out_kind < 0 || out_kind > SR_MAT_DD) return SR_EINVAL;
+  if ((out_kind == SR_MAT_F64 || out_kind == SR_MAT_DD) && !out_im) return SR_EINVAL;
+  if (out_kind == SR_MAT_DD && (!out_re_lo || !out_im_lo)) return SR_EINVAL;
+  if (add_kind >= 0 && !add_re) return SR_EINVAL;
+  if (hermitian && (M != N || (out_kind != SR_MAT_F64 && out_kind != SR_MAT_DD) || add_kind >= 0))
+    return SR_EINVAL;
   DecodeParams p;
   memset(&p, 0, sizeof(p));
   p.M = M;
@@ -344,8 +569,7 @@ extern "C" int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* ta
   p.nchunk = nchunk;
   p.beta_a = beta_a;
   p.beta_b = beta_b;
-  p.out_kind = out_kind;
-  p.has_add = add_re != nullptr;
+  p.hermitian = hermitian;
   p.res_pitch = res_pitch;
   p.res_plane = res_pitch * M;
   p.res_mod = p.res_plane * 2;
@@ -356,17 +580,40 @@ extern "C" int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* ta
   p.add_scale = add_scale;
   for (int l = 0; l < nmod; ++l)
     for (int j = 0; j < MAXCHUNK; ++j) p.w[l][j] = table[l * MAXCHUNK + j];
+  int off[MAXCHUNK];
   for (int j = 0; j < MAXCHUNK; ++j) {
     p.pc[j] = table[nmod * MAXCHUNK + j];
-    p.off[j] = (int)table[nmod * MAXCHUNK + MAXCHUNK + j];
+    off[j] = (int)table[nmod * MAXCHUNK + MAXCHUNK + j];
+    p.offv[j] = ldexp(1.0, off[j]);
+  }
+  for (int j = 1; j < MAXCHUNK; ++j) {
+    p.cw[j] = ldexp(1.0, off[j - 1] - off[j]);
+    p.icw[j] = ldexp(1.0, -(off[j - 1] - off[j]));
   }
   p.inv_p = table[nmod * MAXCHUNK + 2 * MAXCHUNK];
-  if (res_pitch & 3) return SR_EINVAL;
   const long long total = (long long)M * ((N + 3) / 4);
   int grid = (int)((total + 255) / 256);
   if (grid > 148 * 16) grid = 148 * 16;
-  decode_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(p, (const int8_t*)res, exps_a, exps_b, add_re, add_im,
-                                                        out_re, out_im);
+  cudaStream_t st = (cudaStream_t)stream;
+  Src add{add_re, add_im, add_re_lo, add_im_lo, add_kind};
+  Dst out{(double*)out_re, out_im, out_re_lo, out_im_lo};
+  int rc;
+  switch (nchunk) {
+    case 1:
+    case 2:
+    case 3:
+    case 4:
+      rc = dispatch_out<4>(out_kind, add_kind, grid, st, p, (const int8_t*)res, exps_a, exps_b, add, out);
+      break;
+    default:
+      rc = dispatch_out<6>(out_kind, add_kind, grid, st, p, (const int8_t*)res, exps_a, exps_b, add, out);
+  }
+  if (rc != SR_OK) return rc;
   SR_LAUNCH_CHECK();
+  if (hermitian) {
+    dim3 g(sr_ceil_div(N, 32), sr_ceil_div(M, 32));
+    mirror_kernel<<<g, 256, 0, st>>>(M, out, out_kind == SR_MAT_DD ? 4 : 2, ld_out);
+    SR_LAUNCH_CHECK();
+  }
   return SR_OK;
 }

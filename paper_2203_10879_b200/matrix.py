@@ -106,3 +106,60 @@ def lp_empty(rows, cols=None, device="cuda", dtype=torch.complex64):
     """Interleaved lp matrix (rows, ld) with an even leading dimension."""
     cols = rows if cols is None else cols
     return torch.empty((rows, even(max(cols, 1))), dtype=dtype, device=device)
+
+
+class DDPlanar:
+    """Double-double complex matrix on a CUDA device: two planar FP64 pairs,
+    hi = (re_hi, im_hi) and lo = (re_lo, im_lo), each entry a normalised pair
+    (|lo| <= ulp(hi) / 2).  The device counterpart of the reference's DDMatrix
+    (/root/reference/pkg/src/ddschur/ddmatrix.py:29-66): same four planes,
+    row-major instead of column-major."""
+
+    __slots__ = ("hi", "lo")
+
+    def __init__(self, hi, lo):
+        self.hi = hi
+        self.lo = lo
+
+    @classmethod
+    def empty(cls, rows, cols=None, device="cuda"):
+        return cls(ZPlanar.empty(rows, cols, device=device), ZPlanar.empty(rows, cols, device=device))
+
+    @classmethod
+    def from_any(cls, x, device="cuda"):
+        """Exact embedding (lo = 0) of a complex / real matrix, or a copy of
+        a 4-plane (re_hi, re_lo, im_hi, im_lo) tuple (DDMatrix.cells order)."""
+        if isinstance(x, DDPlanar):
+            return x
+        if isinstance(x, (tuple, list)) and len(x) == 4:
+            rh, rl, ih, il = (np.ascontiguousarray(c, dtype=np.float64) for c in x)
+            return cls(ZPlanar.from_any(rh + 1j * ih, device=device, force_complex=True),
+                       ZPlanar.from_any(rl + 1j * il, device=device, force_complex=True))
+        hi = ZPlanar.from_any(x, device=device, force_complex=True)
+        lo = ZPlanar.empty(hi.rows, hi.cols, device=device)
+        lo.re_buf.zero_()
+        lo.im_buf.zero_()
+        return cls(hi, lo)
+
+    @property
+    def rows(self):
+        return self.hi.rows
+
+    @property
+    def cols(self):
+        return self.hi.cols
+
+    @property
+    def shape(self):
+        return self.hi.shape
+
+    @property
+    def ld(self):
+        return self.hi.ld
+
+    def cells(self):
+        """(re_hi, re_lo, im_hi, im_lo) device views, DDMatrix.cells order."""
+        return self.hi.re, self.lo.re, self.hi.im, self.lo.im
+
+    def to_numpy_cells(self):
+        return tuple(c.cpu().numpy() for c in self.cells())

@@ -9,24 +9,30 @@ picks the smallest r with  prod(p_l) > 4 * 2K * 2^(beta_a + beta_b), so the
 CRT representative is unique with a 2-bit margin.
 
 Where it sits in the reference: it replaces matmul_hp / matmul_lp
-(/root/reference/pkg/src/ddschur/matmul.py:52-110) in FP64 mode and
-generalises the reference's own Ozaki-I dd path (_ozaki_gemm_hp,
-matmul.py:151-212), which splits into FP64 slices multiplied by BLAS.
+(/root/reference/pkg/src/ddschur/matmul.py:52-110) — in FP64 mode (hp = FP64,
+beta 60; lp = complex64, beta 26) and in dd mode (hp = double-double, beta
+104; lp = binary64, beta 55) — and generalises the reference's own Ozaki-I
+dd path (_ozaki_gemm_hp, matmul.py:151-212), which splits into FP64 slices
+multiplied by BLAS.
 """
 import math
 
+import numpy as np
 import torch
 
 from . import _lib
+from .matrix import DDPlanar
 
-# pairwise-coprime moduli, largest first (greedy from 256 down)
+# pairwise-coprime moduli <= 256, largest first (greedy from 256 down)
 MODULI = [256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193, 191, 181, 179, 173,
-          167, 163, 157, 151]
+          167, 163, 157, 151, 149, 139, 137, 131, 127, 113, 109, 107]
 CHUNK_BITS = 40
-MAXCHUNK = 4
+MAXCHUNK = 6
 
-HP_BETA = 60   # hp (FP64-mode) operands: every entry within 2^-7 of its row max is exact
-LP_BETA = 26   # lp (complex64) operands: complex64 significand + 2 guard bits
+HP_BETA = 60     # FP64-mode hp operands: every entry within 2^-7 of its row max is exact
+LP_BETA = 26     # FP64-mode lp (complex64) operands: significand + 2 guard bits
+DD_BETA = 102    # dd-mode hp operands (double-double; the stop rule is 10 n 2^-106 ||A||)
+DD_LP_BETA = 55  # dd-mode lp (binary64) operands
 
 
 class OzPlan:
@@ -68,8 +74,8 @@ class OzPlan:
         table += [float(o) for o in offs] + [0.0] * (MAXCHUNK - nchunk)
         table += [1.0 / float(P)]
         self.nchunk = nchunk
-        self.table = (torch.tensor(table, dtype=torch.float64)).numpy()
-        self._moduli_c = (torch.tensor(self.moduli, dtype=torch.int32)).numpy()
+        self.table = np.array(table, dtype=np.float64)
+        self._moduli_c = np.array(self.moduli, dtype=np.int32)
 
     def moduli_ptr(self):
         return self._moduli_c.ctypes.data
@@ -108,19 +114,24 @@ def _stream():
     return torch.cuda.current_stream().cuda_stream
 
 
-def _src(x):
-    """(ptr, im_ptr, ld, c64) for a ZPlanar or an interleaved complex64 tensor."""
+def mat_args(x):
+    """(kind, re, im, re_lo, im_lo, ld, device) for a ZPlanar, DDPlanar or an
+    interleaved complex64 / complex128 (rows, ld) tensor."""
     if isinstance(x, torch.Tensor):
-        return x.data_ptr(), None, x.shape[1], 1
-    return x.re_ptr(), x.im_ptr(), x.ld, 0
+        kind = _lib.SR_MAT_C64 if x.dtype == torch.complex64 else _lib.SR_MAT_C128
+        return kind, x.data_ptr(), None, None, None, x.shape[1], x.device
+    if isinstance(x, DDPlanar):
+        return (_lib.SR_MAT_DD, x.hi.re_ptr(), x.hi.im_ptr(), x.lo.re_ptr(), x.lo.im_ptr(), x.ld,
+                x.hi.re_buf.device)
+    return _lib.SR_MAT_F64, x.re_ptr(), x.im_ptr(), None, None, x.ld, x.re_buf.device
 
 
 def encode(x, rows, cols, role, pl, conj_t=False, out=None):
     """Encode op(X) as an A operand (role "a": rows x K, op = conj-transpose
     when conj_t) or X as a B operand (role "b": K = rows of X, output rows =
-    columns of X).  x: ZPlanar (FP64) or complex64 (rows, ld) tensor."""
-    ptr, im, ld, c64 = _src(x)
-    real = (im is None and not c64)
+    columns of X)."""
+    kind, re, im, re_lo, im_lo, ld, dev = mat_args(x)
+    real = kind == _lib.SR_MAT_F64 and im is None
     if role == "a":
         out_rows, K, transposed, layout, planes, beta = (cols, rows, 1, 0, 2, pl.beta_a) if conj_t else \
             (rows, cols, 0, 0, 2, pl.beta_a)
@@ -129,12 +140,11 @@ def encode(x, rows, cols, role, pl, conj_t=False, out=None):
         out_rows, K, transposed, beta = cols, rows, 1, pl.beta_b
         layout, planes = (2, 1) if real else (1, 3)
         conj = 0
-    dev = x.device if isinstance(x, torch.Tensor) else x.re_buf.device
     enc = out if out is not None else Encoded(out_rows, K, planes, beta, pl.nmod, dev)
     st = _stream()
-    _lib.call("sr_oz_exponents", rows, cols, ptr, im, ld, c64, transposed, enc.exps.data_ptr(), st)
-    _lib.call("sr_oz_encode", out_rows, K, ptr, im, ld, c64, transposed, conj, layout, enc.exps.data_ptr(),
-              beta, pl.nmod, pl.moduli_ptr(), enc.buf.data_ptr(), enc.kp, st)
+    _lib.call("sr_oz_exponents", rows, cols, kind, re, im, ld, transposed, enc.exps.data_ptr(), st)
+    _lib.call("sr_oz_encode", out_rows, K, kind, re, im, re_lo, im_lo, ld, transposed, conj, layout,
+              enc.exps.data_ptr(), beta, pl.nmod, pl.moduli_ptr(), enc.buf.data_ptr(), enc.kp, st)
     return enc
 
 
@@ -163,7 +173,7 @@ def timing_end():
     return ms, float(sum(o for _, _, o in recs)), len(recs)
 
 
-def gemm_residues(ea, eb, pl, res):
+def gemm_residues(ea, eb, pl, res, lower_only=False):
     if ea.K != eb.K:
         raise ValueError("inner dimensions disagree: %d vs %d" % (ea.K, eb.K))
     rec = _TIMING is not None
@@ -171,24 +181,27 @@ def gemm_residues(ea, eb, pl, res):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
     _lib.call("sr_oz_gemm_i8", ea.rows, eb.rows, ea.K, pl.nmod, pl.moduli_ptr(), ea.buf.data_ptr(), ea.planes,
-              ea.kp, eb.buf.data_ptr(), eb.planes, eb.kp, res.buf.data_ptr(), res.pitch, 0, _stream())
+              ea.kp, eb.buf.data_ptr(), eb.planes, eb.kp, res.buf.data_ptr(), res.pitch, 1 if lower_only else 0, 0,
+              _stream())
     if rec:
         e1.record()
         real_products = 4 if eb.planes == 3 else 2
-        _TIMING.append((e0, e1, 2.0 * ea.rows * eb.rows * ea.K * real_products * pl.nmod))
+        ops = 2.0 * ea.rows * eb.rows * ea.K * real_products * pl.nmod
+        if lower_only:  # executed tiles: the lower 128 x 128 tiles only
+            t = (ea.rows + 127) // 128
+            ops *= (t * (t + 1) / 2) / (t * t)
+        _TIMING.append((e0, e1, ops))
 
 
-def decode(res, ea, eb, pl, out, alpha=1.0, shift=0.0, add=None, add_scale=1.0):
-    """out: ZPlanar (FP64 planar) or complex64 (M, ld) tensor."""
-    if isinstance(out, torch.Tensor):
-        out_kind, o_re, o_im, ld_out = 1, out.data_ptr(), None, out.shape[1]
+def decode(res, ea, eb, pl, out, alpha=1.0, shift=0.0, add=None, add_scale=1.0, hermitian=False):
+    """out / add: ZPlanar, DDPlanar, or complex64 / complex128 (M, ld) tensors."""
+    o_kind, o_re, o_im, o_rl, o_il, ld_out, _ = mat_args(out)
+    if add is None:
+        a_kind, a_re, a_im, a_rl, a_il, ld_add = -1, None, None, None, None, 0
     else:
-        out_kind, o_re, o_im, ld_out = 0, out.re_ptr(), out.im_ptr(), out.ld
-    a_re = a_im = None
-    ld_add = 0
-    if add is not None:
-        a_re, a_im, ld_add = add.re_ptr(), add.im_ptr(), add.ld
+        a_kind, a_re, a_im, a_rl, a_il, ld_add, _ = mat_args(add)
     _lib.call("sr_oz_decode", res.M, res.N, pl.nmod, pl.nchunk, pl.table_ptr(), res.buf.data_ptr(), res.pitch,
-              ea.exps.data_ptr(), ea.beta, eb.exps.data_ptr(), eb.beta, float(alpha), float(shift), a_re, a_im,
-              ld_add, float(add_scale), out_kind, o_re, o_im, ld_out, _stream())
+              ea.exps.data_ptr(), ea.beta, eb.exps.data_ptr(), eb.beta, float(alpha), float(shift), a_kind, a_re,
+              a_im, a_rl, a_il, ld_add, float(add_scale), o_kind, o_re, o_im, o_rl, o_il, ld_out,
+              1 if hermitian else 0, _stream())
     return out

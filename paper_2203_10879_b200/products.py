@@ -100,9 +100,9 @@ class OzakiProducts:
         # the constant matrix A, B role (real A keeps one plane)
         self.eb_a = ozaki.encode(a, n, n, "b", hp)
 
-    def _hp(self, ea, eb, out, **kw):
-        ozaki.gemm_residues(ea, eb, self.hp, self.res)
-        ozaki.decode(self.res, ea, eb, self.hp, out, **kw)
+    def _hp(self, ea, eb, out, hermitian=False, **kw):
+        ozaki.gemm_residues(ea, eb, self.hp, self.res, lower_only=hermitian)
+        ozaki.decode(self.res, ea, eb, self.hp, out, hermitian=hermitian, **kw)
         _counters["hp_calls"] += 1
 
     def _lp(self, ea, eb, out):
@@ -115,7 +115,7 @@ class OzakiProducts:
         ws, hp, n = self.ws, self.hp, self.ws.n
         ozaki.encode(qhat, n, n, "a", hp, conj_t=True, out=self.ea_qh)
         ozaki.encode(qhat, n, n, "b", hp, out=self.eb_q)
-        self._hp(self.ea_qh, self.eb_q, ws.y, shift=-1.0)               # G - I
+        self._hp(self.ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True)  # G - I
         ozaki.encode(qhat, n, n, "a", hp, out=self.ea_x)
         ozaki.encode(ws.y, n, n, "b", hp, out=self.eb_s)
         self._hp(self.ea_x, self.eb_s, ws.q, alpha=-0.5, add=qhat)       # Q^ - Q^ (G - I) / 2
@@ -127,7 +127,7 @@ class OzakiProducts:
         self._hp(self.ea_qh, self.eb_a, ws.p)                            # P = Q^H A
         ozaki.encode(ws.p, n, n, "a", hp, out=self.ea_x)
         self._hp(self.ea_x, self.eb_q, ws.that)                          # T^ = P Q
-        self._hp(self.ea_qh, self.eb_q, ws.y, shift=-1.0)                # Y = Q^H Q - I
+        self._hp(self.ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True)  # Y = Q^H Q - I
 
     def update(self, restore_full_sigma):
         ws, hp, lp, n = self.ws, self.hp, self.lp, self.ws.n

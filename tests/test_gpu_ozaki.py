@@ -52,7 +52,7 @@ def test_oz_gemm_residues_bit_exact(M, N, K, cplx):
     out = torch.zeros((len(moduli), 2, M, pitch), dtype=torch.int8, device="cuda")
     mods = np.array(moduli, np.int32)
     _lib.call("sr_oz_gemm_i8", M, N, K, len(moduli), mods.ctypes.data, ad.data_ptr(), 2, kp, bd.data_ptr(), bp,
-              kp, out.data_ptr(), pitch, 0, torch.cuda.current_stream().cuda_stream)
+              kp, out.data_ptr(), pitch, 0, 0, torch.cuda.current_stream().cuda_stream)
     got = out.cpu().numpy()[:, :, :, :N].astype(np.int64)
     for l, p in enumerate(moduli):
         ar, ai = a[l, 0].astype(np.int64), a[l, 1].astype(np.int64)
@@ -76,7 +76,7 @@ def dd_exact(a, b):
     return (o[0] + o[1]) + 1j * (o[2] + o[3]), o
 
 
-def oz_product(x, y, trans=False, alpha=1.0, shift=0.0, beta=ozaki.HP_BETA):
+def oz_product(x, y, trans=False, alpha=1.0, shift=0.0, beta=ozaki.HP_BETA, hermitian=False):
     xm, ym = ZPlanar.from_any(x), ZPlanar.from_any(y)
     K = x.shape[0] if trans else x.shape[1]
     M = x.shape[1] if trans else x.shape[0]
@@ -85,9 +85,9 @@ def oz_product(x, y, trans=False, alpha=1.0, shift=0.0, beta=ozaki.HP_BETA):
     ea = ozaki.encode(xm, x.shape[0], x.shape[1], "a", pl, conj_t=trans)
     eb = ozaki.encode(ym, y.shape[0], y.shape[1], "b", pl)
     res = ozaki.ResidueBuffer(M, N, pl.nmod, "cuda")
-    ozaki.gemm_residues(ea, eb, pl, res)
+    ozaki.gemm_residues(ea, eb, pl, res, lower_only=hermitian)
     out = ZPlanar.empty(M, N)
-    ozaki.decode(res, ea, eb, pl, out, alpha=alpha, shift=shift)
+    ozaki.decode(res, ea, eb, pl, out, alpha=alpha, shift=shift, hermitian=hermitian)
     return out.to_numpy()
 
 
@@ -110,14 +110,16 @@ def test_oz_fp64_product_beats_blas(M, N, K, trans, b_real):
     assert e_oz <= max(2 * e_blas, 4 * 2.0 ** -53 * scale), (e_oz / scale, e_blas / scale)
 
 
-def test_oz_gram_minus_identity_is_accurate():
+@pytest.mark.parametrize("n,hermitian", [(200, False), (200, True), (300, True)])
+def test_oz_gram_minus_identity_is_accurate(n, hermitian):
     rng = np.random.default_rng(3)
-    n = 200
     q, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
     _, o = dd_exact(q.conj().T, q)
     exact = (o[0] - np.eye(n)) + o[1] + 1j * (o[2] + o[3])
-    got = oz_product(q, q, trans=True, shift=-1.0)
+    got = oz_product(q, q, trans=True, shift=-1.0, hermitian=hermitian)
     blas = q.conj().T @ q - np.eye(n)
+    if hermitian:
+        assert np.array_equal(got, got.conj().T)
     assert np.linalg.norm(got - exact) <= np.linalg.norm(blas - exact)
 
 

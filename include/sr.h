@@ -116,6 +116,29 @@ int sr_sigma_ns_f64(int n, const double* g_re, const double* g_im, long long ldg
    refine.py:324). */
 int sr_triu_inplace_f64(int n, double* re, double* im, long long ld, void* stream);
 
+/* ---- dd mode (hp = double-double planes, lp = complex128) ---- */
+
+/* sr_split_lp_c64 for dd mode: lp T, E complex128 from the hi planes of T^,
+   ||E||_F into *d_norm_e (stril_extract + frobenius_norm + to_lp). */
+int sr_split_lp_c128(int n, const double* that_re, const double* that_im, long long ldt, void* t_lp, void* e_lp,
+                     long long ld_lp, double* d_norm_e, void* ws, size_t ws_bytes, void* stream);
+
+/* sr_skew_c64 for complex128 (refine.py:296-297). */
+int sr_skew_c128(int n, const void* l, long long ld, void* w, double* d_norm_w, int* d_flags, void* ws,
+                 size_t ws_bytes, void* stream);
+
+/* interleaved complex128 copy of a planar FP64 pair (DDMatrix.to_lp,
+   ddmatrix.py:84-86, applied to the hi planes). */
+int sr_pack_c128(int m, int n, const double* re, const double* im, long long ld, void* out, long long ld_out,
+                 void* stream);
+
+/* Sigma of merged_update in double-double (orthogonal.py:191-201); w, yw,
+   w2, w3 (w2y, w2yw optional) complex128, Y and S dd planes. */
+int sr_sigma_merged_dd(int n, const void* w, const double* y_re_hi, const double* y_im_hi, const double* y_re_lo,
+                       const double* y_im_lo, long long ldy, const void* yw, const void* w2, const void* w3,
+                       const void* w2y, const void* w2yw, long long ld_lp, double* s_re_hi, double* s_im_hi,
+                       double* s_re_lo, double* s_im_lo, long long lds, int with_identity, void* stream);
+
 /* bytes of reduction workspace the norm kernels need */
 size_t sr_reduce_workspace_bytes(void);
 

@@ -41,6 +41,10 @@ SIGNATURES = {
     "sr_sigma_ns_f64": (_i, [_i, _p, _p, _ll, _p, _p, _ll, _p]),
     "sr_triu_inplace_f64": (_i, [_i, _p, _p, _ll, _p]),
     "sr_reduce_workspace_bytes": (_sz, []),
+    "sr_split_lp_c128": (_i, [_i, _p, _p, _ll, _p, _p, _ll, _p, _p, _sz, _p]),
+    "sr_skew_c128": (_i, [_i, _p, _ll, _p, _p, _p, _p, _sz, _p]),
+    "sr_pack_c128": (_i, [_i, _i, _p, _p, _ll, _p, _ll, _p]),
+    "sr_sigma_merged_dd": (_i, [_i, _p, _p, _p, _p, _p, _ll, _p, _p, _p, _p, _p, _ll, _p, _p, _p, _p, _ll, _i, _p]),
     "sr_oz_exponents": (_i, [_i, _i, _i, _p, _p, _ll, _i, _p, _p]),
     "sr_oz_encode": (_i, [_i, _i, _i, _p, _p, _p, _p, _ll, _i, _i, _i, _p, _i, _i, _p, _p, _ll, _p]),
     "sr_oz_gemm_i8": (_i, [_i, _i, _i, _i, _p, _p, _i, _ll, _p, _i, _ll, _p, _ll, _i, _i, _p]),

@@ -178,6 +178,121 @@ __global__ void triu_kernel(int n, double* re, double* im, long long ld) {
   }
 }
 
+// ---- dd mode (hp = double-double planes, lp = complex128) ---------------------
+
+// T^ (hi planes) -> lp T (upper incl. diagonal) and lp E (strictly lower),
+// complex128; ||E||_F of the hp values (the lo parts change it by < 2^-52).
+__global__ void split_lp_c128_kernel(int n, const double* __restrict__ tr, const double* __restrict__ ti,
+                                     long long ldt, double2* __restrict__ t_lp, double2* __restrict__ e_lp,
+                                     long long ld_lp, double* partials, unsigned int* counter, double* out) {
+  double acc = 0.0;
+  const long long total = (long long)n * n;
+  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    const double re = tr[(size_t)i * ldt + j], im = ti[(size_t)i * ldt + j];
+    const double2 v = make_double2(re, im), z = make_double2(0.0, 0.0);
+    if (i > j) {
+      acc += re * re + im * im;
+      e_lp[(size_t)i * ld_lp + j] = v;
+      t_lp[(size_t)i * ld_lp + j] = z;
+    } else {
+      e_lp[(size_t)i * ld_lp + j] = z;
+      t_lp[(size_t)i * ld_lp + j] = v;
+    }
+  }
+  finish_norm(acc, partials, counter, out);
+}
+
+__global__ void skew_c128_kernel(int n, const double2* __restrict__ l, long long ld, double2* __restrict__ w,
+                                 int* flags, double* partials, unsigned int* counter, double* out) {
+  double acc = 0.0;
+  bool bad = false;
+  const long long total = (long long)n * n;
+  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    const double2 a = l[(size_t)i * ld + j], b = l[(size_t)j * ld + i];
+    const double2 v = make_double2(a.x - b.x, a.y + b.y);  // l - conj(l^T), refine.py:296
+    w[(size_t)i * ld + j] = v;
+    if (!isfinite(a.x) || !isfinite(a.y)) bad = true;
+    acc += v.x * v.x + v.y * v.y;
+  }
+  if (bad) atomicOr(flags, SR_FLAG_NONFINITE);
+  finish_norm(acc, partials, counter, out);
+}
+
+__global__ void pack_c128_kernel(int m, int n, const double* __restrict__ re, const double* __restrict__ im,
+                                 long long ld, double2* __restrict__ out, long long ldo) {
+  const long long total = (long long)m * n;
+  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    out[(size_t)i * ldo + j] = make_double2(re[(size_t)i * ld + j], im[(size_t)i * ld + j]);
+  }
+}
+
+__device__ __forceinline__ void ew_two_sum(double a, double b, double& s, double& e) {
+  s = a + b;
+  const double bb = s - a;
+  e = (a - (s - bb)) + (b - bb);
+}
+__device__ __forceinline__ void ew_quick_two_sum(double a, double b, double& s, double& e) {
+  s = a + b;
+  e = b - (s - a);
+}
+// accurate dd sum (dd.py:96-104): (ah, al) + (bh, bl)
+__device__ __forceinline__ void ew_dd_add(double& ah, double& al, double bh, double bl) {
+  double s1, s2, t1, t2;
+  ew_two_sum(ah, bh, s1, s2);
+  ew_two_sum(al, bl, t1, t2);
+  s2 += t1;
+  ew_quick_two_sum(s1, s2, s1, s2);
+  s2 += t2;
+  ew_quick_two_sum(s1, s2, ah, al);
+}
+
+// Sigma' = S - 2I of merged_update in double-double, summed left to right as
+// the reference does (orthogonal.py:191-200); the binary64 terms are exact
+// embeddings: ((((2W) - Y) - YW) + W^2) + W^3 [+ W^2 Y + W^2 Y W] (+ 2I when
+// with_identity).
+__global__ void sigma_merged_dd_kernel(int n, const double2* __restrict__ w, const double* __restrict__ yrh,
+                                       const double* __restrict__ yih, const double* __restrict__ yrl,
+                                       const double* __restrict__ yil, long long ldy, const double2* __restrict__ yw,
+                                       const double2* __restrict__ w2, const double2* __restrict__ w3,
+                                       const double2* __restrict__ w2y, const double2* __restrict__ w2yw,
+                                       long long ldl, double* __restrict__ srh, double* __restrict__ sih,
+                                       double* __restrict__ srl, double* __restrict__ sil, long long lds,
+                                       double eye) {
+  const long long total = (long long)n * n;
+  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    const size_t o = (size_t)i * ldl + j, oy = (size_t)i * ldy + j;
+    const double2 wv = w[o];
+    double rh = (i == j ? eye : 0.0), rl = 0.0, ih = 0.0, il = 0.0;
+    ew_dd_add(rh, rl, 2.0 * wv.x, 0.0);
+    ew_dd_add(ih, il, 2.0 * wv.y, 0.0);
+    ew_dd_add(rh, rl, -yrh[oy], -yrl[oy]);
+    ew_dd_add(ih, il, -yih[oy], -yil[oy]);
+    const double2 a = yw[o], b = w2[o], c = w3[o];
+    ew_dd_add(rh, rl, -a.x, 0.0);
+    ew_dd_add(ih, il, -a.y, 0.0);
+    ew_dd_add(rh, rl, b.x, 0.0);
+    ew_dd_add(ih, il, b.y, 0.0);
+    ew_dd_add(rh, rl, c.x, 0.0);
+    ew_dd_add(ih, il, c.y, 0.0);
+    if (w2y) {  // restore_full_sigma (orthogonal.py:196-200)
+      const double2 d = w2y[o], e = w2yw[o];
+      ew_dd_add(rh, rl, d.x, 0.0);
+      ew_dd_add(ih, il, d.y, 0.0);
+      ew_dd_add(rh, rl, e.x, 0.0);
+      ew_dd_add(ih, il, e.y, 0.0);
+    }
+    const size_t os = (size_t)i * lds + j;
+    srh[os] = rh;
+    srl[os] = rl;
+    sih[os] = ih;
+    sil[os] = il;
+  }
+}
+
 inline int ew_grid(long long total) {
   long long b = (total + RT - 1) / RT;
   return (int)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
@@ -254,6 +369,53 @@ extern "C" int sr_triu_inplace_f64(int n, double* re, double* im, long long ld, 
   if (n < 0) return SR_EINVAL;
   if (n == 0) return SR_OK;
   triu_kernel<<<ew_grid((long long)n * n), RT, 0, (cudaStream_t)stream>>>(n, re, im, ld);
+  SR_LAUNCH_CHECK();
+  return SR_OK;
+}
+
+extern "C" int sr_split_lp_c128(int n, const double* that_re, const double* that_im, long long ldt, void* t_lp,
+                                void* e_lp, long long ld_lp, double* d_norm_e, void* ws, size_t ws_bytes,
+                                void* stream) {
+  if (n < 0 || !ws || ws_bytes < sr_reduce_workspace_bytes()) return SR_EINVAL;
+  RedWs r = red_ws(ws);
+  split_lp_c128_kernel<<<RBLOCKS, RT, 0, (cudaStream_t)stream>>>(n, that_re, that_im, ldt, (double2*)t_lp,
+                                                                  (double2*)e_lp, ld_lp, r.partials, r.counter,
+                                                                  d_norm_e);
+  SR_LAUNCH_CHECK();
+  return SR_OK;
+}
+
+extern "C" int sr_skew_c128(int n, const void* l, long long ld, void* w, double* d_norm_w, int* d_flags, void* ws,
+                            size_t ws_bytes, void* stream) {
+  if (n < 0 || !ws || ws_bytes < sr_reduce_workspace_bytes()) return SR_EINVAL;
+  RedWs r = red_ws(ws);
+  skew_c128_kernel<<<RBLOCKS, RT, 0, (cudaStream_t)stream>>>(n, (const double2*)l, ld, (double2*)w, d_flags,
+                                                              r.partials, r.counter, d_norm_w);
+  SR_LAUNCH_CHECK();
+  return SR_OK;
+}
+
+extern "C" int sr_pack_c128(int m, int n, const double* re, const double* im, long long ld, void* out,
+                            long long ld_out, void* stream) {
+  if (m < 0 || n < 0) return SR_EINVAL;
+  if ((long long)m * n == 0) return SR_OK;
+  pack_c128_kernel<<<ew_grid((long long)m * n), RT, 0, (cudaStream_t)stream>>>(m, n, re, im, ld, (double2*)out,
+                                                                               ld_out);
+  SR_LAUNCH_CHECK();
+  return SR_OK;
+}
+
+extern "C" int sr_sigma_merged_dd(int n, const void* w, const double* y_re_hi, const double* y_im_hi,
+                                  const double* y_re_lo, const double* y_im_lo, long long ldy, const void* yw,
+                                  const void* w2, const void* w3, const void* w2y, const void* w2yw, long long ld_lp,
+                                  double* s_re_hi, double* s_im_hi, double* s_re_lo, double* s_im_lo, long long lds,
+                                  int with_identity, void* stream) {
+  if (n < 0 || (w2y == nullptr) != (w2yw == nullptr)) return SR_EINVAL;
+  if (n == 0) return SR_OK;
+  sigma_merged_dd_kernel<<<ew_grid((long long)n * n), RT, 0, (cudaStream_t)stream>>>(
+      n, (const double2*)w, y_re_hi, y_im_hi, y_re_lo, y_im_lo, ldy, (const double2*)yw, (const double2*)w2,
+      (const double2*)w3, (const double2*)w2y, (const double2*)w2yw, ld_lp, s_re_hi, s_im_hi, s_re_lo, s_im_lo,
+      lds, with_identity ? 2.0 : 0.0);
   SR_LAUNCH_CHECK();
   return SR_OK;
 }

@@ -345,16 +345,23 @@ def refine_template(a, qhat, cfg=None, device=None):
         raise RuntimeError("refine_template needs a CUDA device (no CPU fallback)")
     device = torch.device("cuda") if device is None else torch.device(device)
     t0 = time.perf_counter()
+    if cfg.precision == "dd":
+        from . import dd_refine
+        a = dd_refine.coerce_dd(a, device)
+        qhat = dd_refine.coerce_dd(qhat, device)
+        if a.shape != qhat.shape:
+            raise ValueError("matrix and candidate shapes differ")
+        pair, report = dd_refine.run_dd(a, qhat, cfg, device)
+        torch.cuda.current_stream().synchronize()
+        report.wall_time = time.perf_counter() - t0
+        return pair, report
     a = _coerce(a, device)
     qhat = _coerce(qhat, device)
     if a.shape != qhat.shape:
         raise ValueError("matrix and candidate shapes differ")
     if qhat.is_real:
         qhat = ZPlanar.from_any(qhat.re, device=device, force_complex=True)
-    if cfg.precision == "dd":
-        from . import dd_refine
-        pair, report = dd_refine.run_dd(a, qhat, cfg, device)
-    else:
+    if True:
         ws = _workspace(a.rows, device)
         pair, report = _run_fp64(a, qhat, cfg, ws)
     torch.cuda.current_stream().synchronize()

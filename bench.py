@@ -13,9 +13,10 @@ copies of A, Q̂ and the device->host copies of Q, T inside the timed region.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-N > 1 (torchrun, one rank per GPU): every rank refines its own replica
-(seed = rank) — "replicas"; the time is the max over
-ranks.  --impl reference times the CPU oracle port of the reference loop
+N > 1 (torchrun, one rank per GPU): one refinement of the same matrix,
+every product sharded by output columns over the ranks with NCCL all-gathers
+(paper_2203_10879_b200/sharded.py) — strong scaling; the time
+is the max over ranks.  --impl reference times the CPU oracle port of the reference loop
 (oracle/refine_fp64.py: numpy BLAS + the C restatement of the reference
 solver) on a bounded sample of the same workload, on rank 0 only.
 """
@@ -102,7 +103,7 @@ def run_reference(args):
               % (SAMPLE_N, out["iterations"], SAMPLE_N))
     line = {"metric": METRIC, "value": v, "unit": "s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1000.0, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "config3: n=%d real Gaussian A, complex64-Schur start, FP32->FP64, "
                                    "stop relE<10u64 or 10 iters" % n, "n": n},
             "cpu_baseline": {"value": v, "unit": "s", "cores": cores(), "kind": "port", "sample": sample},
@@ -169,7 +170,7 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     n = args.n
-    a_np, q_np = workload(n, seed=rank)
+    a_np, q_np = workload(n, seed=0)
     A = ZPlanar.from_any(a_np, device=dev)
     Qh = ZPlanar.from_any(q_np.astype(np.complex128), device=dev)
     cfg = RefineConfig(precision="fp64", tol_factor=10.0 / n, max_iters=10, gemm=args.gemm)
@@ -180,8 +181,16 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    if world > 1:
+        from paper_2203_10879_b200.sharded import refine_template_distributed
+
+        def run(a, q):
+            return refine_template_distributed(a, q, cfg, device=dev)
+    else:
+        def run(a, q):
+            return refine_template(a, q, cfg, device=dev)
     for _ in range(max(args.warmup, 0)):
-        pair, rep = refine_template(A, Qh, cfg, device=dev)
+        pair, rep = run(A, Qh)
     barrier()
     # ---- timed region: K refinements, inputs resident in HBM (A 512 MB + Q^ 1 GB > 126 MB L2)
     sampler = ClockSampler(local)
@@ -193,7 +202,7 @@ def main():
     barrier()
     evs[0].record(st)
     for k in range(args.steps):
-        pair, rep = refine_template(A, Qh, cfg, device=dev)
+        pair, rep = run(A, Qh)
         evs[k + 1].record(st)
         reports.append(rep)
     barrier()
@@ -217,7 +226,7 @@ def main():
     for _ in range(max(1, min(args.steps, 3))):
         barrier()
         t0 = time.perf_counter()
-        pair, _r = refine_template(a_host, q_host, cfg, device=dev)
+        pair, _r = run(a_host, q_host)
         q_out.copy_(pair.q, non_blocking=True)
         t_out.copy_(pair.t, non_blocking=True)
         torch.cuda.synchronize()
@@ -248,18 +257,22 @@ def main():
     line = {
         "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded Philox Gaussian A; LAPACK complex64 Schur start)",
         "config": {"workload": "config3: n=%d real Gaussian A, complex64-Schur start, FP32->FP64, stop "
                                "relE<10u64 or 10 iters" % n, "n": n, "gemm": args.gemm,
-                   "parallelism": "replicas x%d" % world if world > 1 else "single GPU",
+                   "parallelism": "column-sharded products x%d (NCCL)" % world if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (A 512 MiB, Q 1 GiB)"},
         "result": {"status": rep.status.value, "iterations": k_it, "skip_fired": rep.skip_fired,
                    "final_relE": hist[-1][0] / norm_a, "final_ortho": hist[-1][1],
                    "hp_matmul_count": rep.hp_matmul_count, "step_ms": step_ms},
         "roofline": {"bound": "tensor", "kernel": "oz_gemm_kernel (tcgen05 kind::i8)",
                      "achieved": achieved, "peak": int8_peak, "unit": "TOP/s (int8)",
-                     "frac": (achieved / int8_peak) if achieved else None, "traffic": None,
+                     "frac": (achieved / int8_peak) if achieved else None,
+                     "traffic": 34.02e9 if n == 8192 else None,
+                     "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of one hp "
+                                       "complex launch at n=8192 (profiles/r1_oz_gemm_ncu.md); algorithmic operand "
+                                       "+ residue bytes of that launch: 8.4e9",
                      "launches": gemm_launches, "avg_launch_ms": gemm_ms / max(gemm_launches, 1),
                      "share_of_step": gemm_ms / total_ms if total_ms else None, "peak_source": peak_src,
                      "algorithmic_ops_per_launch": gemm_ops / max(gemm_launches, 1)},

@@ -102,8 +102,9 @@ int sr_skew_c64(int n, const void* l, long long ld, void* w, double* d_norm_w, i
    S = ((((2I + 2W) - Y) - YW) + W^2) + W^3 [+ W^2 Y + W^2 Y W].
    w, yw, w2, w3 (and optional w2y, w2yw, NULL to skip) are complex64.
    with_identity = 0 drops the 2I term (S' = S - 2I, used by the Ozaki path,
-   which forms Q S / 2 = Q + Q S' / 2 exactly). */
-int sr_sigma_merged_f64(int n, const void* w, const double* y_re, const double* y_im, long long ldy,
+   which forms Q S / 2 = Q + Q S' / 2 exactly).  n rows x cols columns (a
+   column block of S' in the sharded driver; cols == n with the identity). */
+int sr_sigma_merged_f64(int n, int cols, const void* w, const double* y_re, const double* y_im, long long ldy,
                         const void* yw, const void* w2, const void* w3, const void* w2y, const void* w2yw,
                         long long ld_lp, double* s_re, double* s_im, long long lds, int with_identity,
                         void* stream);
@@ -185,13 +186,15 @@ int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, const void* 
    (host): [nmod][6] CRT weights, [6] modulus-product chunks, [6] chunk
    offsets, 1/P.  hermitian: the residues hold only the lower 128-tiles
    (sr_oz_gemm_i8 with lower_only); the strictly upper tiles are written as
-   the conjugate transpose (out_kind SR_MAT_F64 or SR_MAT_DD, no add). */
+   the conjugate transpose (out_kind SR_MAT_F64 or SR_MAT_DD, no add).
+   diag_col0: the shift lands on entries (i, j) with i == j + diag_col0
+   (column blocks of a sharded product). */
 int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* table, const void* res, long long res_pitch,
                  const int* exps_a, int beta_a, const int* exps_b, int beta_b, double alpha, double shift,
                  int add_kind, const double* add_re, const double* add_im, const double* add_re_lo,
                  const double* add_im_lo, long long ld_add, double add_scale, int out_kind, void* out_re,
                  double* out_im, double* out_re_lo, double* out_im_lo, long long ld_out, int hermitian,
-                 void* stream);
+                 int diag_col0, void* stream);
 
 #ifdef __cplusplus
 }

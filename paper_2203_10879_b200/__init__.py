@@ -16,11 +16,13 @@ from .refine import (
     verify_pair,
 )
 from .trisolve import TriEqProblem, TriEqSolution, solve_block
+from .continuation import refine_continuation
+from .matrix import DDPlanar
 
 __version__ = "0.1.0"
 __all__ = [
     "NonFiniteError", "NormTooLarge", "NotSymmetric", "SeparationError", "counters", "matmul_hp",
     "matmul_lp", "reset_counters", "ZPlanar", "U_FP64", "U_HP", "OrthoStrategy", "RefineConfig",
     "RefineReport", "RefineStatus", "SchurPair", "refine_template", "verify_pair", "TriEqProblem",
-    "TriEqSolution", "solve_block",
+    "TriEqSolution", "solve_block", "refine_continuation", "DDPlanar",
 ]

@@ -37,7 +37,7 @@ SIGNATURES = {
     "sr_trisolve_c64": (_i, [_i, _p, _p, _ll, _p, _f, _p, _p, _p, _sz, _p]),
     "sr_trisolve_c128": (_i, [_i, _p, _p, _ll, _p, _d, _p, _p, _p, _sz, _p]),
     "sr_skew_c64": (_i, [_i, _p, _ll, _p, _p, _p, _p, _sz, _p]),
-    "sr_sigma_merged_f64": (_i, [_i, _p, _p, _p, _ll, _p, _p, _p, _p, _p, _ll, _p, _p, _ll, _i, _p]),
+    "sr_sigma_merged_f64": (_i, [_i, _i, _p, _p, _p, _ll, _p, _p, _p, _p, _p, _ll, _p, _p, _ll, _i, _p]),
     "sr_sigma_ns_f64": (_i, [_i, _p, _p, _ll, _p, _p, _ll, _p]),
     "sr_triu_inplace_f64": (_i, [_i, _p, _p, _ll, _p]),
     "sr_reduce_workspace_bytes": (_sz, []),
@@ -49,7 +49,7 @@ SIGNATURES = {
     "sr_oz_encode": (_i, [_i, _i, _i, _p, _p, _p, _p, _ll, _i, _i, _i, _p, _i, _i, _p, _p, _ll, _p]),
     "sr_oz_gemm_i8": (_i, [_i, _i, _i, _i, _p, _p, _i, _ll, _p, _i, _ll, _p, _ll, _i, _i, _p]),
     "sr_oz_decode": (_i, [_i, _i, _i, _i, _p, _p, _ll, _p, _i, _p, _i, _d, _d, _i, _p, _p, _p, _p, _ll, _d, _i,
-                          _p, _p, _p, _p, _ll, _i, _p]),
+                          _p, _p, _p, _p, _ll, _i, _i, _p]),
 }
 
 _lib = None

@@ -123,12 +123,12 @@ __global__ void skew_kernel(int n, const float2* __restrict__ l, long long ld, f
   finish_norm(acc, partials, counter, out);
 }
 
-__global__ void sigma_merged_kernel(int n, const float2* __restrict__ w, const double* __restrict__ yr,
+__global__ void sigma_merged_kernel(int rows, int n, const float2* __restrict__ w, const double* __restrict__ yr,
                                     const double* __restrict__ yi, long long ldy, const float2* __restrict__ yw,
                                     const float2* __restrict__ w2, const float2* __restrict__ w3,
                                     const float2* __restrict__ w2y, const float2* __restrict__ w2yw, long long ldl,
                                     double* __restrict__ sr, double* __restrict__ si, long long lds, double eye) {
-  const long long total = (long long)n * n;
+  const long long total = (long long)rows * n;
   for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
     int i = (int)(idx / n), j = (int)(idx % n);
     size_t o = (size_t)i * ldl + j;
@@ -343,14 +343,15 @@ extern "C" int sr_skew_c64(int n, const void* l, long long ld, void* w, double* 
   return SR_OK;
 }
 
-extern "C" int sr_sigma_merged_f64(int n, const void* w, const double* y_re, const double* y_im, long long ldy,
-                                   const void* yw, const void* w2, const void* w3, const void* w2y,
+extern "C" int sr_sigma_merged_f64(int n, int cols, const void* w, const double* y_re, const double* y_im,
+                                   long long ldy, const void* yw, const void* w2, const void* w3, const void* w2y,
                                    const void* w2yw, long long ld_lp, double* s_re, double* s_im, long long lds,
                                    int with_identity, void* stream) {
-  if (n < 0 || (w2y == nullptr) != (w2yw == nullptr)) return SR_EINVAL;
-  if (n == 0) return SR_OK;
-  sigma_merged_kernel<<<ew_grid((long long)n * n), RT, 0, (cudaStream_t)stream>>>(
-      n, (const float2*)w, y_re, y_im, ldy, (const float2*)yw, (const float2*)w2, (const float2*)w3,
+  if (n < 0 || cols < 0 || (w2y == nullptr) != (w2yw == nullptr)) return SR_EINVAL;
+  if (with_identity && cols != n) return SR_EINVAL;
+  if ((long long)n * cols == 0) return SR_OK;
+  sigma_merged_kernel<<<ew_grid((long long)n * cols), RT, 0, (cudaStream_t)stream>>>(
+      n, cols, (const float2*)w, y_re, y_im, ldy, (const float2*)yw, (const float2*)w2, (const float2*)w3,
       (const float2*)w2y, (const float2*)w2yw, ld_lp, s_re, s_im, lds, with_identity ? 2.0 : 0.0);
   SR_LAUNCH_CHECK();
   return SR_OK;

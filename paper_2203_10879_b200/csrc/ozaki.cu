@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
 
 // ---- decode -----------------------------------------------------------------
 struct DecodeParams {
-  int M, N, nmod, nchunk, beta_a, beta_b, hermitian;
+  int M, N, nmod, nchunk, beta_a, beta_b, hermitian, diag_col0;
   long long res_pitch, res_plane, res_mod, ld_out, ld_add;
   double alpha, shift, add_scale;
   double w[MAXMOD][MAXCHUNK];  // CRT weights, chunk j in units of 2^off[j]
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(256) decode_kernel(const __grid_constant__ Dec
         const int sc = -(rho + (p.beta_b - eb[j]));
         hi = scale2(hi, sc) * p.alpha;
         lo = scale2(lo, sc) * p.alpha;
-        if (plane == 0 && i == j && p.shift != 0.0) dd_add_d(hi, lo, p.shift);
+        if (plane == 0 && i == j + p.diag_col0 && p.shift != 0.0) dd_add_d(hi, lo, p.shift);
         const size_t oa = (size_t)i * p.ld_add + j;
         if (ADD == SR_MAT_F64) dd_add_d(hi, lo, p.add_scale * (plane == 0 ? add.re[oa] : add.im[oa]));
         if (ADD == SR_MAT_DD)
@@ -552,7 +552,7 @@ extern "C" int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* ta
                             double alpha, double shift, int add_kind, const double* add_re, const double* add_im,
                             const double* add_re_lo, const double* add_im_lo, long long ld_add, double add_scale,
                             int out_kind, void* out_re, double* out_im, double* out_re_lo, double* out_im_lo,
-                            long long ld_out, int hermitian, void* stream) {
+                            long long ld_out, int hermitian, int diag_col0, void* stream) {
   if (M <= 0 || N <= 0 || nmod <= 0 || nmod > MAXMOD || nchunk < 1 || nchunk > MAXCHUNK) return SR_EINVAL;
   if (res_pitch & 3) return SR_EINVAL;
   if (out_kind < 0 || out_kind > SR_MAT_DD) return SR_EINVAL;
@@ -570,6 +570,7 @@ extern "C" int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* ta
   p.beta_a = beta_a;
   p.beta_b = beta_b;
   p.hermitian = hermitian;
+  p.diag_col0 = diag_col0;
   p.res_pitch = res_pitch;
   p.res_plane = res_pitch * M;
   p.res_mod = p.res_plane * 2;

@@ -163,3 +163,40 @@ class DDPlanar:
 
     def to_numpy_cells(self):
         return tuple(c.cpu().numpy() for c in self.cells())
+
+
+class ColView:
+    """Columns j0..j1 of a ZPlanar, as a strided view with the parent's
+    leading dimension (the column block a rank owns in the sharded driver)."""
+
+    __slots__ = ("parent", "j0", "j1")
+
+    def __init__(self, parent, j0, j1):
+        self.parent, self.j0, self.j1 = parent, j0, j1
+
+    @property
+    def rows(self):
+        return self.parent.rows
+
+    @property
+    def cols(self):
+        return self.j1 - self.j0
+
+    @property
+    def ld(self):
+        return self.parent.ld
+
+    @property
+    def is_real(self):
+        return self.parent.is_real
+
+    @property
+    def re_buf(self):
+        return self.parent.re_buf
+
+    def re_ptr(self):
+        return self.parent.re_ptr() + 8 * self.j0
+
+    def im_ptr(self):
+        p = self.parent.im_ptr()
+        return None if p is None else p + 8 * self.j0

@@ -193,7 +193,7 @@ def gemm_residues(ea, eb, pl, res, lower_only=False):
         _TIMING.append((e0, e1, ops))
 
 
-def decode(res, ea, eb, pl, out, alpha=1.0, shift=0.0, add=None, add_scale=1.0, hermitian=False):
+def decode(res, ea, eb, pl, out, alpha=1.0, shift=0.0, add=None, add_scale=1.0, hermitian=False, diag_col0=0):
     """out / add: ZPlanar, DDPlanar, or complex64 / complex128 (M, ld) tensors."""
     o_kind, o_re, o_im, o_rl, o_il, ld_out, _ = mat_args(out)
     if add is None:
@@ -203,5 +203,5 @@ def decode(res, ea, eb, pl, out, alpha=1.0, shift=0.0, add=None, add_scale=1.0, 
     _lib.call("sr_oz_decode", res.M, res.N, pl.nmod, pl.nchunk, pl.table_ptr(), res.buf.data_ptr(), res.pitch,
               ea.exps.data_ptr(), ea.beta, eb.exps.data_ptr(), eb.beta, float(alpha), float(shift), a_kind, a_re,
               a_im, a_rl, a_il, ld_add, float(add_scale), o_kind, o_re, o_im, o_rl, o_il, ld_out,
-              1 if hermitian else 0, _stream())
+              1 if hermitian else 0, int(diag_col0), _stream())
     return out

@@ -29,7 +29,7 @@ def _sigma(ws, restore_full_sigma, with_identity):
     w2y = w2yw = None
     if restore_full_sigma:
         w2y, w2yw = ws.w2y.data_ptr(), ws.w2yw.data_ptr()
-    _lib.call("sr_sigma_merged_f64", n, ws.w_lp.data_ptr(), ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld,
+    _lib.call("sr_sigma_merged_f64", n, n, ws.w_lp.data_ptr(), ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld,
               ws.yw.data_ptr(), ws.w2.data_ptr(), ws.w3.data_ptr(), w2y, w2yw, ws.w_lp.shape[1],
               ws.sigma.re_ptr(), ws.sigma.im_ptr(), ws.sigma.ld, 1 if with_identity else 0, _stream())
 

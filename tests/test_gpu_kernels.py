@@ -162,7 +162,7 @@ def test_sigma_merged_matches_numpy():
     wd, ywd, w2d, w3d = dev(w), dev(yw), dev(w2), dev(w3)
     yz = ZPlanar.from_any(y)
     s = ZPlanar.empty(n)
-    _lib.call("sr_sigma_merged_f64", n, wd.data_ptr(), yz.re_ptr(), yz.im_ptr(), yz.ld, ywd.data_ptr(),
+    _lib.call("sr_sigma_merged_f64", n, n, wd.data_ptr(), yz.re_ptr(), yz.im_ptr(), yz.ld, ywd.data_ptr(),
               w2d.data_ptr(), w3d.data_ptr(), None, None, wd.shape[1], s.re_ptr(), s.im_ptr(), s.ld,
               1, torch.cuda.current_stream().cuda_stream)
     assert np.array_equal(s.to_numpy(), ref)

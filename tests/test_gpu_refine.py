@@ -127,3 +127,24 @@ def test_seed_determinism():
     p2, r2 = refine_template(a, q, cfg)
     assert r1.residual_history == r2.residual_history
     assert torch.equal(p1.q, p2.q)
+
+
+def test_config5_continuation_matches_oracle_chain():
+    """Config 5 shape (smaller n): A(t_j) = A0 + t_j A1, each step started from
+    the previous refined Q; the oracle runs the same chain on the CPU."""
+    from paper_2203_10879_b200 import refine_continuation
+    n, steps = 96, 5
+    a0, a1 = inputs.config5_pair(n, 0)
+    ts = [0.01 * j / 64 for j in range(steps)]
+    q0 = inputs.schur_vectors(a0).astype(np.complex128)
+    cfg = RefineConfig(precision="fp64", tol_factor=10.0 / n, max_iters=10)
+    chain = refine_continuation(a0, a1, ts, q0, cfg)
+    q = q0
+    for (t, pair, rep), tj in zip(chain, ts):
+        a = a0 + tj * a1
+        ref = refine_template_fp64(a, q, tol_factor=10.0 / n, max_iters=10)
+        q = ref["q"]
+        assert rep.status.value == ref["status"] == "Converged"
+        assert abs(rep.iterations - ref["iterations"]) <= 1
+        rel_e, ortho = residuals_fp64(a, pair.q.cpu().numpy())
+        assert rel_e <= 15 * U and ortho <= 2 * max(residuals_fp64(a, ref["q"])[1], 10 * np.sqrt(n) * U)

@@ -24,6 +24,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <stdlib.h>
+
 #include "sr_common.cuh"
 
 namespace {
@@ -32,7 +34,7 @@ constexpr int TM = 128, TN = 128, TK = 64;  // tile: 128 rows x 128 cols, 64-byt
 constexpr int STAGES = 5;
 constexpr int PLANE_BYTES = TM * TK;        // 8 KB per 128-row, 64-byte plane
 constexpr int NUM_THREADS = 192;
-constexpr int GROUP_M = 16;
+constexpr int GROUP_M = 8;  // M-tiles per rasterisation group (measured best with 2-CTA clusters)
 constexpr int MAX_MODULI = 32;
 
 struct OzParams {
@@ -40,6 +42,7 @@ struct OzParams {
   int a_planes, b_planes;
   int tiles_m, tiles_n;
   int lower_only;               // Hermitian product: only tiles with nt <= mt
+  int group_m;                  // work units per rasterisation group (L2 reuse of the A panel)
   long long out_pitch;          // bytes between output rows
   long long out_plane;          // bytes between output planes (re / im)
   long long out_mod;            // bytes between moduli
@@ -81,6 +84,27 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+// Same, multicast to every CTA of the cluster in cta_mask (same smem offset and
+// same mbarrier offset in each destination CTA).
+__device__ __forceinline__ void tma_load_4d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                               int c2, int c3, uint16_t cta_mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6], %7;\n" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar), "h"(cta_mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+
 // UMMA shared-memory descriptor: K-major, 64-byte swizzle, 8-row groups 512 B apart.
 __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
   uint64_t d = 0;
@@ -111,6 +135,14 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
                : "memory");
 }
+// arrive on the mbarrier at the same offset in every CTA of cta_mask
+__device__ __forceinline__ void umma_commit_mc(uint32_t bar, uint16_t cta_mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          bar),
+      "h"(cta_mask)
+      : "memory");
+}
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(
@@ -122,12 +154,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 
 __device__ __forceinline__ void decode_tile(const OzParams& p, int t, int& l, int& mt, int& nt) {
   const int per_mod = p.tiles_m * p.tiles_n;
+  const int G = p.group_m;
   l = t / per_mod;
   int r = t - l * per_mod;
-  const int group = r / (GROUP_M * p.tiles_n);
-  const int first_m = group * GROUP_M;
-  const int gm = min(GROUP_M, p.tiles_m - first_m);
-  const int in = r - group * GROUP_M * p.tiles_n;
+  const int group = r / (G * p.tiles_n);
+  const int first_m = group * G;
+  const int gm = min(G, p.tiles_m - first_m);
+  const int in = r - group * G * p.tiles_n;
   mt = first_m + in % gm;
   nt = in / gm;
 }
@@ -144,6 +177,13 @@ __device__ __forceinline__ int sym_mod(int v, int p, float inv) {
   return r;
 }
 
+// CM = 1: one CTA per tile.  CM = 2: clusters of two CTAs own vertically
+// adjacent M-tiles with the same N-tile; each CTA TMA-loads half the rows of
+// the shared B tile and multicasts it to both, halving the per-SM L2->SM
+// operand traffic (the L1TEX->XBAR request path is the measured limiter,
+// profiles/r1_oz_gemm_ncu.md).  A stage slot is refilled only after both
+// CTAs' MMAs released it (empty barriers count the two multicast commits).
+template <int CM>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                    const __grid_constant__ OzParams p, int8_t* __restrict__ out) {
@@ -165,7 +205,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full_bar(s), 1);
-      mbar_init(empty_bar(s), 1);
+      mbar_init(empty_bar(s), CM);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull_bar(b), 1);
@@ -181,27 +221,47 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  if (CM > 1) cluster_sync();  // peers' barriers are initialised before any multicast
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
 
-  const int total_tiles = p.nmod * p.tiles_m * p.tiles_n;
+  // work units: tiles (CM = 1) or vertical tile pairs (CM = 2), one per cluster
+  const int crank = CM > 1 ? (int)cluster_ctarank() : 0;
+  const int cid = blockIdx.x / CM, ncl = gridDim.x / CM;
+  OzParams pu = p;
+  pu.tiles_m = (p.tiles_m + CM - 1) / CM;
+  const int total_tiles = p.nmod * pu.tiles_m * p.tiles_n;
   const int kblocks = (p.K + TK - 1) / TK;
+  // a Hermitian (lower_only) unit is skipped only when every tile of it is
+  // strictly upper, so both CTAs of a cluster run identical pipelines
+  auto unit = [&](int t, int& l, int& mt, int& nt) -> bool {
+    int mp;
+    decode_tile(pu, t, l, mp, nt);
+    mt = mp * CM + crank;
+    return !(p.lower_only && nt > mp * CM + CM - 1);
+  };
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int t = cid; t < total_tiles; t += ncl) {
         int l, mt, nt;
-        decode_tile(p, t, l, mt, nt);
-        if (p.lower_only && nt > mt) continue;
+        if (!unit(t, l, mt, nt)) continue;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           uint8_t* st = smem + stage * stage_bytes;
           mbar_expect_tx(full_bar(stage), stage_bytes);
           tma_load_4d(smem_u32(st), &tmap_a, full_bar(stage), kb * TK, mt * TM, 0, l);
-          tma_load_4d(smem_u32(st + a_bytes), &tmap_b, full_bar(stage), kb * TK, nt * TN, 0, l);
+          if (CM == 1) {
+            tma_load_4d(smem_u32(st + a_bytes), &tmap_b, full_bar(stage), kb * TK, nt * TN, 0, l);
+          } else {
+            // this CTA's half of every B plane, multicast to the pair
+            for (int pl = 0; pl < p.b_planes; ++pl)
+              tma_load_4d_mc(smem_u32(st + a_bytes + pl * PLANE_BYTES + crank * (PLANE_BYTES / 2)), &tmap_b,
+                             full_bar(stage), kb * TK, nt * TN + crank * (TN / 2), pl, l, (uint16_t)0x3);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -217,11 +277,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      if (p.lower_only) {
+    for (int t = cid; t < total_tiles; t += ncl) {
+      {
         int l, mt, nt;
-        decode_tile(p, t, l, mt, nt);
-        if (nt > mt) continue;
+        if (!unit(t, l, mt, nt)) continue;
       }
       mbar_wait(tempty_bar(acc), acc_phase ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -248,7 +307,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               umma_i8(d + 128, aim, b, id128, acc_flag);
             }
           }
-          umma_commit(empty_bar(stage));
+          if (CM == 1)
+            umma_commit(empty_bar(stage));
+          else
+            umma_commit_mc(empty_bar(stage), (uint16_t)0x3);  // release the slot in both CTAs
           if (kb == kblocks - 1) umma_commit(tfull_bar(acc));
         }
         __syncwarp();
@@ -265,10 +327,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int ew = warp & 3;  // TMEM lane quadrant this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    for (int t = cid; t < total_tiles; t += ncl) {
       int l, mt, nt;
-      decode_tile(p, t, l, mt, nt);
-      if (p.lower_only && nt > mt) continue;
+      if (!unit(t, l, mt, nt)) continue;
       const int pm = p.moduli[l];
       const float inv = p.inv[l];
       mbar_wait(tfull_bar(acc), acc_phase);
@@ -310,6 +371,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  if (CM > 1) cluster_sync();  // no CTA leaves while its peer may still multicast into it
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base));
 }
@@ -327,12 +389,13 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // 4-d map over [nmod][planes][rows][kpitch] int8, box (64, 128, planes, 1).
-int make_map(CUtensorMap* map, const void* base, int K, int rows, int planes, int nmod, long long kpitch) {
+int make_map(CUtensorMap* map, const void* base, int K, int rows, int planes, int nmod, long long kpitch,
+             int box_rows, int box_planes) {
   auto enc = get_encode();
   if (!enc) return SR_ECUDA;
   cuuint64_t dims[4] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)planes, (cuuint64_t)nmod};
   cuuint64_t strides[3] = {(cuuint64_t)kpitch, (cuuint64_t)(kpitch * rows), (cuuint64_t)(kpitch * rows * planes)};
-  cuuint32_t box[4] = {(cuuint32_t)TK, (cuuint32_t)TM, (cuuint32_t)planes, 1};
+  cuuint32_t box[4] = {(cuuint32_t)TK, (cuuint32_t)box_rows, (cuuint32_t)box_planes, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -370,19 +433,46 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
     p.moduli[i] = moduli[i];
     p.inv[i] = 1.0f / (float)moduli[i];
   }
+  const int tiles = nmod * p.tiles_m * p.tiles_n;
+  int grid = num_sms > 0 ? num_sms : 148;
+  // clusters of two CTAs sharing the B tile whenever there are M-tile pairs to share
+  const int cm = (p.tiles_m >= 2 && grid >= 2 && !getenv("SR_OZ_NO_CLUSTER")) ? 2 : 1;
+  // 16 M-tiles (a 2 x 128 x K byte A panel each) per group keep the panel
+  // inside one die's half of the L2 while every N-tile streams past it
+  p.group_m = (getenv("SR_OZ_GROUP_M") ? atoi(getenv("SR_OZ_GROUP_M")) : GROUP_M) / cm;
+  if (p.group_m < 1) p.group_m = 1;
+  if (grid > tiles) grid = tiles;
+  grid -= grid % cm;
+  if (grid < cm) grid = cm;
   CUtensorMap ma, mb;
-  if (make_map(&ma, a, K, M, a_planes, nmod, a_kpitch) != SR_OK) return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(A)");
-  if (make_map(&mb, b, K, N, b_planes, nmod, b_kpitch) != SR_OK) return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(B)");
+  if (make_map(&ma, a, K, M, a_planes, nmod, a_kpitch, TM, a_planes) != SR_OK)
+    return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(A)");
+  if (make_map(&mb, b, K, N, b_planes, nmod, b_kpitch, TN / cm, cm == 1 ? b_planes : 1) != SR_OK)
+    return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(B)");
   const size_t smem = 1024 + (size_t)STAGES * (a_planes + b_planes) * PLANE_BYTES + 256;
   static bool configured = false;
   if (!configured) {
-    SR_CUDA_CHECK(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    SR_CUDA_CHECK(cudaFuncSetAttribute(oz_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    SR_CUDA_CHECK(cudaFuncSetAttribute(oz_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
-  const int tiles = nmod * p.tiles_m * p.tiles_n;
-  int grid = num_sms > 0 ? num_sms : 148;
-  if (grid > tiles) grid = tiles;
-  oz_gemm_kernel<<<grid, NUM_THREADS, smem, (cudaStream_t)stream>>>(ma, mb, p, (int8_t*)out);
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = cm;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  if (cm == 2)
+    SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<2>, ma, mb, p, (int8_t*)out));
+  else
+    SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<1>, ma, mb, p, (int8_t*)out));
   SR_LAUNCH_CHECK();
   return SR_OK;
 }

@@ -6,28 +6,42 @@
 //   _sylvester_tri        trisolve.py:164-196
 //   _scalar_solve_inplace trisolve.py:121-145
 //   _check_separation     trisolve.py:104-113
-// with a right-looking blocked wavefront over NB x NB tiles of L.  Tile
-// (I, J), I >= J, satisfies
+// with a blocked wavefront over NB x NB tiles of L.  Tile (I, J), I >= J,
+// satisfies
 //   T_II L_IJ - L_IJ T_JJ = R_IJ,
 //   R_IJ = -E_IJ - sum_{K>I} T_IK L_KJ + sum_{K<J} L_IK T_KJ
 // (stril() of both sides when I == J).  Tile (I, J) sits on anti-diagonal
-// level (N-1-I) + J and depends only on lower levels.  Launch `lev` of the
-// sweep owns every still-open tile that the tiles solved at level lev-1
-// contribute to — at most one column term (T_IK L_KJ) and one row term
-// (L_IJ T_JM) per tile, so each tile is updated by exactly one CTA and the
-// running right-hand side R lives in HBM with no atomics — and the CTAs whose
-// tile sits on level `lev` then solve it.  N launches per solve, each fully
-// parallel over the open tiles.
+// level (N-1-I) + J and depends only on tiles of lower levels, so launch
+// `lev` of the sweep solves every tile of level `lev` (one CTA each).
+//
+// The contributions of a solved tile (the "source") to the open tiles are
+// applied in one of three places, decided by the levels involved.  Levels are
+// grouped into batches of BW = 4; a source on level s (batch b = s / 4)
+//   * feeds the tiles of level s + 1 inside their SOLVE CTA (the critical path),
+//   * feeds the tiles of levels s + 2 .. 4b + 7 through the NEAR launch of
+//     level s + 1 (rank-NB tile updates, a narrow band of levels),
+//   * feeds every tile of level >= 4b + 8 through the FAR launches of batch b:
+//     once the four levels of batch b are solved, their sources for one column
+//     (row) of targets are four CONSECUTIVE tiles, so each target receives one
+//     rank-4NB update; the FAR launches run on their own stream, overlapped with
+//     the next four levels of SOLVE / NEAR, and write a second right-hand-side
+//     buffer (Rf) so they never race the near band's (Rn).
+// The far updates carry ~93 % of the n^3/3 complex multiply-adds, as register-
+// tiled complex GEMMs on the FP32 (FP64 in dd mode) pipe with cp.async double
+// buffering; the running right-hand sides are read and written once per batch
+// instead of once per level.
 //
 // The tile solve is one warp: lane i owns row i, and entry (i, j) is final at
 // step (NB-1-i) + j.  Each lane keeps its open entries in a 32-wide register
 // window that slides one column per step (fully unrolled, so the slide is
-// register renaming); at every step the lanes finalise one entry each,
+// register renaming); at every step the lanes finalise one entry each
+// (multiplying by a reciprocal pivot computed beforehand by the whole CTA),
 // exchange the new values with warp shuffles (the column terms) and fold
-// their own new value into their later columns (the row terms).  Clipping is
-// applied at finalisation as in the reference (trisolve.py:141-144,192-195),
-// so dependants see the clipped zero; any dependency-respecting order gives
-// the same L up to rounding.
+// their own new value into their later columns through a diagonal-major copy of
+// T_JJ (the row terms, conflict-free shared loads).  Clipping is applied at
+// finalisation as in the reference (trisolve.py:141-144,192-195), so
+// dependants see the clipped zero; any dependency-respecting order gives the
+// same L up to rounding.
 //
 // Templated on the lp type: float2 (FP64 mode, lp = complex64) and double2
 // (dd mode, lp = binary64 complex).
@@ -36,8 +50,10 @@
 namespace {
 
 constexpr int NB = 32;
-constexpr int NT = 128;  // 16 x 8 threads, each owning a 2 x 4 block of the tile
+constexpr int NT = 128;   // SOLVE / NEAR CTAs: 16 x 8 threads, each a 2 x 4 block of the tile
 constexpr int LD = NB + 1;
+constexpr int BW = 4;     // levels per far batch = tiles per far strip = source tiles per far update
+constexpr int FT = 256;   // FAR CTAs
 
 template <typename C>
 struct Real;
@@ -78,44 +94,77 @@ __device__ __forceinline__ double2 shfl_down(double2 v, int d) {
   return make_double2(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d));
 }
 
-// Load an NB x NB tile (rows r0.., cols c0..) with zero fill outside [0, n).
+// Asynchronous copy of a rows x cols block (global rows r0.., cols c0..; r0 or
+// c0 may be negative) into shared memory with row pitch `pitch` elements,
+// zero-filled outside [0, n) x [0, n).  16-byte copies when the global and the
+// shared rows are 16-byte aligned (complex128, or complex64 with an even ld
+// and an even pitch), else one element per copy.  The caller commits and waits.
 template <typename C>
-__device__ __forceinline__ void load_tile(C* s, const C* __restrict__ g, long long ld, int r0, int c0, int n) {
-  for (int idx = threadIdx.x; idx < NB * NB; idx += NT) {
-    int r = idx / NB, c = idx % NB;
-    int gr = r0 + r, gc = c0 + c;
-    s[r * LD + c] = (gr < n && gc < n) ? g[(size_t)gr * ld + gc] : czero<C>();
+__device__ __forceinline__ void load_block_async(C* s, int pitch, const C* __restrict__ g, long long ld, int r0,
+                                                 int c0, int rows, int cols, int n, int tid, int nthreads) {
+  constexpr int EPV = 16 / (int)sizeof(C);  // elements per 16-byte copy
+  const bool vec = EPV == 1 || ((ld % 2) == 0 && (pitch % 2) == 0);
+  if (vec) {
+    const int per_row = cols / EPV;
+    for (int idx = tid; idx < rows * per_row; idx += nthreads) {
+      const int r = idx / per_row, c = (idx % per_row) * EPV;
+      const int gr = r0 + r, gc = c0 + c;
+      int valid = (gr >= 0 && gr < n && gc >= 0) ? min(EPV, n - gc) : 0;
+      valid = valid < 0 ? 0 : valid;
+      const C* src = g + (valid ? (size_t)gr * ld + gc : 0);
+      cp_async_16(s + r * pitch + c, src, valid * (int)sizeof(C));
+    }
+  } else {
+    for (int idx = tid; idx < rows * cols; idx += nthreads) {
+      const int r = idx / cols, c = idx % cols;
+      const int gr = r0 + r, gc = c0 + c;
+      const bool ok = gr >= 0 && gr < n && gc >= 0 && gc < n;
+      const C* src = g + (ok ? (size_t)gr * ld + gc : 0);
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s + r * pitch + c);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0));
+    }
   }
 }
 
-// Same, as asynchronous copies (cp.async, zero-filled outside [0, n)); the
-// caller commits and waits once for all the tiles it issued.
 template <typename C>
-__device__ __forceinline__ void load_tile_async(C* s, const C* __restrict__ g, long long ld, int r0, int c0,
-                                                int n) {
-  for (int idx = threadIdx.x; idx < NB * NB; idx += NT) {
-    const int r = idx / NB, c = idx % NB;
-    const int gr = r0 + r, gc = c0 + c;
-    const bool ok = gr < n && gc < n;
-    const C* src = g + (ok ? (size_t)gr * ld + gc : 0);
-    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s + r * LD + c);
-    if (sizeof(C) == 16)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
-    else
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0));
-  }
+__device__ __forceinline__ void load_tile_async(C* s, const C* __restrict__ g, long long ld, int r0, int c0, int n) {
+  load_block_async<C>(s, LD, g, ld, r0, c0, NB, NB, n, threadIdx.x, NT);
 }
 
 struct SweepArgs {
-  int n, N, lev, countA;
+  int n, N, lev, lmax;
   long long ld;
 };
 
-// In-tile solve by one warp: T2 X - X T1 = R (strict lower part only when diag).
+// acc (2 x 4 block of the tile per thread) -= A B (col term) / += A B (row term)
+template <typename C, bool ADD>
+__device__ __forceinline__ void tile_mac(C (&acc)[2][4], const C* sA, const C* sB, int ty, int tx) {
+#pragma unroll 8
+  for (int k = 0; k < NB; ++k) {
+    const C a0 = sA[(2 * ty) * LD + k], a1 = sA[(2 * ty + 1) * LD + k];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const C b = sB[k * LD + 4 * tx + c];
+      if (ADD) {
+        cfma(acc[0][c], a0, b);
+        cfma(acc[1][c], a1, b);
+      } else {
+        cfms(acc[0][c], a0, b);
+        cfms(acc[1][c], a1, b);
+      }
+    }
+  }
+}
+
+// In-tile solve by warp 0: T2 X - X T1 = R (strict lower part only when DIAG).
+// sP[i][j] = 1 / (T2_ii - T1_jj); sD[d][j] = T1[j][j + d].
 template <typename C, bool DIAG>
-__device__ __forceinline__ void tile_solve_warp(const C* sT2, const C* sT1, const C* sR, C* sX, int valid_i,
-                                                int valid_j, typename Real<C>::T clip, unsigned int* s_clip) {
+__device__ __forceinline__ unsigned tile_solve_warp(const C* sT2, const C* sD, const C* sP, const C* sR, C* sX,
+                                                    int valid_i, int valid_j, typename Real<C>::T clip) {
+  using R = typename Real<C>::T;
   const int i = threadIdx.x & 31;
+  const R clip2 = clip * clip;
+  unsigned nclip = 0;
   C pend[NB];
   C tr[NB];
 #pragma unroll
@@ -124,21 +173,16 @@ __device__ __forceinline__ void tile_solve_warp(const C* sT2, const C* sT1, cons
     pend[d] = (c >= 0) ? sR[i * LD + c] : czero<C>();
     tr[d] = (i + d < NB) ? sT2[i * LD + i + d] : czero<C>();
   }
-  const C tii = tr[0];
-#pragma unroll
+#pragma unroll 1
   for (int t = 0; t < 2 * NB - 1; ++t) {
     const int j = t - (NB - 1) + i;  // this lane's column at step t
     const bool valid = (j >= 0) && (j < NB) && (i < valid_i) && (j < valid_j) && (!DIAG || i > j);
     C x = czero<C>();
     if (valid) {
-      const C tjj = sT1[j * LD + j];
-      C piv;
-      piv.x = tii.x - tjj.x;
-      piv.y = tii.y - tjj.y;
-      x = cdiv(pend[0], piv);
-      if (clip > 0 && sqrt(x.x * x.x + x.y * x.y) > clip) {
+      x = cmul(pend[0], sP[i * LD + j]);
+      if (clip > 0 && x.x * x.x + x.y * x.y > clip2) {
         x = czero<C>();
-        if (threadIdx.x < 32) atomicAdd(s_clip, 1u);
+        ++nclip;
       }
       sX[i * LD + j] = x;
     }
@@ -152,7 +196,7 @@ __device__ __forceinline__ void tile_solve_warp(const C* sT2, const C* sT1, cons
     if (valid) {
 #pragma unroll
       for (int d = 1; d < NB; ++d)
-        if (j + d < NB) cfma(pend[d], x, sT1[j * LD + j + d]);
+        if (j + d < NB) cfma(pend[d], x, sD[d * NB + j]);
     }
     // slide the window one column to the right
 #pragma unroll
@@ -162,55 +206,35 @@ __device__ __forceinline__ void tile_solve_warp(const C* sT2, const C* sT1, cons
       pend[NB - 1] = (c < NB) ? sR[i * LD + c] : czero<C>();
     }
   }
+  return nclip;
 }
 
-// SOLVE = true: one CTA per tile on level `lev` (blockIdx.x = its column M):
-//   fold in the level-(lev-1) contributions, then solve the tile (critical path).
-// SOLVE = false: one CTA per open tile above level `lev` that level lev-1
-//   feeds: fold in the contributions, write R back (bulk work, runs on a
-//   second stream concurrently with the SOLVE launch of the same level).
-template <typename C, bool SOLVE>
-__global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs p, const C* __restrict__ T, C* __restrict__ R,
-                                                   C* __restrict__ L, typename Real<C>::T clip,
+// SOLVE launch of level `lev`: one CTA per tile (M + N - 1 - lev, M).  Folds in
+// the level lev-1 sources, adds the two right-hand-side buffers and solves.
+template <typename C>
+__global__ void __launch_bounds__(NT) solve_kernel(SweepArgs p, const C* __restrict__ T, const C* __restrict__ Rn,
+                                                   const C* __restrict__ Rf, C* __restrict__ L,
+                                                   typename Real<C>::T clip,
                                                    unsigned long long* __restrict__ clipped) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* s0 = reinterpret_cast<C*>(smem_raw);  // 5 tiles of NB x LD
-  C* s1 = s0 + NB * LD;
+  C* sR = reinterpret_cast<C*>(smem_raw);  // 9 tiles of NB x LD + one NB x NB
+  C* sRf = sR + NB * LD;
+  C* s1 = sRf + NB * LD;
   C* s2 = s1 + NB * LD;
   C* s3 = s2 + NB * LD;
   C* s4 = s3 + NB * LD;
-  __shared__ unsigned int s_clip;
+  C* sT2 = s4 + NB * LD;
+  C* sT1 = sT2 + NB * LD;
+  C* sP = sT1 + NB * LD;
+  C* sD = sP + NB * LD;
   const int N = p.N, lev = p.lev, n = p.n;
   const long long ld = p.ld;
-  // ---- which open tile (I, M) this CTA owns
-  int I, M;
-  if (SOLVE) {  // tile (M + N - 1 - lev, M) on level lev
-    M = blockIdx.x;
-    I = M + N - 1 - lev;
-  } else if ((int)blockIdx.x < p.countA) {  // region A: M <= lev-1, I in [M, M + N - lev - 1]
-    const int h = N - lev;
-    M = blockIdx.x / h;
-    I = M + blockIdx.x % h;
-  } else {  // region B: I = N-lev+r, M in [lev, N-lev+r]
-    int rem = blockIdx.x - p.countA, r = 0;
-    while (true) {
-      const int cnt = N - 2 * lev + r + 1;
-      if (cnt > 0) {
-        if (rem < cnt) break;
-        rem -= cnt;
-      }
-      ++r;
-    }
-    M = lev + rem;
-    I = N - lev + r;
-  }
-  const int tlev = (N - 1 - I) + M;
-  if (!SOLVE && tlev == lev) return;  // owned by the SOLVE launch
+  const int M = blockIdx.x, I = M + N - 1 - lev;
   const bool has_col = lev >= 1 && M <= lev - 1;
   const bool has_row = lev >= 1 && I >= N - lev;
   const int tid = threadIdx.x;
-  // ---- load R_IM and the contributing tiles
-  load_tile_async(s0, R, ld, I * NB, M * NB, n);
+  load_tile_async(sR, Rn, ld, I * NB, M * NB, n);
+  load_tile_async(sRf, Rf, ld, I * NB, M * NB, n);
   if (has_col) {
     const int K = M + N - lev;
     load_tile_async(s1, T, ld, I * NB, K * NB, n);  // T_IK
@@ -221,96 +245,263 @@ __global__ void __launch_bounds__(NT) sweep_kernel(SweepArgs p, const C* __restr
     load_tile_async(s3, L, ld, I * NB, J * NB, n);  // L_IJ
     load_tile_async(s4, T, ld, J * NB, M * NB, n);  // T_JM
   }
-  if (SOLVE) {  // the diagonal blocks for the tile solve, behind a separate group
-    asm volatile("cp.async.commit_group;\n" ::);
-  }
-  if (tid == 0) s_clip = 0;
-  asm volatile("cp.async.commit_group;\n" ::);
-  asm volatile("cp.async.wait_all;\n" ::);
+  load_tile_async(sT2, T, ld, I * NB, I * NB, n);  // T_II
+  load_tile_async(sT1, T, ld, M * NB, M * NB, n);  // T_MM
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
-  if (has_col || has_row) {
+  {
     const int ty = tid / 8, tx = tid % 8;  // rows 2ty..2ty+1, cols 4tx..4tx+3
     C acc[2][4];
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) acc[a][c] = s0[(2 * ty + a) * LD + 4 * tx + c];
-    if (has_col) {
-#pragma unroll 8
-      for (int k = 0; k < NB; ++k) {
-        C a0 = s1[(2 * ty) * LD + k], a1 = s1[(2 * ty + 1) * LD + k];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          C b = s2[k * LD + 4 * tx + c];
-          cfms(acc[0][c], a0, b);
-          cfms(acc[1][c], a1, b);
-        }
+      for (int c = 0; c < 4; ++c) {
+        const int o = (2 * ty + a) * LD + 4 * tx + c;
+        acc[a][c].x = sR[o].x + sRf[o].x;
+        acc[a][c].y = sR[o].y + sRf[o].y;
       }
-    }
-    if (has_row) {
-#pragma unroll 8
-      for (int k = 0; k < NB; ++k) {
-        C a0 = s3[(2 * ty) * LD + k], a1 = s3[(2 * ty + 1) * LD + k];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          C b = s4[k * LD + 4 * tx + c];
-          cfma(acc[0][c], a0, b);
-          cfma(acc[1][c], a1, b);
-        }
-      }
-    }
-    if (!SOLVE) {  // still open: write the updated right-hand side back
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int gi = I * NB + 2 * ty + a, gj = M * NB + 4 * tx + c;
-          if (gi < n && gj < n) R[(size_t)gi * ld + gj] = acc[a][c];
-        }
-      return;
-    }
-    __syncthreads();  // everyone is done reading s0 before it is overwritten
+    if (has_col) tile_mac<C, false>(acc, s1, s2, ty, tx);
+    if (has_row) tile_mac<C, true>(acc, s3, s4, ty, tx);
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) s0[(2 * ty + a) * LD + 4 * tx + c] = acc[a][c];
+      for (int c = 0; c < 4; ++c) sRf[(2 * ty + a) * LD + 4 * tx + c] = acc[a][c];  // sRf is not read again
+    // reciprocal pivots and the diagonal-major copy of T_MM
+    for (int idx = tid; idx < NB * NB; idx += NT) {
+      const int i = idx / NB, j = idx % NB;
+      C d;
+      d.x = sT2[i * LD + i].x - sT1[j * LD + j].x;
+      d.y = sT2[i * LD + i].y - sT1[j * LD + j].y;
+      C one;
+      one.x = 1;
+      one.y = 0;
+      sP[i * LD + j] = cdiv(one, d);
+      // idx = dd * NB + jj: sD[dd][jj] = T1[jj][jj + dd]
+      sD[idx] = (i + j < NB) ? sT1[j * LD + j + i] : czero<C>();
+    }
   }
-  if (!SOLVE) return;
-  // ---- solve the tile: T_II X - X T_MM = R_IM
   __syncthreads();
-  load_tile(s1, T, ld, I * NB, I * NB, n);  // T_II
-  load_tile(s2, T, ld, M * NB, M * NB, n);  // T_MM
-  __syncthreads();
+  if (tid >= 32) return;
   const int vi = min(NB, n - I * NB), vj = min(NB, n - M * NB);
-  // every warp runs the (identical) tile solve: keeping the shuffles outside any
-  // thread-dependent branch lets them compile to plain SHFL instead of
-  // convergence-barrier sequences; all warps store the same values
+  const auto cl = clip;
+  unsigned nclip;
   if (I == M)
-    tile_solve_warp<C, true>(s1, s2, s0, s3, vi, vj, clip, &s_clip);
+    nclip = tile_solve_warp<C, true>(sT2, sD, sP, sRf, s1, vi, vj, cl);
   else
-    tile_solve_warp<C, false>(s1, s2, s0, s3, vi, vj, clip, &s_clip);
-  __syncthreads();
-  for (int idx = tid; idx < NB * NB; idx += NT) {
-    const int i = idx / NB, j = idx % NB;
-    const int gi = I * NB + i, gj = M * NB + j;
-    if (gi < n && gj < n) L[(size_t)gi * ld + gj] = (I == M && i <= j) ? czero<C>() : s3[i * LD + j];
+    nclip = tile_solve_warp<C, false>(sT2, sD, sP, sRf, s1, vi, vj, cl);
+  __syncwarp();
+  const int gj = M * NB + tid;
+  for (int r = 0; r < NB; ++r) {
+    const int gi = I * NB + r;
+    if (gi < n && gj < n) L[(size_t)gi * ld + gj] = (I == M && r <= tid) ? czero<C>() : s1[r * LD + tid];
   }
-  if (tid == 0 && s_clip) atomicAdd(clipped, (unsigned long long)s_clip);
+  nclip = __reduce_add_sync(0xffffffffu, nclip);
+  if (tid == 0 && nclip) atomicAdd(clipped, (unsigned long long)nclip);
 }
 
-// R = -stril(E) (only the strictly lower part is ever read), L = 0.
+// NEAR launch of level `lev` (sources: the tiles solved at level lev-1): one
+// CTA per tile on levels lev+1 .. lmax (blockIdx.y = level - lev - 1,
+// blockIdx.x = column M <= level), rank-NB update of Rn in place.
 template <typename C>
-__global__ void init_kernel(int n, const C* __restrict__ E, C* __restrict__ R, C* __restrict__ L, long long ld) {
+__global__ void __launch_bounds__(NT) near_kernel(SweepArgs p, const C* __restrict__ T, C* __restrict__ Rn,
+                                                  const C* __restrict__ L) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* s0 = reinterpret_cast<C*>(smem_raw);  // 5 tiles of NB x LD
+  C* s1 = s0 + NB * LD;
+  C* s2 = s1 + NB * LD;
+  C* s3 = s2 + NB * LD;
+  C* s4 = s3 + NB * LD;
+  const int N = p.N, lev = p.lev, n = p.n;
+  const long long ld = p.ld;
+  const int level = lev + 1 + blockIdx.y;
+  const int M = blockIdx.x;
+  if (M > level) return;
+  const int I = M + N - 1 - level;
+  const bool has_col = M <= lev - 1;   // source (K, M), K = M + N - lev
+  const bool has_row = I >= N - lev;   // source (I, J), J = I - N + lev
+  if (!has_col && !has_row) return;
+  const int tid = threadIdx.x;
+  load_tile_async(s0, Rn, ld, I * NB, M * NB, n);
+  if (has_col) {
+    const int K = M + N - lev;
+    load_tile_async(s1, T, ld, I * NB, K * NB, n);
+    load_tile_async(s2, L, ld, K * NB, M * NB, n);
+  }
+  if (has_row) {
+    const int J = I - N + lev;
+    load_tile_async(s3, L, ld, I * NB, J * NB, n);
+    load_tile_async(s4, T, ld, J * NB, M * NB, n);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  const int ty = tid / 8, tx = tid % 8;
+  C acc[2][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = s0[(2 * ty + a) * LD + 4 * tx + c];
+  if (has_col) tile_mac<C, false>(acc, s1, s2, ty, tx);
+  if (has_row) tile_mac<C, true>(acc, s3, s4, ty, tx);
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int gi = I * NB + 2 * ty + a, gj = M * NB + 4 * tx + c;
+      if (gi < n && gj < n) Rn[(size_t)gi * ld + gj] = acc[a][c];
+    }
+}
+
+struct FarArgs {
+  int n, N, beta, h, first;  // h = targets per source line; first = first column (COL) / row (ROW)
+  long long ld;
+};
+
+// FAR launch of batch `beta` (sources: the tiles of levels 4b .. 4b+3).
+//   COL (ROW = false): blockIdx.y -> column M = first + y (M <= 4b+3); the
+//     sources of column M are K = M+N-4b-4 .. M+N-4b-1, the targets its tiles
+//     I = M .. M+h-1 (levels >= 4b+8, h = N-4b-8).  CTA = strip of BW target
+//     tiles (BW NB x NB rows): Rf[strip, M] -= T[strip, Ks] L[Ks, M].
+//   ROW (ROW = true): blockIdx.y -> row I = first + y (I >= N-4b-4); sources
+//     J = I-N+1+4b .. I-N+4+4b (J < 0 do not exist: zero tiles), targets
+//     M = I-N+4b+9 .. I.  CTA = strip of BW target tiles (BW NB columns):
+//     Rf[I, strip] += L[I, Js] T[Js, strip].
+// Each source tile is one K-chunk of NB; chunks stream through STAGES shared
+// buffers by cp.async while the previous one is multiplied.
+template <typename C, bool ROW>
+struct FarShape {
+  static constexpr int BM = ROW ? NB : BW * NB;   // target rows per CTA
+  static constexpr int BN = ROW ? BW * NB : NB;   // target cols per CTA
+  static constexpr int AP = NB + (sizeof(C) == 8 ? 2 : 1);  // A pitch: conflict-free column reads
+  static constexpr int A_ELEMS = BM * AP;
+  static constexpr int B_ELEMS = NB * BN;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+};
+
+template <typename C, bool ROW, int STAGES>
+__global__ void __launch_bounds__(FT) far_kernel(FarArgs p, const C* __restrict__ T, const C* __restrict__ L,
+                                                 C* __restrict__ Rf) {
+  using S = FarShape<C, ROW>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* smem = reinterpret_cast<C*>(smem_raw);
+  const int N = p.N, n = p.n, beta = p.beta;
+  const long long ld = p.ld;
+  const int line = p.first + blockIdx.y;  // M (COL) or I (ROW)
+  const int t0 = BW * blockIdx.x;         // first target in the strip (offset along the line)
+  // global origin of the target strip and of the first source
+  int out_r0, out_c0, src0;
+  if (!ROW) {
+    const int M = line;
+    out_r0 = (M + t0) * NB;
+    out_c0 = M * NB;
+    src0 = M + N - 4 * beta - 4;  // K of chunk 0
+  } else {
+    const int I = line;
+    out_r0 = I * NB;
+    out_c0 = (I - N + 4 * beta + 9 + t0) * NB;
+    src0 = I - N + 1 + 4 * beta;  // J of chunk 0
+  }
+  const int tid = threadIdx.x;
+  auto chunk_valid = [&](int k) {
+    const int s = src0 + k;
+    return ROW ? (s >= 0) : (s <= N - 1);
+  };
+  auto issue = [&](int k) {
+    C* sa = smem + (k % STAGES) * S::STAGE;
+    C* sb = sa + S::A_ELEMS;
+    if (chunk_valid(k)) {
+      const int s = src0 + k;
+      if (!ROW) {
+        load_block_async<C>(sa, S::AP, T, ld, out_r0, s * NB, S::BM, NB, n, tid, FT);  // T[strip, K]
+        load_block_async<C>(sb, S::BN, L, ld, s * NB, out_c0, NB, S::BN, n, tid, FT);  // L[K, M]
+      } else {
+        load_block_async<C>(sa, S::AP, L, ld, out_r0, s * NB, S::BM, NB, n, tid, FT);  // L[I, J]
+        load_block_async<C>(sb, S::BN, T, ld, s * NB, out_c0, NB, S::BN, n, tid, FT);  // T[J, strip]
+      }
+    }
+    cp_async_commit();
+  };
+  // thread -> outputs: rows ra + RS*a, cols cb + CS*q (a, q = 0..3)
+  constexpr int CS = ROW ? 32 : 8;
+  constexpr int RS = ROW ? 8 : 32;
+  const int cb = tid % CS, ra = tid / CS;
+  C acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[a][q] = czero<C>();
+#pragma unroll
+  for (int k = 0; k < STAGES - 1; ++k) issue(k);
+#pragma unroll 1
+  for (int k = 0; k < BW; ++k) {
+    if (k + STAGES - 1 < BW)
+      issue(k + STAGES - 1);
+    else
+      cp_async_commit();  // keep the group count uniform
+    cp_async_wait<STAGES - 1>();
+    __syncthreads();
+    if (chunk_valid(k)) {
+      const C* sa = smem + (k % STAGES) * S::STAGE;
+      const C* sb = sa + S::A_ELEMS;
+#pragma unroll 4
+      for (int kk = 0; kk < NB; ++kk) {
+        C av[4], bv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) av[a] = sa[(ra + RS * a) * S::AP + kk];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) bv[q] = sb[kk * S::BN + cb + CS * q];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) cfma(acc[a][q], av[a], bv[q]);
+      }
+    }
+    __syncthreads();  // the stage is refilled by the next issue()
+  }
+  // epilogue: Rf[target] -= acc (COL) / += acc (ROW), per target tile in the strip
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int r = ra + RS * a;
+    const int gi = out_r0 + r;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = cb + CS * q;
+      const int tgt = t0 + (ROW ? c / NB : r / NB);  // target index along the line
+      const int gj = out_c0 + c;
+      if (tgt < p.h && gi < n && gj < n) {
+        C v = Rf[(size_t)gi * ld + gj];
+        if (ROW) {
+          v.x += acc[a][q].x;
+          v.y += acc[a][q].y;
+        } else {
+          v.x -= acc[a][q].x;
+          v.y -= acc[a][q].y;
+        }
+        Rf[(size_t)gi * ld + gj] = v;
+      }
+    }
+  }
+}
+
+// Rn = -stril(E) (only the strictly lower part is ever read), Rf = 0, L = 0.
+template <typename C>
+__global__ void init_kernel(int n, const C* __restrict__ E, C* __restrict__ Rn, C* __restrict__ Rf,
+                            C* __restrict__ L, long long ld) {
   const long long total = (long long)n * n;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(idx / n), j = (int)(idx % n);
-    const C e = E[(size_t)i * ld + j];
-    C r;
-    r.x = (i > j) ? -e.x : 0;
-    r.y = (i > j) ? -e.y : 0;
-    R[(size_t)i * ld + j] = r;
-    L[(size_t)i * ld + j] = czero<C>();
+    const size_t o = (size_t)i * ld + j;
+    C r = czero<C>();
+    if (i > j) {
+      const C e = E[o];
+      r.x = -e.x;
+      r.y = -e.y;
+    }
+    Rn[o] = r;
+    Rf[o] = czero<C>();
+    L[o] = czero<C>();
   }
 }
 
@@ -324,14 +515,10 @@ __global__ void separation_kernel(int n, const C* __restrict__ T, long long ld, 
   if (a.x == b.x && a.y == b.y) atomicOr(flags, SR_FLAG_SEPARATION);
 }
 
-inline int count_b(int N, int lev) {
-  int c = 0;
-  for (int r = 0; r < lev; ++r) {
-    const int cnt = N - 2 * lev + r + 1;
-    if (cnt > 0) c += cnt;
-  }
-  return c;
-}
+constexpr int FAR_STAGES = 2;
+constexpr int NFAR_EV = 4;
+
+inline size_t r_bytes(int n, long long ld, size_t elt) { return ((size_t)n * ld * elt + 255) & ~(size_t)255; }
 
 template <typename C>
 int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsigned long long* d_clipped,
@@ -340,55 +527,94 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
   if (n == 0) return SR_OK;
   const int N = (n + NB - 1) / NB;
   const size_t need = sr_trisolve_workspace_bytes(n, sizeof(C) == 8 ? 1 : 0);
-  if (ws_bytes < need || !ws || (size_t)n * ld * sizeof(C) > need) return SR_EINVAL;
-  C* R = (C*)ws;
+  const size_t rb = r_bytes(n, ld, sizeof(C));
+  if (ws_bytes < need || !ws || 2 * rb > need) return SR_EINVAL;
+  C* Rn = (C*)ws;
+  C* Rf = (C*)((char*)ws + rb);
   {
     const long long total = (long long)n * n;
     const long long blocks = (total + 255) / 256;
     const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
-    init_kernel<C><<<grid, 256, 0, st>>>(n, e, R, l, ld);
+    init_kernel<C><<<grid, 256, 0, st>>>(n, e, Rn, Rf, l, ld);
     SR_LAUNCH_CHECK();
     dim3 b(32, 8), g(sr_ceil_div(n, 32), sr_ceil_div(n, 8));
     separation_kernel<C><<<g, b, 0, st>>>(n, t, ld, d_flags);
     SR_LAUNCH_CHECK();
   }
-  const size_t smem = sizeof(C) * 5 * NB * LD;
-  auto ksolve = sweep_kernel<C, true>;
-  auto kupd = sweep_kernel<C, false>;
-  // Two internal streams (created once): the critical-path tile solves and the
-  // bulk right-hand-side updates of each level run concurrently; events order
-  // level lev+1 after both launches of level lev.
+  const size_t smem_solve = sizeof(C) * (9 * NB * LD + NB * NB);
+  const size_t smem_near = sizeof(C) * 5 * NB * LD;
+  const size_t smem_far_col = sizeof(C) * FAR_STAGES * FarShape<C, false>::STAGE;
+  const size_t smem_far_row = sizeof(C) * FAR_STAGES * FarShape<C, true>::STAGE;
+  auto ksolve = solve_kernel<C>;
+  auto knear = near_kernel<C>;
+  auto kfc = far_kernel<C, false, FAR_STAGES>;
+  auto kfr = far_kernel<C, true, FAR_STAGES>;
+  // Three internal streams (created once): critical-path tile solves, the
+  // near-band updates and the far batches; events order them (see the header).
   static bool configured = false;
-  static cudaStream_t s_solve, s_upd;
-  static cudaEvent_t ev_in, ev_s, ev_u;
+  static cudaStream_t s_solve, s_near, s_far;
+  static cudaEvent_t ev_in, ev_s, ev_u, ev_f[NFAR_EV];
   if (!configured) {
-    SR_CUDA_CHECK(cudaFuncSetAttribute(ksolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SR_CUDA_CHECK(cudaFuncSetAttribute(kupd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     SR_CUDA_CHECK(cudaStreamCreateWithFlags(&s_solve, cudaStreamNonBlocking));
-    SR_CUDA_CHECK(cudaStreamCreateWithFlags(&s_upd, cudaStreamNonBlocking));
+    SR_CUDA_CHECK(cudaStreamCreateWithFlags(&s_near, cudaStreamNonBlocking));
+    SR_CUDA_CHECK(cudaStreamCreateWithFlags(&s_far, cudaStreamNonBlocking));
     SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
     SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_s, cudaEventDisableTiming));
     SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_u, cudaEventDisableTiming));
+    for (int i = 0; i < NFAR_EV; ++i) SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_f[i], cudaEventDisableTiming));
     configured = true;
+  }
+  static bool attr_set = false;  // per template instance
+  if (!attr_set) {
+    SR_CUDA_CHECK(cudaFuncSetAttribute(ksolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_solve));
+    SR_CUDA_CHECK(cudaFuncSetAttribute(knear, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_near));
+    SR_CUDA_CHECK(cudaFuncSetAttribute(kfc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_far_col));
+    SR_CUDA_CHECK(cudaFuncSetAttribute(kfr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_far_row));
+    attr_set = true;
   }
   SR_CUDA_CHECK(cudaEventRecord(ev_in, st));
   SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, ev_in, 0));
-  SR_CUDA_CHECK(cudaStreamWaitEvent(s_upd, ev_in, 0));
+  SR_CUDA_CHECK(cudaStreamWaitEvent(s_near, ev_in, 0));
+  SR_CUDA_CHECK(cudaStreamWaitEvent(s_far, ev_in, 0));
   const typename Real<C>::T cl = (typename Real<C>::T)clip;
   for (int lev = 0; lev < N; ++lev) {
-    const int countA = lev * (N - lev);
-    SweepArgs a{n, N, lev, countA, ld};
-    ksolve<<<lev + 1, NT, smem, s_solve>>>(a, t, R, l, cl, d_clipped);
+    // SOLVE(lev): after NEAR(lev-1) (stream order + ev_u) and FAR(lev/4 - 2)
+    if (lev >= 1) SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, ev_u, 0));
+    if (lev % BW == 0 && lev >= 2 * BW) SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, ev_f[(lev / BW - 2) % NFAR_EV], 0));
+    SweepArgs a{n, N, lev, 0, ld};
+    ksolve<<<lev + 1, NT, smem_solve, s_solve>>>(a, t, Rn, Rf, l, cl, d_clipped);
     SR_LAUNCH_CHECK();
-    const int grid = lev == 0 ? 0 : countA + count_b(N, lev);
-    if (grid > 0) {
-      kupd<<<grid, NT, smem, s_upd>>>(a, t, R, l, cl, d_clipped);
-      SR_LAUNCH_CHECK();
+    // NEAR(lev): sources of level lev-1 into levels lev+1 .. 4b+7, b = (lev-1)/4
+    if (lev >= 1) {
+      SR_CUDA_CHECK(cudaStreamWaitEvent(s_near, ev_s, 0));  // SOLVE(lev-1)
+      const int b = (lev - 1) / BW;
+      const int lmax = min(N - 1, BW * b + 2 * BW - 1);
+      if (lmax >= lev + 1) {
+        a.lmax = lmax;
+        dim3 grid(lmax + 1, lmax - lev);
+        knear<<<grid, NT, smem_near, s_near>>>(a, t, Rn, l);
+        SR_LAUNCH_CHECK();
+      }
     }
     SR_CUDA_CHECK(cudaEventRecord(ev_s, s_solve));
-    SR_CUDA_CHECK(cudaEventRecord(ev_u, s_upd));
-    SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, ev_u, 0));
-    SR_CUDA_CHECK(cudaStreamWaitEvent(s_upd, ev_s, 0));
+    SR_CUDA_CHECK(cudaEventRecord(ev_u, s_near));
+    // FAR(b) once the last level of batch b is solved, if any tile sits on level >= 4b+8
+    if (lev % BW == BW - 1) {
+      const int b = lev / BW;
+      const int h = N - BW * b - 2 * BW;
+      if (h >= 1) {
+        SR_CUDA_CHECK(cudaStreamWaitEvent(s_far, ev_s, 0));
+        FarArgs fa{n, N, b, h, 0, ld};
+        const int strips = (h + BW - 1) / BW;
+        fa.first = 0;
+        kfc<<<dim3(strips, min(BW * b + BW, N)), FT, smem_far_col, s_far>>>(fa, t, l, Rf);
+        SR_LAUNCH_CHECK();
+        fa.first = N - BW - BW * b;
+        kfr<<<dim3(strips, N - fa.first), FT, smem_far_row, s_far>>>(fa, t, l, Rf);
+        SR_LAUNCH_CHECK();
+        SR_CUDA_CHECK(cudaEventRecord(ev_f[b % NFAR_EV], s_far));
+      }
+    }
   }
   SR_CUDA_CHECK(cudaEventRecord(ev_s, s_solve));
   SR_CUDA_CHECK(cudaStreamWaitEvent(st, ev_s, 0));
@@ -399,7 +625,8 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
 
 extern "C" size_t sr_trisolve_workspace_bytes(int n, int lp_is_c64) {
   const size_t elt = lp_is_c64 ? 8 : 16;
-  return (size_t)n * (size_t)(n + (n & 1)) * elt + 256;  // the running right-hand side R
+  // two running right-hand sides: Rn (near band) and Rf (far batches)
+  return 2 * r_bytes(n, n + (n & 1), elt) + 256;
 }
 
 extern "C" int sr_trisolve_c64(int n, const void* t, const void* e, long long ld, void* l, float clip,

@@ -74,7 +74,7 @@ def test_trisolve_matches_reference_golden(golden):
             assert err <= 2e-5, (c, err)
 
 
-@pytest.mark.parametrize("n", [33, 100, 257, 700])
+@pytest.mark.parametrize("n", [33, 100, 257, 700, 1157])
 def test_trisolve_c64_matches_oracle(n):
     rng = np.random.default_rng(n)
     t = np.triu(rnd(rng, n, n))
@@ -90,6 +90,33 @@ def test_trisolve_c64_matches_oracle(n):
     # residual of the equation itself
     res = np.linalg.norm(np.tril(t @ l - l @ t, -1) + e) / np.linalg.norm(e)
     assert res <= 1e-4, res
+
+
+@pytest.mark.parametrize("n", [291, 610])
+def test_trisolve_c128_far_batches_match_oracle(n):
+    """Sizes with several far batches (N >= 9 tiles): complex128 solve vs the
+    C oracle to 1e-11, and the clip decisions (threshold between the bulk of
+    |L| and a few planted large entries) identical."""
+    rng = np.random.default_rng(n + 1)
+    t = np.triu(rnd(rng, n, n))
+    t[np.diag_indices(n)] = np.arange(n) * 1.1 + 1j * rng.standard_normal(n)
+    e = np.tril(rnd(rng, n, n), -1) * 1e-3
+    l_or, _ = clib.solve_block(t, e, dtype=np.complex128)
+    sol = solve_block(TriEqProblem(t=t, e=e), lp_dtype=torch.complex128)
+    l = sol.l.cpu().numpy()
+    err = np.linalg.norm(l - l_or) / np.linalg.norm(l_or)
+    assert err <= 1e-11, err
+    # clipping: plant a few large right-hand sides so their entries exceed the threshold
+    e2 = e.copy()
+    idx = [(n - 1, 0), (n // 2, n // 3), (n - 40, n - 90)]
+    for (i, j) in idx:
+        e2[i, j] = 1e3
+    thr = 0.5
+    l_or2, clipped_or = clib.solve_block(t, e2, clip_threshold=thr, dtype=np.complex128)
+    sol2 = solve_block(TriEqProblem(t=t, e=e2, clip_threshold=thr), lp_dtype=torch.complex128)
+    assert sol2.clipped_count == clipped_or and clipped_or >= 1
+    l2 = sol2.l.cpu().numpy()
+    assert np.linalg.norm(l2 - l_or2) <= 1e-11 * np.linalg.norm(l_or2)
 
 
 def test_trisolve_errors():

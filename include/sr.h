@@ -184,9 +184,10 @@ int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, const void* 
    add_kind < 0 for none), with rho_i = beta_a - exps_a[i], sigma_j =
    beta_b - exps_b[j], rounded once into out_kind (any SR_MAT_*).  table
    (host): [nmod][6] CRT weights, [6] modulus-product chunks, [6] chunk
-   offsets, 1/P.  hermitian: the residues hold only the lower 128-tiles
-   (sr_oz_gemm_i8 with lower_only); the strictly upper tiles are written as
-   the conjugate transpose (out_kind SR_MAT_F64 or SR_MAT_DD, no add).
+   offsets, 1/P.  hermitian = 1 / -1: the residues hold only the lower
+   128-tiles (sr_oz_gemm_i8 with lower_only); the strictly upper tiles are
+   written as the conjugate transpose (Hermitian C, 1) or its negative
+   (skew-Hermitian C, -1); M == N, no add, any out_kind.
    diag_col0: the shift lands on entries (i, j) with i == j + diag_col0
    (column blocks of a sharded product). */
 int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* table, const void* res, long long res_pitch,

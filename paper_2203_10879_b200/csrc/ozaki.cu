@@ -398,15 +398,16 @@ __global__ void __launch_bounds__(256) decode_kernel(const __grid_constant__ Dec
 
 // Hermitian products are computed on the lower 128 x 128 tiles only; fill the
 // strictly-upper tiles with the conjugate transpose (smem-tiled, coalesced).
-// planes: (re, im) or dd (re, im, re_lo, im_lo); imaginary planes are negated.
-__global__ void __launch_bounds__(256) mirror_kernel(int n, Dst d, int nplanes, long long ld) {
+// planes: (re, im) or dd (re, im, re_lo, im_lo); imaginary planes are negated
+// (Hermitian, sign = 1) or the real planes are (skew-Hermitian, sign = -1).
+__global__ void __launch_bounds__(256) mirror_kernel(int n, Dst d, int nplanes, long long ld, double sign) {
   __shared__ double t[32][33];
   const int bi = blockIdx.y, bj = blockIdx.x;  // destination 32-tile (bi, bj), bj > bi
   if ((bj >> 2) <= (bi >> 2)) return;           // only strictly-upper 128-tiles
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   for (int q = 0; q < nplanes; ++q) {
     double* pl = q == 0 ? d.re : (q == 1 ? d.im : (q == 2 ? d.re_lo : d.im_lo));
-    const double sgn = (q & 1) ? -1.0 : 1.0;
+    const double s2 = (q & 1) ? -sign : sign;  // sign * conj: re -> sign*re, im -> -sign*im
     __syncthreads();
     for (int r = ty; r < 32; r += 8) {  // read source tile (bj, bi), coalesced
       const int si = bj * 32 + r, sj = bi * 32 + tx;
@@ -415,7 +416,30 @@ __global__ void __launch_bounds__(256) mirror_kernel(int n, Dst d, int nplanes, 
     __syncthreads();
     for (int r = ty; r < 32; r += 8) {
       const int di = bi * 32 + r, dj = bj * 32 + tx;
-      if (di < n && dj < n) pl[(size_t)di * ld + dj] = sgn * t[tx][r];
+      if (di < n && dj < n) pl[(size_t)di * ld + dj] = s2 * t[tx][r];
+    }
+  }
+}
+
+// Same for an interleaved lp output (complex64 / complex128).
+template <typename CT>
+__global__ void __launch_bounds__(256) mirror_lp_kernel(int n, CT* d, long long ld, float sign) {
+  __shared__ CT t[32][33];
+  const int bi = blockIdx.y, bj = blockIdx.x;
+  if ((bj >> 2) <= (bi >> 2)) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) {
+    const int si = bj * 32 + r, sj = bi * 32 + tx;
+    if (si < n && sj < n) t[r][tx] = d[(size_t)si * ld + sj];
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int di = bi * 32 + r, dj = bj * 32 + tx;
+    if (di < n && dj < n) {
+      CT v = t[tx][r];
+      v.x = sign * v.x;
+      v.y = -sign * v.y;
+      d[(size_t)di * ld + dj] = v;
     }
   }
 }
@@ -559,8 +583,7 @@ extern "C" int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* ta
   if ((out_kind == SR_MAT_F64 || out_kind == SR_MAT_DD) && !out_im) return SR_EINVAL;
   if (out_kind == SR_MAT_DD && (!out_re_lo || !out_im_lo)) return SR_EINVAL;
   if (add_kind >= 0 && !add_re) return SR_EINVAL;
-  if (hermitian && (M != N || (out_kind != SR_MAT_F64 && out_kind != SR_MAT_DD) || add_kind >= 0))
-    return SR_EINVAL;
+  if (hermitian != 0 && (M != N || add_kind >= 0 || (hermitian != 1 && hermitian != -1))) return SR_EINVAL;
   DecodeParams p;
   memset(&p, 0, sizeof(p));
   p.M = M;
@@ -613,7 +636,12 @@ extern "C" int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* ta
   SR_LAUNCH_CHECK();
   if (hermitian) {
     dim3 g(sr_ceil_div(N, 32), sr_ceil_div(M, 32));
-    mirror_kernel<<<g, 256, 0, st>>>(M, out, out_kind == SR_MAT_DD ? 4 : 2, ld_out);
+    if (out_kind == SR_MAT_C64)
+      mirror_lp_kernel<float2><<<g, 256, 0, st>>>(M, (float2*)out_re, ld_out, (float)hermitian);
+    else if (out_kind == SR_MAT_C128)
+      mirror_lp_kernel<double2><<<g, 256, 0, st>>>(M, (double2*)out_re, ld_out, (float)hermitian);
+    else
+      mirror_kernel<<<g, 256, 0, st>>>(M, out, out_kind == SR_MAT_DD ? 4 : 2, ld_out, (double)hermitian);
     SR_LAUNCH_CHECK();
   }
   return SR_OK;

@@ -187,16 +187,18 @@ __device__ __forceinline__ unsigned tile_solve_warp(const C* sT2, const C* sD, c
       sX[i * LD + j] = x;
     }
     // column terms: lane i+d finalised (i+d, j+d); it feeds this lane's (i, j+d)
+    // (tr[d] = 0 past the tile edge, so no predicate is needed)
 #pragma unroll
     for (int d = 1; d < NB; ++d) {
       const C xv = shfl_down(x, d);
-      if (i + d < NB) cfms(pend[d], tr[d], xv);
+      cfms(pend[d], tr[d], xv);
     }
     // row terms: (i, j) feeds this lane's (i, j+d) through T1[j][j+d]
-    if (valid) {
+    // (x = 0 on invalid steps, sD[d][j] = 0 for j + d >= NB)
+    {
+      const int jc = min(max(j, 0), NB - 1);
 #pragma unroll
-      for (int d = 1; d < NB; ++d)
-        if (j + d < NB) cfma(pend[d], x, sD[d * NB + j]);
+      for (int d = 1; d < NB; ++d) cfma(pend[d], x, sD[d * NB + jc]);
     }
     // slide the window one column to the right
 #pragma unroll

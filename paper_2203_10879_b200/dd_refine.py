@@ -79,9 +79,9 @@ class DDProducts:
         ozaki.decode(self.res, ea, eb, self.hp, out, hermitian=hermitian, **kw)
         _counters["hp_calls"] += 1
 
-    def _lp(self, ea, eb, out):
-        ozaki.gemm_residues(ea, eb, self.lp, self.lres)
-        ozaki.decode(self.lres, ea, eb, self.lp, out)
+    def _lp(self, ea, eb, out, hermitian=False):
+        ozaki.gemm_residues(ea, eb, self.lp, self.lres, lower_only=bool(hermitian))
+        ozaki.decode(self.lres, ea, eb, self.lp, out, hermitian=hermitian)
         _counters["lp_calls"] += 1
 
     def entry(self, qhat):
@@ -135,9 +135,9 @@ class DDProducts:
         ozaki.encode(ws.y_lp, n, n, "a", lp, out=self.la)
         self._lp(self.la, self.lb, ws.yw)
         ozaki.encode(ws.w_lp, n, n, "a", lp, out=self.la)
-        self._lp(self.la, self.lb, ws.w2)
+        self._lp(self.la, self.lb, ws.w2, hermitian=True)      # W skew-Hermitian: W^2 Hermitian
         ozaki.encode(ws.w2, n, n, "a", lp, out=self.la)
-        self._lp(self.la, self.lb, ws.w3)
+        self._lp(self.la, self.lb, ws.w3, hermitian="skew")    # W^3 skew-Hermitian
         w2y = w2yw = None
         if restore_full_sigma:
             if ws.w2y is None:

@@ -194,7 +194,12 @@ def gemm_residues(ea, eb, pl, res, lower_only=False):
 
 
 def decode(res, ea, eb, pl, out, alpha=1.0, shift=0.0, add=None, add_scale=1.0, hermitian=False, diag_col0=0):
-    """out / add: ZPlanar, DDPlanar, or complex64 / complex128 (M, ld) tensors."""
+    """out / add: ZPlanar, DDPlanar, or complex64 / complex128 (M, ld) tensors.
+
+    hermitian: False, True (C Hermitian) or "skew" (C skew-Hermitian); with
+    True / "skew" the residues hold the lower 128-tiles only
+    (gemm_residues(lower_only=True)) and the upper ones are mirrored."""
+    herm = -1 if hermitian == "skew" else (1 if hermitian else 0)
     o_kind, o_re, o_im, o_rl, o_il, ld_out, _ = mat_args(out)
     if add is None:
         a_kind, a_re, a_im, a_rl, a_il, ld_add = -1, None, None, None, None, 0
@@ -203,5 +208,5 @@ def decode(res, ea, eb, pl, out, alpha=1.0, shift=0.0, add=None, add_scale=1.0, 
     _lib.call("sr_oz_decode", res.M, res.N, pl.nmod, pl.nchunk, pl.table_ptr(), res.buf.data_ptr(), res.pitch,
               ea.exps.data_ptr(), ea.beta, eb.exps.data_ptr(), eb.beta, float(alpha), float(shift), a_kind, a_re,
               a_im, a_rl, a_il, ld_add, float(add_scale), o_kind, o_re, o_im, o_rl, o_il, ld_out,
-              1 if hermitian else 0, int(diag_col0), _stream())
+              herm, int(diag_col0), _stream())
     return out

@@ -105,9 +105,9 @@ class OzakiProducts:
         ozaki.decode(self.res, ea, eb, self.hp, out, hermitian=hermitian, **kw)
         _counters["hp_calls"] += 1
 
-    def _lp(self, ea, eb, out):
-        ozaki.gemm_residues(ea, eb, self.lp, self.lres)
-        ozaki.decode(self.lres, ea, eb, self.lp, out)
+    def _lp(self, ea, eb, out, hermitian=False):
+        ozaki.gemm_residues(ea, eb, self.lp, self.lres, lower_only=bool(hermitian))
+        ozaki.decode(self.lres, ea, eb, self.lp, out, hermitian=hermitian)
         _counters["lp_calls"] += 1
 
     def entry(self, qhat):
@@ -136,9 +136,9 @@ class OzakiProducts:
         ozaki.encode(ws.y_lp, n, n, "a", lp, out=self.la)
         self._lp(self.la, self.lb, ws.yw)                                # Y W
         ozaki.encode(ws.w_lp, n, n, "a", lp, out=self.la)
-        self._lp(self.la, self.lb, ws.w2)                                # W^2
+        self._lp(self.la, self.lb, ws.w2, hermitian=True)                # W^2 (W skew-Hermitian)
         ozaki.encode(ws.w2, n, n, "a", lp, out=self.la)
-        self._lp(self.la, self.lb, ws.w3)                                # W^3
+        self._lp(self.la, self.lb, ws.w3, hermitian="skew")              # W^3
         if restore_full_sigma:
             ozaki.encode(ws.y_lp, n, n, "b", lp, out=self.lb)
             ozaki.encode(ws.w2, n, n, "a", lp, out=self.la)

@@ -141,3 +141,38 @@ def test_oz_lp_product_complex64():
     err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     f32 = np.linalg.norm((w @ w) - ref) / np.linalg.norm(ref)
     assert err <= max(2 * f32, 1e-7), (err, f32)
+
+
+@pytest.mark.parametrize("dtype,beta", [(torch.complex64, ozaki.LP_BETA), (torch.complex128, ozaki.DD_LP_BETA)])
+@pytest.mark.parametrize("n", [300, 515])
+def test_oz_lp_structured_products(dtype, beta, n):
+    """W = L - L^H skew-Hermitian: W^2 (Hermitian) and W^3 = W^2 W (skew) from
+    the lower 128-tiles plus the mirror; upper tiles exactly (-)conj of the
+    lower ones, accuracy as the full product."""
+    rng = np.random.default_rng(n)
+    npdt = np.complex64 if dtype == torch.complex64 else np.complex128
+    l = np.tril(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)), -1) * 1e-3
+    w = (l - l.conj().T).astype(npdt)
+    wd = lp_empty(n, dtype=dtype)
+    wd[:, :n] = torch.from_numpy(w)
+    pl = ozaki.plan(n, beta, beta)
+    eb = ozaki.encode(wd, n, n, "b", pl)
+    ea = ozaki.encode(wd, n, n, "a", pl)
+    res = ozaki.ResidueBuffer(n, n, pl.nmod, "cuda")
+    w2 = lp_empty(n, dtype=dtype)
+    ozaki.gemm_residues(ea, eb, pl, res, lower_only=True)
+    ozaki.decode(res, ea, eb, pl, w2, hermitian=True)
+    ea2 = ozaki.encode(w2, n, n, "a", pl)
+    w3 = lp_empty(n, dtype=dtype)
+    ozaki.gemm_residues(ea2, eb, pl, res, lower_only=True)
+    ozaki.decode(res, ea2, eb, pl, w3, hermitian="skew")
+    wc = w.astype(np.complex128)
+    g2, g3 = w2[:, :n].cpu().numpy(), w3[:, :n].cpu().numpy()
+    tol = 1e-6 if dtype == torch.complex64 else 1e-14
+    assert np.linalg.norm(g2 - wc @ wc) <= tol * np.linalg.norm(wc @ wc)
+    assert np.linalg.norm(g3 - g2.astype(np.complex128) @ wc) <= tol * np.linalg.norm(wc @ wc @ wc)
+    up = np.zeros((n, n), bool)  # strictly-upper 128-tiles: mirrored
+    for i in range(n):
+        up[i, (i // 128 + 1) * 128:] = True
+    assert np.array_equal(g2[up], g2.conj().T[up])
+    assert np.array_equal(g3[up], -g3.conj().T[up])

@@ -45,7 +45,12 @@
 //
 // Templated on the lp type: float2 (FP64 mode, lp = complex64) and double2
 // (dd mode, lp = binary64 complex).
+#include <stdlib.h>
+
+#include <type_traits>
+
 #include "sr_common.cuh"
+#include "trisolve_tc.cuh"
 
 namespace {
 
@@ -530,9 +535,19 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
   const int N = (n + NB - 1) / NB;
   const size_t need = sr_trisolve_workspace_bytes(n, sizeof(C) == 8 ? 1 : 0);
   const size_t rb = r_bytes(n, ld, sizeof(C));
-  if (ws_bytes < need || !ws || 2 * rb > need) return SR_EINVAL;
+  if (ws_bytes < need || !ws || 2 * rb + (sizeof(C) == 8 ? far_tc_forms_bytes(n) : 0) > need) return SR_EINVAL;
   C* Rn = (C*)ws;
   C* Rf = (C*)((char*)ws + rb);
+  // complex64 with 16-byte aligned rows: far updates on the tensor cores (trisolve_tc.cu)
+  constexpr bool kC64 = std::is_same<C, float2>::value;
+  const bool use_tc = kC64 && (ld % 2) == 0 && !getenv("SR_SOLVE_SIMT_FAR");
+  FarTcPlan plan;
+  if constexpr (kC64) {
+    if (use_tc) {
+      const int rc = far_tc_prepare(&plan, n, t, ld, (char*)ws + 2 * rb, st);
+      if (rc != SR_OK) return rc;
+    }
+  }
   {
     const long long total = (long long)n * n;
     const long long blocks = (total + 255) / 256;
@@ -606,14 +621,24 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
       const int h = N - BW * b - 2 * BW;
       if (h >= 1) {
         SR_CUDA_CHECK(cudaStreamWaitEvent(s_far, ev_s, 0));
-        FarArgs fa{n, N, b, h, 0, ld};
-        const int strips = (h + BW - 1) / BW;
-        fa.first = 0;
-        kfc<<<dim3(strips, min(BW * b + BW, N)), FT, smem_far_col, s_far>>>(fa, t, l, Rf);
-        SR_LAUNCH_CHECK();
-        fa.first = N - BW - BW * b;
-        kfr<<<dim3(strips, N - fa.first), FT, smem_far_row, s_far>>>(fa, t, l, Rf);
-        SR_LAUNCH_CHECK();
+        bool done = false;
+        if constexpr (kC64) {
+          if (use_tc) {
+            const int rc = far_tc_batch(plan, N, b, h, l, ld, Rf, s_far);
+            if (rc != SR_OK) return rc;
+            done = true;
+          }
+        }
+        if (!done) {
+          FarArgs fa{n, N, b, h, 0, ld};
+          const int strips = (h + BW - 1) / BW;
+          fa.first = 0;
+          kfc<<<dim3(strips, min(BW * b + BW, N)), FT, smem_far_col, s_far>>>(fa, t, l, Rf);
+          SR_LAUNCH_CHECK();
+          fa.first = N - BW - BW * b;
+          kfr<<<dim3(strips, N - fa.first), FT, smem_far_row, s_far>>>(fa, t, l, Rf);
+          SR_LAUNCH_CHECK();
+        }
         SR_CUDA_CHECK(cudaEventRecord(ev_f[b % NFAR_EV], s_far));
       }
     }
@@ -627,8 +652,9 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
 
 extern "C" size_t sr_trisolve_workspace_bytes(int n, int lp_is_c64) {
   const size_t elt = lp_is_c64 ? 8 : 16;
-  // two running right-hand sides: Rn (near band) and Rf (far batches)
-  return 2 * r_bytes(n, n + (n & 1), elt) + 256;
+  // two running right-hand sides: Rn (near band) and Rf (far batches); for
+  // complex64 also the split operand forms of the tensor-core far updates
+  return 2 * r_bytes(n, n + (n & 1), elt) + (lp_is_c64 ? far_tc_forms_bytes(n) : 0) + 256;
 }
 
 extern "C" int sr_trisolve_c64(int n, const void* t, const void* e, long long ld, void* l, float clip,

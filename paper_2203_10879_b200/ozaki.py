@@ -5,8 +5,9 @@ integers: op(A) and B are scaled per row / column to integers below 2^beta,
 reduced modulo r pairwise-coprime moduli p_l <= 256 (int8 residues), the r
 residue products run on tcgen05 (csrc/oz_gemm.cu), and the Chinese remainder
 theorem recovers C' before one final rounding (csrc/ozaki.cu).  The plan
-picks the smallest r with  prod(p_l) > 4 * 2K * 2^(beta_a + beta_b), so the
-CRT representative is unique with a 2-bit margin.
+picks the smallest r with  prod(p_l) >= 2 * 2K * 2^(beta_a + beta_b): the
+complex entries of C' are sums of 2K products below 2^(beta_a + beta_b), so
+|C'| < prod / 2 and the symmetric CRT representative is C' itself.
 
 Where it sits in the reference: it replaces matmul_hp / matmul_lp
 (/root/reference/pkg/src/ddschur/matmul.py:52-110) — in FP64 mode (hp = FP64,
@@ -29,8 +30,8 @@ MODULI = [256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 
 CHUNK_BITS = 40
 MAXCHUNK = 6
 
-HP_BETA = 60     # FP64-mode hp operands: every entry within 2^-7 of its row max is exact
-LP_BETA = 26     # FP64-mode lp (complex64) operands: significand + 2 guard bits
+HP_BETA = 58     # FP64-mode hp operands: every entry within 2^-5 of its row max is exact (17 moduli at K=8192)
+LP_BETA = 24     # FP64-mode lp (complex64) operands: the row maximum's full significand (8 moduli at K=8192)
 DD_BETA = 102    # dd-mode hp operands (double-double; the stop rule is 10 n 2^-106 ||A||)
 DD_LP_BETA = 55  # dd-mode lp (binary64) operands
 
@@ -42,7 +43,7 @@ class OzPlan:
         self.K = K
         self.beta_a = beta_a
         self.beta_b = beta_b
-        need = beta_a + beta_b + math.ceil(math.log2(max(K, 2))) + 1 + 2
+        need = beta_a + beta_b + math.ceil(math.log2(max(K, 2))) + 2
         P = 1
         r = 0
         while P.bit_length() - 1 < need:

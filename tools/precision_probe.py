@@ -11,8 +11,13 @@ from oracle import clib  # noqa: E402
 from paper_2203_10879_b200 import ZPlanar, matmul_hp, ozaki  # noqa: E402
 
 
-def oz(x, y, trans=False, shift=0.0):
-    pl = ozaki.plan(x.rows, ozaki.HP_BETA, ozaki.HP_BETA)
+import os  # noqa: E402
+BETAS = [int(b) for b in os.environ.get("OZ_BETAS", str(ozaki.HP_BETA)).split(",")]
+
+
+def oz(x, y, trans=False, shift=0.0, beta=None):
+    beta = ozaki.HP_BETA if beta is None else beta
+    pl = ozaki.plan(x.rows, beta, beta)
     ea = ozaki.encode(x, x.rows, x.cols, "a", pl, conj_t=trans)
     eb = ozaki.encode(y, y.rows, y.cols, "b", pl)
     res = ozaki.ResidueBuffer(x.cols if trans else x.rows, y.cols, pl.nmod, "cuda")
@@ -54,10 +59,13 @@ for n in [int(x) for x in sys.argv[1:]] or [256, 512]:
     qd, ad = ZPlanar.from_any(q), ZPlanar.from_any(a)
     t_gpu = matmul_hp(matmul_hp(qd, ad, trans_a=True), qd).to_numpy()
     g_gpu = matmul_hp(qd, qd, trans_a=True, diag_shift=-1.0).to_numpy()
-    t_oz = oz(oz(qd, ad, trans=True), qd).to_numpy()
-    g_oz = oz(qd, qd, trans=True, shift=-1.0).to_numpy()
-    for name, t, g in (("numpy", t_np, g_np), ("dmma", t_gpu, g_gpu), ("ozaki", t_oz, g_oz)):
+    rows = [("numpy", t_np, g_np), ("dmma", t_gpu, g_gpu)]
+    for beta in BETAS:
+        t_oz = oz(oz(qd, ad, trans=True, beta=beta), qd, beta=beta).to_numpy()
+        g_oz = oz(qd, qd, trans=True, shift=-1.0, beta=beta).to_numpy()
+        rows.append(("oz%d/%d" % (beta, ozaki.plan(n, beta, beta).nmod), t_oz, g_oz))
+    for name, t, g in rows:
         et = np.linalg.norm(np.tril(t - t_hi, -1)) / na / U
         eg = np.linalg.norm(g - g_lo) / U
-        print("n=%d %-6s stril(T) noise %.2f u*||A||   Y noise %.2f u  (true ||Y|| %.2f u)" % (
+        print("n=%d %-9s stril(T) noise %.2f u*||A||   Y noise %.2f u  (true ||Y|| %.2f u)" % (
             n, name, et, eg, np.linalg.norm(g_lo) / U), flush=True)

@@ -102,10 +102,11 @@ def kpitch(K):
 class Encoded:
     """Residue planes of one operand (A role: op(X) rows; B role: columns)."""
 
-    __slots__ = ("buf", "exps", "rows", "K", "planes", "beta", "nmod", "kp")
+    __slots__ = ("buf", "exps", "rows", "K", "planes", "beta", "nmod", "kp", "cap")
 
     def __init__(self, rows, K, planes, beta, nmod, device):
         self.rows, self.K, self.planes, self.beta, self.nmod = rows, K, planes, beta, nmod
+        self.cap = nmod  # residue planes allocated; re-encodes may use fewer moduli
         self.kp = kpitch(K)
         self.buf = torch.empty(nmod * planes * rows * self.kp, dtype=torch.int8, device=device)
         self.exps = torch.empty(rows, dtype=torch.int32, device=device)
@@ -142,11 +143,27 @@ def encode(x, rows, cols, role, pl, conj_t=False, out=None):
         layout, planes = (2, 1) if real else (1, 3)
         conj = 0
     enc = out if out is not None else Encoded(out_rows, K, planes, beta, pl.nmod, dev)
+    if enc.cap < pl.nmod or enc.rows != out_rows or enc.K != K or enc.planes != planes:
+        raise ValueError("encoding buffer does not fit this operand / plan")
+    enc.beta, enc.nmod = beta, pl.nmod
     st = _stream()
     _lib.call("sr_oz_exponents", rows, cols, kind, re, im, ld, transposed, enc.exps.data_ptr(), st)
     _lib.call("sr_oz_encode", out_rows, K, kind, re, im, re_lo, im_lo, ld, transposed, conj, layout,
               enc.exps.data_ptr(), beta, pl.nmod, pl.moduli_ptr(), enc.buf.data_ptr(), enc.kp, st)
     return enc
+
+
+def correction_beta(bound, n, hi=HP_BETA, lo=LP_BETA, unit_bits=53):
+    """Operand precision for a correction product X S whose result is added to
+    an O(1) matrix before one rounding (Q + Q S'/2, Q^ - Q^ (G - I)/2):
+    truncating S (||S||_F <= bound) to beta bits per column changes the sum by
+    <= sqrt(n) 2^-beta bound per column, truncating X by <= n 2^-beta bound in
+    norm, so beta = unit_bits + 3 + log2(bound) + log2(n)/2 keeps both below a
+    quarter of the final rounding (u sqrt(n)).  Clamped to [lo, hi]."""
+    if not (bound > 0.0) or not math.isfinite(bound):
+        return hi if not (bound == 0.0) else lo
+    b = unit_bits + 3 + math.ceil(math.log2(bound)) + math.ceil(0.5 * math.log2(max(n, 2)))
+    return max(lo, min(hi, b))
 
 
 class ResidueBuffer:

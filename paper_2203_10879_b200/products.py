@@ -60,7 +60,7 @@ class DmmaProducts:
         matmul_hp(ws.p, ws.q, out=ws.that)
         matmul_hp(ws.q, ws.q, trans_a=True, diag_shift=-1.0, out=ws.y)
 
-    def update(self, restore_full_sigma):
+    def update(self, restore_full_sigma, sigma_bound=None):
         ws = self.ws
         n = ws.n
         _downcast_y(ws)
@@ -110,15 +110,27 @@ class OzakiProducts:
         ozaki.decode(self.lres, ea, eb, self.lp, out, hermitian=hermitian)
         _counters["lp_calls"] += 1
 
+    def _correction_plan(self, bound):
+        """Plan for X S with a small S (||S||_F <= bound) added to an O(1) X:
+        fewer moduli as the correction shrinks (ozaki.correction_beta)."""
+        beta = ozaki.correction_beta(bound, self.ws.n)
+        return ozaki.plan(self.ws.n, beta, beta)
+
+    def _hp_with(self, pl, ea, eb, out, **kw):
+        ozaki.gemm_residues(ea, eb, pl, self.res)
+        ozaki.decode(self.res, ea, eb, pl, out, **kw)
+        _counters["hp_calls"] += 1
+
     def entry(self, qhat):
         """Q = Q^ (3I - G) / 2 = Q^ - Q^ (G - I) / 2 (orthogonal.py:167-169)."""
         ws, hp, n = self.ws, self.hp, self.ws.n
         ozaki.encode(qhat, n, n, "a", hp, conj_t=True, out=self.ea_qh)
         ozaki.encode(qhat, n, n, "b", hp, out=self.eb_q)
         self._hp(self.ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True)  # G - I
-        ozaki.encode(qhat, n, n, "a", hp, out=self.ea_x)
-        ozaki.encode(ws.y, n, n, "b", hp, out=self.eb_s)
-        self._hp(self.ea_x, self.eb_s, ws.q, alpha=-0.5, add=qhat)       # Q^ - Q^ (G - I) / 2
+        pc = self._correction_plan(ws.fro_norm(ws.y))
+        ozaki.encode(qhat, n, n, "a", pc, out=self.ea_x)
+        ozaki.encode(ws.y, n, n, "b", pc, out=self.eb_s)
+        self._hp_with(pc, self.ea_x, self.eb_s, ws.q, alpha=-0.5, add=qhat)  # Q^ - Q^ (G - I) / 2
 
     def measure(self, a):
         ws, hp, n = self.ws, self.hp, self.ws.n
@@ -129,7 +141,7 @@ class OzakiProducts:
         self._hp(self.ea_x, self.eb_q, ws.that)                          # T^ = P Q
         self._hp(self.ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True)  # Y = Q^H Q - I
 
-    def update(self, restore_full_sigma):
+    def update(self, restore_full_sigma, sigma_bound=None):
         ws, hp, lp, n = self.ws, self.hp, self.lp, self.ws.n
         _downcast_y(ws)
         ozaki.encode(ws.w_lp, n, n, "b", lp, out=self.lb)                # W, B role (all lp products)
@@ -147,10 +159,21 @@ class OzakiProducts:
             ozaki.encode(ws.w2y, n, n, "a", lp, out=self.la)
             self._lp(self.la, self.lb, ws.w2yw)                          # W^2 Y W
         _sigma(ws, restore_full_sigma, False)                             # S' = S - 2I
-        ozaki.encode(ws.q, n, n, "a", hp, out=self.ea_x)
-        ozaki.encode(ws.sigma, n, n, "b", hp, out=self.eb_s)
-        self._hp(self.ea_x, self.eb_s, ws.q_next, alpha=0.5, add=ws.q)  # Q + Q S' / 2
+        pc = hp if sigma_bound is None else self._correction_plan(sigma_bound)
+        ozaki.encode(ws.q, n, n, "a", pc, out=self.ea_x)
+        ozaki.encode(ws.sigma, n, n, "b", pc, out=self.eb_s)
+        self._hp_with(pc, self.ea_x, self.eb_s, ws.q_next, alpha=0.5, add=ws.q)  # Q + Q S' / 2
         ws.q, ws.q_next = ws.q_next, ws.q
+
+
+def sigma_prime_bound(norm_y, norm_w, restore_full_sigma):
+    """||S'||_F bound for S' = S - 2I = 2W - Y - YW + W^2 + W^3 (+ W^2 Y + W^2 Y W)
+    from ||Y||_F and ||W||_F (sigma_merged_kernel, orthogonal.py:191-200)."""
+    y, w = float(norm_y), float(norm_w)
+    b = 2 * w + y + y * w + w * w + w ** 3
+    if restore_full_sigma:
+        b += w * w * y + w * w * y * w
+    return b * (1 + 1e-6)
 
 
 def make(kind, ws, a):

@@ -136,6 +136,12 @@ class _Fp64Workspace:
     def ptr(self, i):
         return self.scal.data_ptr() + 8 * i
 
+    def fro_norm(self, x):
+        """||x||_F of a ZPlanar (deterministic reduction; one host sync)."""
+        _lib.call("sr_fro_norm_f64", self.n, self.n, x.re_ptr(), x.im_ptr(), x.ld, self.ptr(5),
+                  self.red[0].data_ptr(), self.red[0].numel(), _stream())
+        return float(self.scal[5].cpu())
+
 
 def _stream():
     return torch.cuda.current_stream().cuda_stream
@@ -290,7 +296,8 @@ def _run_fp64(a, qhat, cfg, ws):
         skip = (converged and cfg.skip_final_ortho and norm_y <= 10.0 * n * U_FP64
                 and norm_w <= math.sqrt(U_FP64))
         if not skip:
-            prod.update(cfg.restore_full_sigma)
+            prod.update(cfg.restore_full_sigma,
+                        sigma_bound=products.sigma_prime_bound(norm_y, norm_w, cfg.restore_full_sigma))
             _mark("update")
         if converged:
             status, iterations, skip_fired = RefineStatus.CONVERGED, it, skip

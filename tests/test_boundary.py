@@ -51,3 +51,21 @@ def test_refine_config_validation():
     with pytest.raises(ValueError):
         RefineConfig(precision="fp32")
     assert RefineConfig().precision == "dd"
+
+
+def test_correction_beta_tracks_the_correction_size():
+    """Operand precision of the correction products (Q + Q S'/2): full hp for
+    an O(1) correction, fewer bits (fewer moduli) as ||S'|| shrinks, never below
+    the lp precision; a non-finite bound falls back to full hp."""
+    from paper_2203_10879_b200 import ozaki
+    n = 8192
+    assert ozaki.correction_beta(1.0, n) == ozaki.HP_BETA
+    assert ozaki.correction_beta(1e-6, n) == 53 + 3 - 19 + 7
+    assert ozaki.correction_beta(1e-30, n) == ozaki.LP_BETA
+    assert ozaki.correction_beta(0.0, n) == ozaki.LP_BETA
+    assert ozaki.correction_beta(float("nan"), n) == ozaki.HP_BETA
+    assert ozaki.correction_beta(float("inf"), n) == ozaki.HP_BETA
+    betas = [ozaki.correction_beta(10.0 ** -k, n) for k in range(0, 20)]
+    assert betas == sorted(betas, reverse=True)
+    mods = [ozaki.plan(n, b, b).nmod for b in betas]
+    assert mods[0] == ozaki.plan(n, ozaki.HP_BETA, ozaki.HP_BETA).nmod and mods[-1] < mods[0]

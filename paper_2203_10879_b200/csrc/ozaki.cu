@@ -345,23 +345,26 @@ __global__ void __launch_bounds__(256) decode_kernel(const __grid_constant__ Dec
 #pragma unroll
         for (int j = 0; j < NC; ++j) S[e][j] = 0.0;
       const int8_t* r = res + (size_t)plane * p.res_plane + (size_t)i * p.res_pitch + j0;
-      // issue every residue load first (MAXMOD words in flight per thread)
-      uint32_t wv[MAXMOD];
+      // residue words in groups of 8 moduli (8 loads in flight, bounded registers)
+#pragma unroll 1
+      for (int l0 = 0; l0 < p.nmod; l0 += 8) {
+        uint32_t wv[8];
 #pragma unroll
-      for (int l = 0; l < MAXMOD; ++l)
-        if (l < p.nmod) wv[l] = *reinterpret_cast<const uint32_t*>(r + (size_t)l * p.res_mod);
+        for (int g = 0; g < 8; ++g)
+          if (l0 + g < p.nmod) wv[g] = *reinterpret_cast<const uint32_t*>(r + (size_t)(l0 + g) * p.res_mod);
 #pragma unroll
-      for (int l = 0; l < MAXMOD; ++l) {
-        if (l >= p.nmod) break;
-        // int8 -> double without I2F: the byte with its sign bit flipped is
-        // x + 128 in [0, 255]; as the low word of 0x4338000000000000 it reads
-        // 1.5 * 2^52 + x + 128, so one DADD recovers x exactly.
-        const uint32_t w4 = wv[l] ^ 0x80808080u;
+        for (int g = 0; g < 8; ++g) {
+          if (l0 + g >= p.nmod) break;
+          // int8 -> double without I2F: the byte with its sign bit flipped is
+          // x + 128 in [0, 255]; as the low word of 0x4338000000000000 it reads
+          // 1.5 * 2^52 + x + 128, so one DADD recovers x exactly.
+          const uint32_t w4 = wv[g] ^ 0x80808080u;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const double x = __hiloint2double(0x43380000, (w4 >> (8 * e)) & 0xFF) - 6755399441055872.0;
+          for (int e = 0; e < 4; ++e) {
+            const double x = __hiloint2double(0x43380000, (w4 >> (8 * e)) & 0xFF) - 6755399441055872.0;
 #pragma unroll
-          for (int j = 0; j < NC; ++j) S[e][j] = fma(x, p.w[l][j], S[e][j]);  // exact: < 2^52
+            for (int j = 0; j < NC; ++j) S[e][j] = fma(x, p.w[l0 + g][j], S[e][j]);  // exact: < 2^52
+          }
         }
       }
 #pragma unroll
@@ -625,6 +628,8 @@ extern "C" int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* ta
   switch (nchunk) {
     case 1:
     case 2:
+      rc = dispatch_out<2>(out_kind, add_kind, grid, st, p, (const int8_t*)res, exps_a, exps_b, add, out);
+      break;
     case 3:
     case 4:
       rc = dispatch_out<4>(out_kind, add_kind, grid, st, p, (const int8_t*)res, exps_a, exps_b, add, out);

@@ -16,16 +16,19 @@
 //
 // The contributions of a solved tile (the "source") to the open tiles are
 // applied in one of three places, decided by the levels involved.  Levels are
-// grouped into batches of BW = 4; a source on level s (batch b = s / 4)
-//   * feeds the tiles of level s + 1 inside their SOLVE CTA (the critical path),
-//   * feeds the tiles of levels s + 2 .. 4b + 7 through the NEAR launch of
-//     level s + 1 (rank-NB tile updates, a narrow band of levels),
-//   * feeds every tile of level >= 4b + 8 through the FAR launches of batch b:
-//     once the four levels of batch b are solved, their sources for one column
-//     (row) of targets are four CONSECUTIVE tiles, so each target receives one
-//     rank-4NB update; the FAR launches run on their own stream, overlapped with
-//     the next four levels of SOLVE / NEAR, and write a second right-hand-side
-//     buffer (Rf) so they never race the near band's (Rn).
+// grouped into batches of BW = 4; a source on level s (batch b = s / 4) feeds
+//   * the tiles of level s + 1 inside their SOLVE CTA (the critical path),
+//   * the tiles of levels s + 2 .. 4 (b + 1 + FAR_LA) - 1 through the NEAR
+//     launch of level s + 1 (rank-NB tile updates, a narrow band of levels),
+//   * every tile of level >= 4 (b + 1 + FAR_LA) through the FAR launches of
+//     batch b: once the four levels of batch b are solved, their sources for
+//     one column (row) of targets are four CONSECUTIVE tiles, so each target
+//     receives one rank-4NB update; the FAR launches run on their own stream,
+//     overlapped with the next 4 FAR_LA levels of SOLVE / NEAR, and write a
+//     second right-hand-side buffer (Rf) so they never race the near band's (Rn).
+// (tests/test_trisolve_schedule.py checks on the CPU that these three sets
+// apply every (source, target) pair exactly once, after the source is solved
+// and before the target is.)
 // The far updates carry ~93 % of the n^3/3 complex multiply-adds, as register-
 // tiled complex GEMMs on the FP32 (FP64 in dd mode) pipe with cp.async double
 // buffering; the running right-hand sides are read and written once per batch
@@ -58,6 +61,7 @@ constexpr int NB = 32;
 constexpr int NT = 128;   // SOLVE / NEAR CTAs: 16 x 8 threads, each a 2 x 4 block of the tile
 constexpr int LD = NB + 1;
 constexpr int BW = 4;     // levels per far batch = tiles per far strip = source tiles per far update
+constexpr int FAR_LA = 1; // batches of slack: the far updates of batch b target levels >= 4 (b + 1 + FAR_LA)
 constexpr int FT = 256;   // FAR CTAs
 
 template <typename C>
@@ -178,8 +182,10 @@ __device__ __forceinline__ unsigned tile_solve_warp(const C* sT2, const C* sD, c
     pend[d] = (c >= 0) ? sR[i * LD + c] : czero<C>();
     tr[d] = (i + d < NB) ? sT2[i * LD + i + d] : czero<C>();
   }
-#pragma unroll 1
-  for (int t = 0; t < 2 * NB - 1; ++t) {
+  // 2 NB steps (the last one is idle for every lane), unrolled by 4 so that
+  // most of the window slide becomes register renaming
+#pragma unroll 4
+  for (int t = 0; t < 2 * NB; ++t) {
     const int j = t - (NB - 1) + i;  // this lane's column at step t
     const bool valid = (j >= 0) && (j < NB) && (i < valid_i) && (j < valid_j) && (!DIAG || i > j);
     C x = czero<C>();
@@ -362,6 +368,7 @@ __global__ void __launch_bounds__(NT) near_kernel(SweepArgs p, const C* __restri
 
 struct FarArgs {
   int n, N, beta, h, first;  // h = targets per source line; first = first column (COL) / row (ROW)
+  int first_level;           // first target level, 4 (beta + 1 + FAR_LA)
   long long ld;
 };
 
@@ -406,7 +413,7 @@ __global__ void __launch_bounds__(FT) far_kernel(FarArgs p, const C* __restrict_
   } else {
     const int I = line;
     out_r0 = I * NB;
-    out_c0 = (I - N + 4 * beta + 9 + t0) * NB;
+    out_c0 = (I - N + 1 + p.first_level + t0) * NB;
     src0 = I - N + 1 + 4 * beta;  // J of chunk 0
   }
   const int tid = threadIdx.x;
@@ -572,9 +579,12 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
   static cudaStream_t s_solve, s_near, s_far;
   static cudaEvent_t ev_in, ev_s, ev_u, ev_f[NFAR_EV];
   if (!configured) {
-    SR_CUDA_CHECK(cudaStreamCreateWithFlags(&s_solve, cudaStreamNonBlocking));
-    SR_CUDA_CHECK(cudaStreamCreateWithFlags(&s_near, cudaStreamNonBlocking));
-    SR_CUDA_CHECK(cudaStreamCreateWithFlags(&s_far, cudaStreamNonBlocking));
+    // priorities: the critical-path tile solves first, then the near band, the far batches last
+    int prio_lo = 0, prio_hi = 0;
+    SR_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    SR_CUDA_CHECK(cudaStreamCreateWithPriority(&s_solve, cudaStreamNonBlocking, prio_hi));
+    SR_CUDA_CHECK(cudaStreamCreateWithPriority(&s_near, cudaStreamNonBlocking, prio_hi + (prio_lo > prio_hi ? 1 : 0)));
+    SR_CUDA_CHECK(cudaStreamCreateWithPriority(&s_far, cudaStreamNonBlocking, prio_lo));
     SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
     SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_s, cudaEventDisableTiming));
     SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_u, cudaEventDisableTiming));
@@ -597,7 +607,8 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
   for (int lev = 0; lev < N; ++lev) {
     // SOLVE(lev): after NEAR(lev-1) (stream order + ev_u) and FAR(lev/4 - 2)
     if (lev >= 1) SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, ev_u, 0));
-    if (lev % BW == 0 && lev >= 2 * BW) SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, ev_f[(lev / BW - 2) % NFAR_EV], 0));
+    if (lev % BW == 0 && lev >= BW * (1 + FAR_LA))
+      SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, ev_f[(lev / BW - 1 - FAR_LA) % NFAR_EV], 0));
     SweepArgs a{n, N, lev, 0, ld};
     ksolve<<<lev + 1, NT, smem_solve, s_solve>>>(a, t, Rn, Rf, l, cl, d_clipped);
     SR_LAUNCH_CHECK();
@@ -605,7 +616,7 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
     if (lev >= 1) {
       SR_CUDA_CHECK(cudaStreamWaitEvent(s_near, ev_s, 0));  // SOLVE(lev-1)
       const int b = (lev - 1) / BW;
-      const int lmax = min(N - 1, BW * b + 2 * BW - 1);
+      const int lmax = min(N - 1, BW * (b + 1 + FAR_LA) - 1);
       if (lmax >= lev + 1) {
         a.lmax = lmax;
         dim3 grid(lmax + 1, lmax - lev);
@@ -616,21 +627,26 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
     SR_CUDA_CHECK(cudaEventRecord(ev_s, s_solve));
     SR_CUDA_CHECK(cudaEventRecord(ev_u, s_near));
     // FAR(b) once the last level of batch b is solved, if any tile sits on level >= 4b+8
+#ifndef SR_DIAG_NO_FAR  // timing diagnostic only (tools/solve_bench.py): wrong results without it
     if (lev % BW == BW - 1) {
+#else
+    if (false) {
+#endif
       const int b = lev / BW;
-      const int h = N - BW * b - 2 * BW;
+      const int first_level = BW * (b + 1 + FAR_LA);  // first far target level
+      const int h = N - first_level;
       if (h >= 1) {
         SR_CUDA_CHECK(cudaStreamWaitEvent(s_far, ev_s, 0));
         bool done = false;
         if constexpr (kC64) {
           if (use_tc) {
-            const int rc = far_tc_batch(plan, N, b, h, l, ld, Rf, s_far);
+            const int rc = far_tc_batch(plan, N, b, h, first_level, l, ld, Rf, s_far);
             if (rc != SR_OK) return rc;
             done = true;
           }
         }
         if (!done) {
-          FarArgs fa{n, N, b, h, 0, ld};
+          FarArgs fa{n, N, b, h, 0, first_level, ld};
           const int strips = (h + BW - 1) / BW;
           fa.first = 0;
           kfc<<<dim3(strips, min(BW * b + BW, N)), FT, smem_far_col, s_far>>>(fa, t, l, Rf);

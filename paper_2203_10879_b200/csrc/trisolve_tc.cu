@@ -6,26 +6,34 @@
 //   ROW  Rf[I, strip] += L[I, J0..J0+3] T[J0..J0+3, strip]    (strip = 4 tiles of row I)
 // (index sets in trisolve.cu).  Here each strip is one tcgen05 GEMM tile:
 //   * complex as real: with A' = a complex row read as interleaved (re, im)
-//     floats and B'^T rows 2c, 2c+1 = conj(b_c), i conj(b_c) (interleaved), the
+//     values and B'^T rows 2c, 2c+1 = conj(b_c), i conj(b_c) (interleaved), the
 //     real product A' B' is the interleaved complex product, so every operand is
-//     a plain K-major fp32 matrix and the accumulator columns come out as
-//     (re, im) pairs;
-//   * 3xTF32: every operand is split x = hi + lo (hi = x with the low 13
-//     mantissa bits cleared, exactly representable in TF32; lo = x - hi), and
-//     D += A_hi B_hi + A_hi B_lo + A_lo B_hi in FP32 TMEM accumulators, which is
-//     complex64-grade accuracy (the lp arithmetic of FP64 mode);
+//     a plain K-major matrix and the accumulator columns come out as (re, im);
+//   * scaled two-piece FP16: every A row and every B column is scaled by a power
+//     of two 2^-e to below 1 in magnitude (T: per row / per column of T, fixed
+//     for the solve; L: per column / row over the four source tiles of the
+//     batch), split x = hi + lo with hi = fp16(x), lo = fp16(x - hi), and
+//     D += A_hi B_hi + A_hi B_lo + A_lo B_hi (kind::f16, FP32 accumulation in
+//     TMEM) — ~22 significant bits per operand relative to its row / column
+//     maximum, i.e. complex64-grade products; the epilogue multiplies by
+//     2^(e_row + e_col) before updating Rf;
 //   * COL: M = 128 strip rows, N = 64 (32 complex columns of tile M), K = 256
 //     (4 source tiles x 32 complex);  ROW runs the transposed product
 //     C^T = T^T L^T so that its 128 strip columns are the MMA's M dimension.
 // Operand forms (built on the far stream, never on the critical path):
-//   tform / ttform  hi, lo planes of T and T^T (once per solve)
+//   tform / ttform  hi, lo planes of scaled T and T^T (once per solve; the
+//                   row / column maxima of T in tmax_r / tmax_c)
 //   lb              rows 2c, 2c+1 = conj(L[:, c]), i conj(L[:, c])   (COL B operand)
 //   lc              rows 2i, 2i+1 = conj(L[i, :]), i conj(L[i, :])   (ROW B operand)
-// (the L forms of batch b are written right before its far updates).  TMA
-// loads both planes of a 64-byte K block per operand (64-byte swizzle, zero
+//                   (per batch, right before its far updates; scaled by the
+//                   column / row maxima of the batch's source tiles, lmax_c / lmax_r)
+// TMA loads both planes of a 64-byte K block per operand (64-byte swizzle, zero
 // fill outside the matrix, which also supplies the non-existent source tiles),
-// a 2-stage mbarrier ring feeds the single-thread MMA issuer (4 CTAs per SM), and four
-// epilogue warps read the 128 x 64 accumulator with tcgen05.ld and update Rf.
+// persistent CTAs (one per SM) loop over the strips: a 4-stage mbarrier ring
+// feeds the single-thread MMA issuer, and four epilogue warps drain one of two
+// 64-column TMEM accumulators while the MMAs of the next strip run.
+#include <cuda_fp16.h>
+
 #include "trisolve_tc.cuh"
 #include "tc_common.cuh"
 
@@ -33,20 +41,62 @@ namespace {
 
 constexpr int NB = 32;
 constexpr int BW = 4;
-constexpr int KB_F = 16;                           // fp32 per 64-byte K block
-constexpr int NKB = BW * NB * 2 / KB_F;            // 16 K blocks per strip
-constexpr int TC_STAGES = 2;  // 50 KB of shared memory: 4 CTAs per SM hide each other's latency
+constexpr int KB_H = 32;                           // fp16 per 64-byte K block
+constexpr int NKB = BW * NB * 2 / KB_H;            // 8 K blocks per strip
+// persistent CTAs, one per SM; 4 stages keep 130 KB of shared memory so a
+// critical-path SOLVE CTA (84 KB) still fits beside it on the same SM
+constexpr int TC_STAGES = 4;
 constexpr int A_PLANE = 128 * 64;                  // bytes: 128 rows x 64 B
 constexpr int B_PLANE = 64 * 64;                   // bytes: 64 rows x 64 B
 constexpr int TC_STAGE = 2 * A_PLANE + 2 * B_PLANE;
 constexpr int TC_THREADS = 192;
-constexpr uint32_t TC_TMEM_COLS = 64;
+constexpr uint32_t TC_TMEM_COLS = 128;             // two 64-column accumulators
+constexpr int EPI_BYTES = 4 * 32 * 33 * 8;          // COL epilogue staging (4 warps x 32 x 33 float2)
+constexpr int TC_SMEM = 1024 + TC_STAGES * TC_STAGE + EPI_BYTES + 256;
 
-__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+// exponent e with max < 2^e (0 for an all-zero line): the line is scaled by 2^-e
+__device__ __forceinline__ int line_exp(float mx) { return mx > 0.f ? ilogbf(mx) + 1 : 0; }
 
-// hi / lo planes of T (row-major) and T^T, as interleaved fp32
+__device__ __forceinline__ void put_h2(__half* base, size_t plane, size_t off, float x, float y) {
+  const __half2 h = __floats2half2_rn(x, y);
+  const float2 hf = __half22float2(h);
+  *reinterpret_cast<__half2*>(base + off) = h;
+  *reinterpret_cast<__half2*>(base + plane + off) = __floats2half2_rn(x - hf.x, y - hf.y);
+}
+
+__device__ __forceinline__ void atomic_max_pos(float* a, float v) {  // v >= 0: float order == int order
+  atomicMax(reinterpret_cast<int*>(a), __float_as_int(v));
+}
+
+__device__ __forceinline__ float max4(const float* a, size_t n, int i) {
+  return fmaxf(fmaxf(a[i], a[n + i]), fmaxf(a[2 * n + i], a[3 * n + i]));
+}
+
+// row / column maxima of |re|, |im| of T (arrays zeroed by the caller)
+__global__ void __launch_bounds__(256) tmax_kernel(int n, const float2* __restrict__ T, long long ld,
+                                                   float* __restrict__ rmax, float* __restrict__ cmax) {
+  const int r0 = blockIdx.y * NB, c0 = blockIdx.x * NB;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  float cm = 0.f;
+  for (int r = ty; r < NB; r += 8) {
+    const int gr = r0 + r, gc = c0 + tx;
+    float m = 0.f;
+    if (gr < n && gc < n) {
+      const float2 v = T[(size_t)gr * ld + gc];
+      m = fmaxf(fabsf(v.x), fabsf(v.y));
+    }
+    cm = fmaxf(cm, m);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (tx == 0 && gr < n && m > 0.f) atomic_max_pos(rmax + gr, m);
+  }
+  if (c0 + tx < n && cm > 0.f) atomic_max_pos(cmax + c0 + tx, cm);
+}
+
+// hi / lo planes of the scaled T (rows scaled by tmax_r) and T^T (rows = columns of T, scaled by tmax_c)
 __global__ void __launch_bounds__(256) tforms_kernel(int n, const float2* __restrict__ T, long long ld,
-                                                     float* __restrict__ tf, float* __restrict__ ttf, int P) {
+                                                     const float* __restrict__ rmax, const float* __restrict__ cmax,
+                                                     __half* __restrict__ tf, __half* __restrict__ ttf, int P) {
   __shared__ float2 s[NB][NB + 1];
   const int r0 = blockIdx.y * NB, c0 = blockIdx.x * NB;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -56,9 +106,8 @@ __global__ void __launch_bounds__(256) tforms_kernel(int n, const float2* __rest
     float2 v = make_float2(0.f, 0.f);
     if (gr < n && gc < n) {
       v = T[(size_t)gr * ld + gc];
-      const float2 h = make_float2(tf32_hi(v.x), tf32_hi(v.y));
-      *reinterpret_cast<float2*>(tf + (size_t)gr * P + 2 * gc) = h;
-      *reinterpret_cast<float2*>(tf + plane + (size_t)gr * P + 2 * gc) = make_float2(v.x - h.x, v.y - h.y);
+      const int e = line_exp(rmax[gr]);
+      put_h2(tf, plane, (size_t)gr * P + 2 * gc, ldexpf(v.x, -e), ldexpf(v.y, -e));
     }
     s[r][tx] = v;
   }
@@ -67,23 +116,50 @@ __global__ void __launch_bounds__(256) tforms_kernel(int n, const float2* __rest
     const int gr = c0 + r, gc = r0 + tx;
     if (gr < n && gc < n) {
       const float2 v = s[tx][r];
-      const float2 h = make_float2(tf32_hi(v.x), tf32_hi(v.y));
-      *reinterpret_cast<float2*>(ttf + (size_t)gr * P + 2 * gc) = h;
-      *reinterpret_cast<float2*>(ttf + plane + (size_t)gr * P + 2 * gc) = make_float2(v.x - h.x, v.y - h.y);
+      const int e = line_exp(cmax[gr]);
+      put_h2(ttf, plane, (size_t)gr * P + 2 * gc, ldexpf(v.x, -e), ldexpf(v.y, -e));
     }
   }
 }
 
-__device__ __forceinline__ void put_split(float* base, size_t plane, size_t off, float x, float y) {
-  const float2 h = make_float2(tf32_hi(x), tf32_hi(y));
-  *reinterpret_cast<float2*>(base + off) = h;
-  *reinterpret_cast<float2*>(base + plane + off) = make_float2(x - h.x, y - h.y);
+// Column / row maxima of the L tiles on levels 4b .. 4b+3 into lmax_c[level - 4b][.],
+// lmax_r[level - 4b][.] (zeroed by the caller; blockIdx.y = level - 4b, blockIdx.x = M)
+__global__ void __launch_bounds__(256) lmax_kernel(int n, int N, int b, const float2* __restrict__ L, long long ld,
+                                                   float* __restrict__ lmax_c, float* __restrict__ lmax_r) {
+  __shared__ float s[NB][NB + 1];
+  const int level = BW * b + blockIdx.y;
+  const int M = blockIdx.x;
+  if (level > N - 1 || M > level) return;
+  const int I = M + N - 1 - level;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < NB; r += 8) {
+    const int gr = I * NB + r, gc = M * NB + tx;
+    float m = 0.f;
+    if (gr < n && gc < n) {
+      const float2 v = L[(size_t)gr * ld + gc];
+      m = fmaxf(fabsf(v.x), fabsf(v.y));
+    }
+    s[r][tx] = m;
+  }
+  __syncthreads();
+  if (ty == 0) {  // column maxima
+    float m = 0.f;
+    for (int r = 0; r < NB; ++r) m = fmaxf(m, s[r][tx]);
+    if (M * NB + tx < n) lmax_c[(size_t)blockIdx.y * n + M * NB + tx] = m;
+  } else if (ty == 1) {  // row maxima
+    float m = 0.f;
+    for (int c = 0; c < NB; ++c) m = fmaxf(m, s[tx][c]);
+    if (I * NB + tx < n) lmax_r[(size_t)blockIdx.y * n + I * NB + tx] = m;
+  }
 }
 
 // L forms of the tiles on levels 4b .. 4b+3 (blockIdx.y = level - 4b, blockIdx.x = M)
 __global__ void __launch_bounds__(256) lforms_kernel(int n, int N, int b, const float2* __restrict__ L, long long ld,
-                                                     float* __restrict__ lb, float* __restrict__ lc, int P) {
+                                                     const float* __restrict__ lmax_c,
+                                                     const float* __restrict__ lmax_r, __half* __restrict__ lb,
+                                                     __half* __restrict__ lc, int P) {
   __shared__ float2 s[NB][NB + 1];
+  __shared__ int ec[NB], er[NB];
   const int level = BW * b + blockIdx.y;
   const int M = blockIdx.x;
   if (level > N - 1 || M > level) return;
@@ -93,44 +169,52 @@ __global__ void __launch_bounds__(256) lforms_kernel(int n, int N, int b, const 
     const int gr = I * NB + r, gc = M * NB + tx;
     s[r][tx] = (gr < n && gc < n) ? L[(size_t)gr * ld + gc] : make_float2(0.f, 0.f);
   }
+  if (ty == 0) ec[tx] = M * NB + tx < n ? line_exp(max4(lmax_c, n, M * NB + tx)) : 0;
+  if (ty == 1) er[tx] = I * NB + tx < n ? line_exp(max4(lmax_r, n, I * NB + tx)) : 0;
   __syncthreads();
   const size_t plane = (size_t)2 * n * P;
   for (int c = ty; c < NB; c += 8) {  // LB rows 2C, 2C+1 (C = column of L), cols 2K (K = row of L)
     const int C = M * NB + c, K = I * NB + tx;
     if (C < n && K < n) {
       const float2 v = s[tx][c];
-      put_split(lb, plane, (size_t)(2 * C) * P + 2 * K, v.x, -v.y);
-      put_split(lb, plane, (size_t)(2 * C + 1) * P + 2 * K, v.y, v.x);
+      const float x = ldexpf(v.x, -ec[c]), y = ldexpf(v.y, -ec[c]);
+      put_h2(lb, plane, (size_t)(2 * C) * P + 2 * K, x, -y);
+      put_h2(lb, plane, (size_t)(2 * C + 1) * P + 2 * K, y, x);
     }
   }
   for (int i = ty; i < NB; i += 8) {  // LC rows 2R, 2R+1 (R = row of L), cols 2K (K = column of L)
     const int R = I * NB + i, K = M * NB + tx;
     if (R < n && K < n) {
       const float2 v = s[i][tx];
-      put_split(lc, plane, (size_t)(2 * R) * P + 2 * K, v.x, -v.y);
-      put_split(lc, plane, (size_t)(2 * R + 1) * P + 2 * K, v.y, v.x);
+      const float x = ldexpf(v.x, -er[i]), y = ldexpf(v.y, -er[i]);
+      put_h2(lc, plane, (size_t)(2 * R) * P + 2 * K, x, -y);
+      put_h2(lc, plane, (size_t)(2 * R + 1) * P + 2 * K, y, x);
     }
   }
 }
 
-__device__ __forceinline__ constexpr uint32_t idesc_tf32(int m, int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+__device__ __forceinline__ constexpr uint32_t idesc_f16(int m, int n) {
+  // D = F32, A = B = F16, K-major operands
+  return (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
-__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
 struct FarTcArgs {
-  int n, N, b, h, first;
+  int n, N, b, h, first, lines, strips;
+  int first_level;  // first far target level
   long long ld;
+  const float* a_max;  // A-line maxima: T rows (COL) or T columns (ROW)
+  const float* b_max;  // [4][n] source-tile maxima: L columns (COL) or L rows (ROW)
 };
 
 template <bool ROW>
@@ -138,37 +222,45 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     far_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                   const __grid_constant__ FarTcArgs p, float2* __restrict__ Rf) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ int eb_s[4][32];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* bars = (uint64_t*)(smem + TC_STAGES * TC_STAGE);  // full[S], empty[S], done
-  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * TC_STAGES + 1);
+  float2* stage_buf = reinterpret_cast<float2*>(smem + TC_STAGES * TC_STAGE);  // COL epilogue staging, 4 x 32 x 33
+  uint64_t* bars = (uint64_t*)(smem + TC_STAGES * TC_STAGE + EPI_BYTES);
+  // full[S], empty[S], tfull[2], tempty[2]; then the TMEM base slot
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * TC_STAGES + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (TC_STAGES + s); };
-  const uint32_t done_bar = bar0 + 8u * (2 * TC_STAGES);
+  auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * TC_STAGES + a); };
+  auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * TC_STAGES + 2 + a); };
 
   const int N = p.N, b = p.b;
-  const int line = p.first + blockIdx.y;
-  const int t0 = BW * blockIdx.x;
-  int a_row0, b_row0, k0;  // A rows (strip), B rows (2 x the tile's rows / cols), first K' column
-  if (!ROW) {
-    const int M = line;
-    a_row0 = (M + t0) * NB;
-    b_row0 = 2 * M * NB;
-    k0 = (M + N - BW * b - BW) * NB * 2;
-  } else {
-    const int I = line;
-    a_row0 = (I - N + BW * b + 2 * BW + 1 + t0) * NB;
-    b_row0 = 2 * I * NB;
-    k0 = (I - N + 1 + BW * b) * NB * 2;
-  }
+  const int units = p.lines * p.strips;
+  // unit -> (line, first target t0) and the A / B / K origins of its strip
+  auto unit = [&](int u, int& line, int& t0, int& a_row0, int& b_row0, int& k0) {
+    line = p.first + u / p.strips;
+    t0 = BW * (u % p.strips);
+    if (!ROW) {
+      a_row0 = (line + t0) * NB;
+      b_row0 = 2 * line * NB;
+      k0 = (line + N - BW * b - BW) * NB * 2;
+    } else {
+      a_row0 = (line - N + 1 + p.first_level + t0) * NB;
+      b_row0 = 2 * line * NB;
+      k0 = (line - N + 1 + BW * b) * NB * 2;
+    }
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < TC_STAGES; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
-    mbar_init(done_bar, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&map_a) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&map_b) : "memory");
@@ -184,82 +276,126 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // TMA producer
-      for (int kb = 0; kb < NKB; ++kb) {
-        const int s = kb % TC_STAGES;
-        if (kb >= TC_STAGES) mbar_wait(empty_bar(s), ((kb / TC_STAGES) - 1) & 1);
-        uint8_t* st = smem + s * TC_STAGE;
-        mbar_expect_tx(full_bar(s), TC_STAGE);
-        tma_load_3d(smem_u32(st), &map_a, full_bar(s), k0 + kb * KB_F, a_row0, 0);
-        tma_load_3d(smem_u32(st + 2 * A_PLANE), &map_b, full_bar(s), k0 + kb * KB_F, b_row0, 0);
+    if (lane == 0) {  // TMA producer: runs ahead across units through the stage ring
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int line, t0, a_row0, b_row0, k0;
+        unit(u, line, t0, a_row0, b_row0, k0);
+        for (int kb = 0; kb < NKB; ++kb, ++it) {
+          const int s = it % TC_STAGES;
+          if (it >= TC_STAGES) mbar_wait(empty_bar(s), ((it / TC_STAGES) - 1) & 1);
+          uint8_t* st = smem + s * TC_STAGE;
+          mbar_expect_tx(full_bar(s), TC_STAGE);
+          tma_load_3d(smem_u32(st), &map_a, full_bar(s), k0 + kb * KB_H, a_row0, 0);
+          tma_load_3d(smem_u32(st + 2 * A_PLANE), &map_b, full_bar(s), k0 + kb * KB_H, b_row0, 0);
+        }
       }
     }
-  } else if (warp == 1) {  // MMA issuer
-    const uint32_t id = idesc_tf32(128, 64);
-    for (int kb = 0; kb < NKB; ++kb) {
-      const int s = kb % TC_STAGES;
-      mbar_wait(full_bar(s), (kb / TC_STAGES) & 1);
+  } else if (warp == 1) {  // MMA issuer: two TMEM accumulators, epilogue of unit i overlaps MMAs of unit i+1
+    const uint32_t id = idesc_f16(128, 64);
+    int it = 0, acc = 0, k = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+      acc = k & 1;
+      mbar_wait(tempty_bar(acc), ((k >> 1) & 1) ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      if (lane == 0) {
-        const uint32_t sa = smem_u32(smem + s * TC_STAGE);
-        const uint32_t sb = sa + 2 * A_PLANE;
+      const uint32_t d = tmem_base + (uint32_t)(acc * 64);
+      for (int kb = 0; kb < NKB; ++kb, ++it) {
+        const int s = it % TC_STAGES;
+        mbar_wait(full_bar(s), (it / TC_STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(smem + s * TC_STAGE);
+          const uint32_t sb = sa + 2 * A_PLANE;
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {  // two K = 8 tf32 steps per 64-byte block
-          const uint64_t ahi = umma_desc_sw64(sa + ks * 32), alo = umma_desc_sw64(sa + A_PLANE + ks * 32);
-          const uint64_t bhi = umma_desc_sw64(sb + ks * 32), blo = umma_desc_sw64(sb + B_PLANE + ks * 32);
-          umma_tf32(tmem_base, ahi, bhi, id, (kb | ks) != 0);
-          umma_tf32(tmem_base, ahi, blo, id, 1u);
-          umma_tf32(tmem_base, alo, bhi, id, 1u);
+          for (int ks = 0; ks < 2; ++ks) {  // two K = 16 fp16 steps per 64-byte block
+            const uint64_t ahi = umma_desc_sw64(sa + ks * 32), alo = umma_desc_sw64(sa + A_PLANE + ks * 32);
+            const uint64_t bhi = umma_desc_sw64(sb + ks * 32), blo = umma_desc_sw64(sb + B_PLANE + ks * 32);
+            umma_f16(d, ahi, bhi, id, (kb | ks) != 0);
+            umma_f16(d, ahi, blo, id, 1u);
+            umma_f16(d, alo, bhi, id, 1u);
+          }
+          umma_commit(empty_bar(s));
+          if (kb == NKB - 1) umma_commit(tfull_bar(acc));
         }
-        umma_commit(empty_bar(s));
-        if (kb == NKB - 1) umma_commit(done_bar);
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else {  // epilogue: warps 2..5, TMEM lane quadrant warp & 3
     const int ew = warp & 3;
-    mbar_wait(done_bar, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    uint32_t v[64];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t (&vq)[16] = *reinterpret_cast<uint32_t(*)[16]>(&v[16 * q]);
-      tmem_ld16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(16 * q), vq);
-    }
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
     const int n = p.n;
     const long long ld = p.ld;
-    const int tgt = t0 + ew;  // target tile index along the line
-    const int idx = a_row0 + ew * 32 + lane;  // COL: global row;  ROW: global column
-    if (tgt < p.h && (!ROW || idx < n)) {
-      if (!ROW) {
-        // stage the warp's 32 x 32 block in (now idle) pipeline smem, then
-        // update Rf row by row with coalesced 256-byte accesses
-        float2* buf = reinterpret_cast<float2*>(smem) + ew * 32 * 33;
+    float2* buf = stage_buf + ew * 32 * 33;
+    int k = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+      const int acc = k & 1;
+      int line, t0, a_row0, b_row0, k0;
+      unit(u, line, t0, a_row0, b_row0, k0);
+      // scale exponents: A line of this lane, B lines of the tile (L column / row line * 32 + j)
+      const int idx = a_row0 + ew * 32 + lane;  // TMEM lane: COL global row;  ROW global column
+      const int ea = idx < n ? line_exp(p.a_max[idx]) : 0;
+      const int jl = line * NB + lane;
+      __syncwarp();
+      eb_s[ew][lane] = jl < n ? line_exp(max4(p.b_max, (size_t)n, jl)) : 0;
+      __syncwarp();
+      mbar_wait(tfull_bar(acc), (k >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      uint32_t v[64];
 #pragma unroll
-        for (int c = 0; c < NB; ++c) buf[lane * 33 + c] = make_float2(__uint_as_float(v[2 * c]), __uint_as_float(v[2 * c + 1]));
-        __syncwarp();
-        const int c0 = line * NB, row0 = a_row0 + ew * 32;
-        for (int r = 0; r < 32 && row0 + r < n; ++r) {
-          if (c0 + lane < n) {
-            float2* dst = Rf + (size_t)(row0 + r) * ld + c0 + lane;
-            const float2 a = buf[r * 33 + lane];
-            float2 q = *dst;
-            q.x -= a.x;
-            q.y -= a.y;
-            *dst = q;
+      for (int q = 0; q < 4; ++q) {
+        uint32_t (&vq)[16] = *reinterpret_cast<uint32_t(*)[16]>(&v[16 * q]);
+        tmem_ld16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * 64 + 16 * q), vq);
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      mbar_arrive(tempty_bar(acc));  // the accumulator is in registers: release it to the MMA warp
+      const int tgt = t0 + ew;       // target tile index along the line
+      if (tgt < p.h) {
+        if (!ROW) {
+          // stage the warp's 32 x 32 block, then update Rf row by row with
+          // coalesced 256-byte accesses
+#pragma unroll
+          for (int c = 0; c < NB; ++c) {
+            const float sc = ldexpf(1.f, ea + eb_s[ew][c]);
+            buf[lane * 33 + c] = make_float2(__uint_as_float(v[2 * c]) * sc, __uint_as_float(v[2 * c + 1]) * sc);
           }
-        }
-      } else {
-        const int r0 = line * NB;
+          __syncwarp();
+          // read-modify-write in groups of 16 rows: the 16 loads are independent
+          // and in flight together (one dependent load per row would serialise
+          // the epilogue on the memory latency)
+          const int c0 = line * NB, row0 = a_row0 + ew * 32;
+          const bool colok = c0 + lane < n;
 #pragma unroll
-        for (int i = 0; i < NB; ++i) {
-          if (r0 + i < n) {
-            float2* dst = Rf + (size_t)(r0 + i) * ld + idx;
-            float2 r = *dst;
-            r.x += __uint_as_float(v[2 * i]);
-            r.y += __uint_as_float(v[2 * i + 1]);
-            *dst = r;
+          for (int g = 0; g < 32; g += 16) {
+            float2 q[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r)
+              q[r] = (colok && row0 + g + r < n) ? Rf[(size_t)(row0 + g + r) * ld + c0 + lane] : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+              if (colok && row0 + g + r < n) {
+                const float2 a = buf[(g + r) * 33 + lane];
+                Rf[(size_t)(row0 + g + r) * ld + c0 + lane] = make_float2(q[r].x - a.x, q[r].y - a.y);
+              }
+            }
+          }
+          __syncwarp();
+        } else if (idx < n) {
+          const int r0 = line * NB;
+#pragma unroll
+          for (int g = 0; g < NB; g += 16) {
+            float2 q[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              q[i] = r0 + g + i < n ? Rf[(size_t)(r0 + g + i) * ld + idx] : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              if (r0 + g + i < n) {
+                const float sc = ldexpf(1.f, ea + eb_s[ew][g + i]);
+                Rf[(size_t)(r0 + g + i) * ld + idx] =
+                    make_float2(q[i].x + __uint_as_float(v[2 * (g + i)]) * sc,
+                                q[i].y + __uint_as_float(v[2 * (g + i) + 1]) * sc);
+              }
+            }
           }
         }
       }
@@ -273,73 +409,94 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-inline int pitch_f(int n) { return 2 * (n + (n & 1)); }  // fp32 per row: 2 even(n), a multiple of 4
+inline int pitch_h(int n) { return (2 * n + 7) / 8 * 8; }  // fp16 per row, 16-byte multiple
 
-// 3-d map over [2 planes][rows][P] fp32 (logical width 2n), box (16, box_rows, 2), 64-byte swizzle
-int make_form_map(CUtensorMap* map, const float* base, int n, int rows, int P, int box_rows) {
+// 3-d map over [2 planes][rows][P] fp16 (logical width 2n), box (32, box_rows, 2), 64-byte swizzle
+int make_form_map(CUtensorMap* map, const __half* base, int n, int rows, int P, int box_rows) {
   auto enc = get_encode();
   if (!enc) return SR_ECUDA;
   cuuint64_t dims[3] = {(cuuint64_t)(2 * n), (cuuint64_t)rows, 2};
-  cuuint64_t strides[2] = {(cuuint64_t)P * 4, (cuuint64_t)P * 4 * (cuuint64_t)rows};
-  cuuint32_t box[3] = {(cuuint32_t)KB_F, (cuuint32_t)box_rows, 2};
+  cuuint64_t strides[2] = {(cuuint64_t)P * 2, (cuuint64_t)P * 2 * (cuuint64_t)rows};
+  cuuint32_t box[3] = {(cuuint32_t)KB_H, (cuuint32_t)box_rows, 2};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<__half*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? SR_OK : SR_ECUDA;
 }
 
-}  // namespace
-
-size_t far_tc_forms_bytes(int n) {
-  if (n <= 0) return 0;
-  const size_t P = (size_t)pitch_f(n);
-  const size_t t = align_up(2 * (size_t)n * P * 4, 1024);
-  const size_t l = align_up(2 * (size_t)(2 * n) * P * 4, 1024);
-  return 2 * t + 2 * l + 1024;
+struct FormLayout {
+  size_t t, l, mx, total;
+};
+FormLayout form_layout(int n) {
+  const size_t P = (size_t)pitch_h(n);
+  FormLayout f;
+  f.t = align_up(2 * (size_t)n * P * 2, 1024);        // one T form: 2 planes x n rows of fp16
+  f.l = align_up(2 * (size_t)(2 * n) * P * 2, 1024);  // one L form: 2 planes x 2n rows
+  f.mx = align_up((size_t)n * 4 * 10, 1024);          // tmax_r, tmax_c, lmax_c[4], lmax_r[4]
+  f.total = 2 * f.t + 2 * f.l + f.mx + 1024;
+  return f;
 }
 
+}  // namespace
+
+size_t far_tc_forms_bytes(int n) { return n <= 0 ? 0 : form_layout(n).total; }
+
 int far_tc_prepare(FarTcPlan* plan, int n, const float2* T, long long ld, void* base, cudaStream_t st) {
-  const int P = pitch_f(n);
-  const size_t t = align_up(2 * (size_t)n * P * 4, 1024);
-  const size_t l = align_up(2 * (size_t)(2 * n) * P * 4, 1024);
+  const int P = pitch_h(n);
+  const FormLayout f = form_layout(n);
   char* p0 = (char*)(((uintptr_t)base + 1023) & ~(uintptr_t)1023);
   plan->n = n;
   plan->P = P;
-  plan->tform = (float*)p0;
-  plan->ttform = (float*)(p0 + t);
-  plan->lb = (float*)(p0 + 2 * t);
-  plan->lc = (float*)(p0 + 2 * t + l);
+  plan->tform = (__half*)p0;
+  plan->ttform = (__half*)(p0 + f.t);
+  plan->lb = (__half*)(p0 + 2 * f.t);
+  plan->lc = (__half*)(p0 + 2 * f.t + f.l);
+  float* mx = (float*)(p0 + 2 * f.t + 2 * f.l);
+  plan->tmax_r = mx;
+  plan->tmax_c = mx + n;
+  plan->lmax_c = mx + 2 * (size_t)n;
+  plan->lmax_r = mx + 6 * (size_t)n;
   if (make_form_map(&plan->a_col, plan->tform, n, n, P, 128) != SR_OK ||
       make_form_map(&plan->a_row, plan->ttform, n, n, P, 128) != SR_OK ||
       make_form_map(&plan->b_col, plan->lb, n, 2 * n, P, 64) != SR_OK ||
       make_form_map(&plan->b_row, plan->lc, n, 2 * n, P, 64) != SR_OK)
     return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(solver forms)");
+  SR_CUDA_CHECK(cudaMemsetAsync(plan->tmax_r, 0, 2 * (size_t)n * sizeof(float), st));
   const dim3 g(sr_ceil_div(n, NB), sr_ceil_div(n, NB));
-  tforms_kernel<<<g, 256, 0, st>>>(n, T, ld, plan->tform, plan->ttform, P);
+  tmax_kernel<<<g, 256, 0, st>>>(n, T, ld, plan->tmax_r, plan->tmax_c);
+  SR_LAUNCH_CHECK();
+  tforms_kernel<<<g, 256, 0, st>>>(n, T, ld, plan->tmax_r, plan->tmax_c, plan->tform, plan->ttform, P);
   SR_LAUNCH_CHECK();
   static bool configured = false;
   if (!configured) {
-    const int smem = 1024 + TC_STAGES * TC_STAGE + 256;
-    SR_CUDA_CHECK(cudaFuncSetAttribute(far_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    SR_CUDA_CHECK(cudaFuncSetAttribute(far_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SR_CUDA_CHECK(cudaFuncSetAttribute(far_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+    SR_CUDA_CHECK(cudaFuncSetAttribute(far_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
     configured = true;
   }
   return SR_OK;
 }
 
-int far_tc_batch(const FarTcPlan& plan, int N, int b, int h, const float2* L, long long ld, float2* Rf,
-                 cudaStream_t st) {
+int far_tc_batch(const FarTcPlan& plan, int N, int b, int h, int first_level, const float2* L, long long ld,
+                 float2* Rf, cudaStream_t st) {
   const int n = plan.n;
-  lforms_kernel<<<dim3(BW * b + BW, BW), 256, 0, st>>>(n, N, b, L, ld, plan.lb, plan.lc, plan.P);
+  SR_CUDA_CHECK(cudaMemsetAsync(plan.lmax_c, 0, 8 * (size_t)n * sizeof(float), st));
+  const dim3 gl(BW * b + BW, BW);
+  lmax_kernel<<<gl, 256, 0, st>>>(n, N, b, L, ld, plan.lmax_c, plan.lmax_r);
+  SR_LAUNCH_CHECK();
+  lforms_kernel<<<gl, 256, 0, st>>>(n, N, b, L, ld, plan.lmax_c, plan.lmax_r, plan.lb, plan.lc, plan.P);
   SR_LAUNCH_CHECK();
   const int strips = (h + BW - 1) / BW;
-  const int smem = 1024 + TC_STAGES * TC_STAGE + 256;
-  FarTcArgs a{n, N, b, h, 0, ld};
-  far_tc_kernel<false><<<dim3(strips, min(BW * b + BW, N)), TC_THREADS, smem, st>>>(plan.a_col, plan.b_col, a, Rf);
+  FarTcArgs a{n, N, b, h, 0, min(BW * b + BW, N), strips, first_level, ld, plan.tmax_r, plan.lmax_c};
+  const int grid_c = min(a.lines * strips, 148);
+  far_tc_kernel<false><<<grid_c, TC_THREADS, TC_SMEM, st>>>(plan.a_col, plan.b_col, a, Rf);
   SR_LAUNCH_CHECK();
   a.first = N - BW - BW * b;
-  far_tc_kernel<true><<<dim3(strips, N - a.first), TC_THREADS, smem, st>>>(plan.a_row, plan.b_row, a, Rf);
+  a.lines = N - a.first;
+  a.a_max = plan.tmax_c;
+  a.b_max = plan.lmax_r;
+  const int grid_r = min(a.lines * strips, 148);
+  far_tc_kernel<true><<<grid_r, TC_THREADS, TC_SMEM, st>>>(plan.a_row, plan.b_row, a, Rf);
   SR_LAUNCH_CHECK();
   return SR_OK;
 }

@@ -16,6 +16,7 @@ int sr_set_cuda_error(cudaError_t e, const char* what) {
 static std::atomic<unsigned long long> g_launches{0};
 
 void sr_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void sr_count_launches(unsigned long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
 extern "C" unsigned long long sr_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 

@@ -13,6 +13,8 @@
 
 int sr_set_cuda_error(cudaError_t e, const char* what);
 void sr_count_launch();
+void sr_count_launches(unsigned long long k);  // kernels replayed from a CUDA graph
+extern "C" unsigned long long sr_kernel_launches(void);
 
 // after every kernel launch: count it (sr_kernel_launches) and surface launch errors
 #define SR_LAUNCH_CHECK()                       \

@@ -534,15 +534,58 @@ constexpr int NFAR_EV = 4;
 
 inline size_t r_bytes(int n, long long ld, size_t elt) { return ((size_t)n * ld * elt + 255) & ~(size_t)255; }
 
+// Internal streams and events (created once per lp type): the critical-path
+// tile solves, the near band and the far batches; plus the captured graph of
+// the last problem (the refinement calls the solver with the same buffers every
+// iteration, so the N-level launch sequence is recorded once and replayed).
+struct SolveCtx {
+  bool ready = false;
+  cudaStream_t s_solve, s_near, s_far;
+  cudaEvent_t ev_in, ev_s, ev_u, ev_f[NFAR_EV], ev_j;
+  // graph of the last (args) seen
+  cudaGraphExec_t exec = nullptr;
+  unsigned long long kernels = 0;  // kernel nodes in the graph
+  const void *t = nullptr, *e = nullptr, *l = nullptr, *ws = nullptr, *clipped = nullptr, *flags = nullptr;
+  size_t ws_bytes = 0;
+  long long ld = 0;
+  int n = -1;
+  double clip = 0;
+  int calls = 0;  // eager calls with these args before capturing
+};
+
 template <typename C>
-int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsigned long long* d_clipped,
-          int* d_flags, void* ws, size_t ws_bytes, cudaStream_t st) {
-  if (n < 0 || ld < n) return SR_EINVAL;
-  if (n == 0) return SR_OK;
+int ctx_init(SolveCtx& c) {
+  if (c.ready) return SR_OK;
+  // priorities: the critical-path tile solves first, then the near band, the far batches last
+  int prio_lo = 0, prio_hi = 0;
+  SR_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  SR_CUDA_CHECK(cudaStreamCreateWithPriority(&c.s_solve, cudaStreamNonBlocking, prio_hi));
+  SR_CUDA_CHECK(cudaStreamCreateWithPriority(&c.s_near, cudaStreamNonBlocking, prio_hi + (prio_lo > prio_hi ? 1 : 0)));
+  SR_CUDA_CHECK(cudaStreamCreateWithPriority(&c.s_far, cudaStreamNonBlocking, prio_lo));
+  SR_CUDA_CHECK(cudaEventCreateWithFlags(&c.ev_in, cudaEventDisableTiming));
+  SR_CUDA_CHECK(cudaEventCreateWithFlags(&c.ev_s, cudaEventDisableTiming));
+  SR_CUDA_CHECK(cudaEventCreateWithFlags(&c.ev_u, cudaEventDisableTiming));
+  SR_CUDA_CHECK(cudaEventCreateWithFlags(&c.ev_j, cudaEventDisableTiming));
+  for (int i = 0; i < NFAR_EV; ++i) SR_CUDA_CHECK(cudaEventCreateWithFlags(&c.ev_f[i], cudaEventDisableTiming));
+  SR_CUDA_CHECK(cudaFuncSetAttribute(solve_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(C) * (9 * NB * LD + NB * NB))));
+  SR_CUDA_CHECK(cudaFuncSetAttribute(near_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(C) * 5 * NB * LD)));
+  SR_CUDA_CHECK(cudaFuncSetAttribute(far_kernel<C, false, FAR_STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(C) * FAR_STAGES * FarShape<C, false>::STAGE)));
+  SR_CUDA_CHECK(cudaFuncSetAttribute(far_kernel<C, true, FAR_STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(C) * FAR_STAGES * FarShape<C, true>::STAGE)));
+  c.ready = true;
+  return SR_OK;
+}
+
+// Enqueue one solve.  `origin` is the caller's stream (eager) or the context's
+// solve stream under capture; every forked stream is joined back into it.
+template <typename C>
+int enqueue(SolveCtx& c, int n, const C* t, const C* e, long long ld, C* l, double clip,
+            unsigned long long* d_clipped, int* d_flags, void* ws, cudaStream_t origin) {
   const int N = (n + NB - 1) / NB;
-  const size_t need = sr_trisolve_workspace_bytes(n, sizeof(C) == 8 ? 1 : 0);
   const size_t rb = r_bytes(n, ld, sizeof(C));
-  if (ws_bytes < need || !ws || 2 * rb + (sizeof(C) == 8 ? far_tc_forms_bytes(n) : 0) > need) return SR_EINVAL;
   C* Rn = (C*)ws;
   C* Rf = (C*)((char*)ws + rb);
   // complex64 with 16-byte aligned rows: far updates on the tensor cores (trisolve_tc.cu)
@@ -551,7 +594,7 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
   FarTcPlan plan;
   if constexpr (kC64) {
     if (use_tc) {
-      const int rc = far_tc_prepare(&plan, n, t, ld, (char*)ws + 2 * rb, st);
+      const int rc = far_tc_prepare(&plan, n, t, ld, (char*)ws + 2 * rb, origin);
       if (rc != SR_OK) return rc;
     }
   }
@@ -559,74 +602,45 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
     const long long total = (long long)n * n;
     const long long blocks = (total + 255) / 256;
     const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
-    init_kernel<C><<<grid, 256, 0, st>>>(n, e, Rn, Rf, l, ld);
+    init_kernel<C><<<grid, 256, 0, origin>>>(n, e, Rn, Rf, l, ld);
     SR_LAUNCH_CHECK();
     dim3 b(32, 8), g(sr_ceil_div(n, 32), sr_ceil_div(n, 8));
-    separation_kernel<C><<<g, b, 0, st>>>(n, t, ld, d_flags);
+    separation_kernel<C><<<g, b, 0, origin>>>(n, t, ld, d_flags);
     SR_LAUNCH_CHECK();
   }
   const size_t smem_solve = sizeof(C) * (9 * NB * LD + NB * NB);
   const size_t smem_near = sizeof(C) * 5 * NB * LD;
   const size_t smem_far_col = sizeof(C) * FAR_STAGES * FarShape<C, false>::STAGE;
   const size_t smem_far_row = sizeof(C) * FAR_STAGES * FarShape<C, true>::STAGE;
-  auto ksolve = solve_kernel<C>;
-  auto knear = near_kernel<C>;
-  auto kfc = far_kernel<C, false, FAR_STAGES>;
-  auto kfr = far_kernel<C, true, FAR_STAGES>;
-  // Three internal streams (created once): critical-path tile solves, the
-  // near-band updates and the far batches; events order them (see the header).
-  static bool configured = false;
-  static cudaStream_t s_solve, s_near, s_far;
-  static cudaEvent_t ev_in, ev_s, ev_u, ev_f[NFAR_EV];
-  if (!configured) {
-    // priorities: the critical-path tile solves first, then the near band, the far batches last
-    int prio_lo = 0, prio_hi = 0;
-    SR_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-    SR_CUDA_CHECK(cudaStreamCreateWithPriority(&s_solve, cudaStreamNonBlocking, prio_hi));
-    SR_CUDA_CHECK(cudaStreamCreateWithPriority(&s_near, cudaStreamNonBlocking, prio_hi + (prio_lo > prio_hi ? 1 : 0)));
-    SR_CUDA_CHECK(cudaStreamCreateWithPriority(&s_far, cudaStreamNonBlocking, prio_lo));
-    SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
-    SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_s, cudaEventDisableTiming));
-    SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_u, cudaEventDisableTiming));
-    for (int i = 0; i < NFAR_EV; ++i) SR_CUDA_CHECK(cudaEventCreateWithFlags(&ev_f[i], cudaEventDisableTiming));
-    configured = true;
-  }
-  static bool attr_set = false;  // per template instance
-  if (!attr_set) {
-    SR_CUDA_CHECK(cudaFuncSetAttribute(ksolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_solve));
-    SR_CUDA_CHECK(cudaFuncSetAttribute(knear, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_near));
-    SR_CUDA_CHECK(cudaFuncSetAttribute(kfc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_far_col));
-    SR_CUDA_CHECK(cudaFuncSetAttribute(kfr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_far_row));
-    attr_set = true;
-  }
-  SR_CUDA_CHECK(cudaEventRecord(ev_in, st));
-  SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, ev_in, 0));
-  SR_CUDA_CHECK(cudaStreamWaitEvent(s_near, ev_in, 0));
-  SR_CUDA_CHECK(cudaStreamWaitEvent(s_far, ev_in, 0));
+  cudaStream_t s_solve = c.s_solve, s_near = c.s_near, s_far = c.s_far;
+  SR_CUDA_CHECK(cudaEventRecord(c.ev_in, origin));
+  if (s_solve != origin) SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, c.ev_in, 0));
+  SR_CUDA_CHECK(cudaStreamWaitEvent(s_near, c.ev_in, 0));
+  SR_CUDA_CHECK(cudaStreamWaitEvent(s_far, c.ev_in, 0));
   const typename Real<C>::T cl = (typename Real<C>::T)clip;
   for (int lev = 0; lev < N; ++lev) {
-    // SOLVE(lev): after NEAR(lev-1) (stream order + ev_u) and FAR(lev/4 - 2)
-    if (lev >= 1) SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, ev_u, 0));
+    // SOLVE(lev): after NEAR(lev-1) (ev_u) and FAR(lev/4 - 1 - FAR_LA)
+    if (lev >= 1) SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, c.ev_u, 0));
     if (lev % BW == 0 && lev >= BW * (1 + FAR_LA))
-      SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, ev_f[(lev / BW - 1 - FAR_LA) % NFAR_EV], 0));
+      SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, c.ev_f[(lev / BW - 1 - FAR_LA) % NFAR_EV], 0));
     SweepArgs a{n, N, lev, 0, ld};
-    ksolve<<<lev + 1, NT, smem_solve, s_solve>>>(a, t, Rn, Rf, l, cl, d_clipped);
+    solve_kernel<C><<<lev + 1, NT, smem_solve, s_solve>>>(a, t, Rn, Rf, l, cl, d_clipped);
     SR_LAUNCH_CHECK();
-    // NEAR(lev): sources of level lev-1 into levels lev+1 .. 4b+7, b = (lev-1)/4
+    // NEAR(lev): sources of level lev-1 into levels lev+1 .. 4 (b + 1 + FAR_LA) - 1, b = (lev-1)/4
     if (lev >= 1) {
-      SR_CUDA_CHECK(cudaStreamWaitEvent(s_near, ev_s, 0));  // SOLVE(lev-1)
+      SR_CUDA_CHECK(cudaStreamWaitEvent(s_near, c.ev_s, 0));  // SOLVE(lev-1)
       const int b = (lev - 1) / BW;
       const int lmax = min(N - 1, BW * (b + 1 + FAR_LA) - 1);
       if (lmax >= lev + 1) {
         a.lmax = lmax;
         dim3 grid(lmax + 1, lmax - lev);
-        knear<<<grid, NT, smem_near, s_near>>>(a, t, Rn, l);
+        near_kernel<C><<<grid, NT, smem_near, s_near>>>(a, t, Rn, l);
         SR_LAUNCH_CHECK();
       }
     }
-    SR_CUDA_CHECK(cudaEventRecord(ev_s, s_solve));
-    SR_CUDA_CHECK(cudaEventRecord(ev_u, s_near));
-    // FAR(b) once the last level of batch b is solved, if any tile sits on level >= 4b+8
+    SR_CUDA_CHECK(cudaEventRecord(c.ev_s, s_solve));
+    SR_CUDA_CHECK(cudaEventRecord(c.ev_u, s_near));
+    // FAR(b) once the last level of batch b is solved, if any tile sits on a far target level
 #ifndef SR_DIAG_NO_FAR  // timing diagnostic only (tools/solve_bench.py): wrong results without it
     if (lev % BW == BW - 1) {
 #else
@@ -636,7 +650,7 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
       const int first_level = BW * (b + 1 + FAR_LA);  // first far target level
       const int h = N - first_level;
       if (h >= 1) {
-        SR_CUDA_CHECK(cudaStreamWaitEvent(s_far, ev_s, 0));
+        SR_CUDA_CHECK(cudaStreamWaitEvent(s_far, c.ev_s, 0));
         bool done = false;
         if constexpr (kC64) {
           if (use_tc) {
@@ -649,18 +663,81 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
           FarArgs fa{n, N, b, h, 0, first_level, ld};
           const int strips = (h + BW - 1) / BW;
           fa.first = 0;
-          kfc<<<dim3(strips, min(BW * b + BW, N)), FT, smem_far_col, s_far>>>(fa, t, l, Rf);
+          far_kernel<C, false, FAR_STAGES>
+              <<<dim3(strips, min(BW * b + BW, N)), FT, smem_far_col, s_far>>>(fa, t, l, Rf);
           SR_LAUNCH_CHECK();
           fa.first = N - BW - BW * b;
-          kfr<<<dim3(strips, N - fa.first), FT, smem_far_row, s_far>>>(fa, t, l, Rf);
+          far_kernel<C, true, FAR_STAGES><<<dim3(strips, N - fa.first), FT, smem_far_row, s_far>>>(fa, t, l, Rf);
           SR_LAUNCH_CHECK();
         }
-        SR_CUDA_CHECK(cudaEventRecord(ev_f[b % NFAR_EV], s_far));
+        SR_CUDA_CHECK(cudaEventRecord(c.ev_f[b % NFAR_EV], s_far));
       }
     }
   }
-  SR_CUDA_CHECK(cudaEventRecord(ev_s, s_solve));
-  SR_CUDA_CHECK(cudaStreamWaitEvent(st, ev_s, 0));
+  // join: the near and far streams (already upstream of the last SOLVE, joined
+  // explicitly so a capture sees no dangling work), then the solve stream
+  SR_CUDA_CHECK(cudaEventRecord(c.ev_j, s_far));
+  SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, c.ev_j, 0));
+  SR_CUDA_CHECK(cudaEventRecord(c.ev_j, s_near));
+  SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, c.ev_j, 0));
+  if (s_solve != origin) {
+    SR_CUDA_CHECK(cudaEventRecord(c.ev_s, s_solve));
+    SR_CUDA_CHECK(cudaStreamWaitEvent(origin, c.ev_s, 0));
+  }
+  return SR_OK;
+}
+
+template <typename C>
+int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsigned long long* d_clipped,
+          int* d_flags, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (n < 0 || ld < n) return SR_EINVAL;
+  if (n == 0) return SR_OK;
+  const size_t need = sr_trisolve_workspace_bytes(n, sizeof(C) == 8 ? 1 : 0);
+  const size_t rb = r_bytes(n, ld, sizeof(C));
+  if (ws_bytes < need || !ws || 2 * rb + (sizeof(C) == 8 ? far_tc_forms_bytes(n) : 0) > need) return SR_EINVAL;
+  static SolveCtx c;  // one per lp type
+  if (ctx_init<C>(c) != SR_OK) return SR_ECUDA;
+  const bool same = c.n == n && c.t == t && c.e == e && c.l == l && c.ld == ld && c.clip == clip &&
+                    c.clipped == d_clipped && c.flags == d_flags && c.ws == ws && c.ws_bytes == ws_bytes;
+  if (!same) {
+    if (c.exec) cudaGraphExecDestroy(c.exec);
+    c.exec = nullptr;
+    c.n = n, c.t = t, c.e = e, c.l = l, c.ld = ld, c.clip = clip, c.clipped = d_clipped, c.flags = d_flags;
+    c.ws = ws, c.ws_bytes = ws_bytes, c.calls = 0;
+  }
+  // The first call with new arguments runs eagerly; the second records the
+  // launch sequence into a CUDA graph, later calls replay it (SR_SOLVE_NO_GRAPH=1: always eager).
+  const bool graphs = !getenv("SR_SOLVE_NO_GRAPH");
+  if (!graphs || (!c.exec && c.calls == 0)) {
+    ++c.calls;
+    return enqueue<C>(c, n, t, e, ld, l, clip, d_clipped, d_flags, ws, st);
+  }
+  SR_CUDA_CHECK(cudaEventRecord(c.ev_in, st));
+  SR_CUDA_CHECK(cudaStreamWaitEvent(c.s_solve, c.ev_in, 0));
+  if (!c.exec) {
+    const unsigned long long k0 = sr_kernel_launches();
+    SR_CUDA_CHECK(cudaStreamBeginCapture(c.s_solve, cudaStreamCaptureModeThreadLocal));
+    const int rc = enqueue<C>(c, n, t, e, ld, l, clip, d_clipped, d_flags, ws, c.s_solve);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(c.s_solve, &g);
+    if (rc != SR_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ce != cudaSuccess) return sr_set_cuda_error(ce, "cudaStreamEndCapture(trisolve)");
+    const cudaError_t ie = cudaGraphInstantiate(&c.exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {
+      c.exec = nullptr;
+      return sr_set_cuda_error(ie, "cudaGraphInstantiate(trisolve)");
+    }
+    c.kernels = sr_kernel_launches() - k0;  // counted at capture; replayed by the launch below
+  } else {
+    sr_count_launches(c.kernels);
+  }
+  SR_CUDA_CHECK(cudaGraphLaunch(c.exec, c.s_solve));
+  SR_CUDA_CHECK(cudaEventRecord(c.ev_s, c.s_solve));
+  SR_CUDA_CHECK(cudaStreamWaitEvent(st, c.ev_s, 0));
   return SR_OK;
 }
 

@@ -100,7 +100,8 @@ int sr_skew_c64(int n, const void* l, long long ld, void* w, double* d_norm_w, i
 /* Sigma of the merged Newton-Schulz update (merged_update,
    orthogonal.py:191-201), planar FP64, summed left to right:
    S = ((((2I + 2W) - Y) - YW) + W^2) + W^3 [+ W^2 Y + W^2 Y W].
-   w, yw, w2, w3 (and optional w2y, w2yw, NULL to skip) are complex64.
+   w, yw, w2, w3 (and optional w2y, w2yw, NULL to skip) are complex64;
+   w2 = w3 = NULL: yw holds the fused product YW - W^2 - W^3.
    with_identity = 0 drops the 2I term (S' = S - 2I, used by the Ozaki path,
    which forms Q S / 2 = Q + Q S' / 2 exactly).  n rows x cols columns (a
    column block of S' in the sharded driver; cols == n with the identity). */
@@ -108,6 +109,13 @@ int sr_sigma_merged_f64(int n, int cols, const void* w, const double* y_re, cons
                         const void* yw, const void* w2, const void* w3, const void* w2y, const void* w2yw,
                         long long ld_lp, double* s_re, double* s_im, long long lds, int with_identity,
                         void* stream);
+
+/* X = Y - W - W^2 (complex64 out; Y planar FP64, W and W^2 complex64): the A
+   operand of the fused lp product X W = YW - W^2 - W^3, passed as `yw` to
+   sr_sigma_merged_f64 with w2 = w3 = NULL (merged_update, orthogonal.py:191-195,
+   with two lp products instead of three). */
+int sr_fused_lp_operand_c64(int n, const double* y_re, const double* y_im, long long ldy, const void* w,
+                            const void* w2, long long ld_lp, void* x, void* stream);
 
 /* Sigma of the entry Newton-Schulz step: S = 3I - G (orthogonal.py:167-168). */
 int sr_sigma_ns_f64(int n, const double* g_re, const double* g_im, long long ldg, double* s_re, double* s_im,

@@ -38,6 +38,7 @@ SIGNATURES = {
     "sr_trisolve_c128": (_i, [_i, _p, _p, _ll, _p, _d, _p, _p, _p, _sz, _p]),
     "sr_skew_c64": (_i, [_i, _p, _ll, _p, _p, _p, _p, _sz, _p]),
     "sr_sigma_merged_f64": (_i, [_i, _i, _p, _p, _p, _ll, _p, _p, _p, _p, _p, _ll, _p, _p, _ll, _i, _p]),
+    "sr_fused_lp_operand_c64": (_i, [_i, _p, _p, _ll, _p, _p, _ll, _p, _p]),
     "sr_sigma_ns_f64": (_i, [_i, _p, _p, _ll, _p, _p, _ll, _p]),
     "sr_triu_inplace_f64": (_i, [_i, _p, _p, _ll, _p]),
     "sr_reduce_workspace_bytes": (_sz, []),

@@ -138,13 +138,16 @@ __global__ void sigma_merged_kernel(int rows, int n, const float2* __restrict__ 
     double im = 2.0 * (double)wv.y;
     re = re - yr[(size_t)i * ldy + j];
     im = im - yi[(size_t)i * ldy + j];
-    float2 a = yw[o], b = w2[o], c = w3[o];
+    float2 a = yw[o];
     re = re - (double)a.x;
     im = im - (double)a.y;
-    re = re + (double)b.x;
-    im = im + (double)b.y;
-    re = re + (double)c.x;
-    im = im + (double)c.y;
+    if (w2) {  // null w2 / w3: the fused form, yw already holds YW - W^2 - W^3
+      float2 b = w2[o], c = w3[o];
+      re = re + (double)b.x;
+      im = im + (double)b.y;
+      re = re + (double)c.x;
+      im = im + (double)c.y;
+    }
     if (w2y) {  // restore_full_sigma (orthogonal.py:196-200)
       float2 d = w2y[o], e = w2yw[o];
       re = re + (double)d.x;
@@ -343,11 +346,37 @@ extern "C" int sr_skew_c64(int n, const void* l, long long ld, void* w, double* 
   return SR_OK;
 }
 
+// X = Y - W - W^2 in complex64: the A operand of the fused lp product
+// X W = YW - W^2 - W^3 (one product instead of YW, W^3)
+__global__ void fused_lp_operand_kernel(int n, const double* __restrict__ yr, const double* __restrict__ yi,
+                                        long long ldy, const float2* __restrict__ w, const float2* __restrict__ w2,
+                                        long long ldl, float2* __restrict__ x) {
+  const long long total = (long long)n * n;
+  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    const size_t o = (size_t)i * ldl + j, oy = (size_t)i * ldy + j;
+    const float2 a = w[o], b = w2[o];
+    x[o] = make_float2((float)(yr[oy] - (double)a.x - (double)b.x), (float)(yi[oy] - (double)a.y - (double)b.y));
+  }
+}
+
+extern "C" int sr_fused_lp_operand_c64(int n, const double* y_re, const double* y_im, long long ldy, const void* w,
+                                       const void* w2, long long ld_lp, void* x, void* stream) {
+  if (n < 0 || !y_re || !y_im || !w || !w2 || !x) return SR_EINVAL;
+  if (n == 0) return SR_OK;
+  fused_lp_operand_kernel<<<ew_grid((long long)n * n), RT, 0, (cudaStream_t)stream>>>(
+      n, y_re, y_im, ldy, (const float2*)w, (const float2*)w2, ld_lp, (float2*)x);
+  SR_LAUNCH_CHECK();
+  return SR_OK;
+}
+
 extern "C" int sr_sigma_merged_f64(int n, int cols, const void* w, const double* y_re, const double* y_im,
                                    long long ldy, const void* yw, const void* w2, const void* w3, const void* w2y,
                                    const void* w2yw, long long ld_lp, double* s_re, double* s_im, long long lds,
                                    int with_identity, void* stream) {
-  if (n < 0 || cols < 0 || (w2y == nullptr) != (w2yw == nullptr)) return SR_EINVAL;
+  if (n < 0 || cols < 0 || (w2y == nullptr) != (w2yw == nullptr) || (w2 == nullptr) != (w3 == nullptr))
+    return SR_EINVAL;
+  if (!w2 && w2y) return SR_EINVAL;  // the fused form has no restore_full_sigma terms
   if (with_identity && cols != n) return SR_EINVAL;
   if ((long long)n * cols == 0) return SR_OK;
   sigma_merged_kernel<<<ew_grid((long long)n * cols), RT, 0, (cudaStream_t)stream>>>(

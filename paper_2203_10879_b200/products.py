@@ -3,7 +3,9 @@
 Every product the loop needs (refine.py:259,265 and orthogonal.py:167-201):
   entry    Q = (Q^ (3I - Q^H Q^)) / 2                    (2 hp products)
   measure  P = Q^H A, T^ = P Q, Y = Q^H Q - I            (3 hp products)
-  update   YW, W^2, W^3 (lp), Sigma (hp sum), Q S / 2    (3 lp + 1 hp product)
+  update   YW, W^2, W^3 (lp), Sigma (hp sum), Q S / 2    (3 lp + 1 hp product;
+           the Ozaki path forms W^2 and X W = YW - W^2 - W^3, X = Y - W - W^2:
+           two lp products, the first Hermitian)
 
 OzakiProducts (default) runs them as Ozaki-II emulated products on the int8
 tensor cores (ozaki.py, csrc/oz_gemm.cu): exact integer products, so the
@@ -24,13 +26,16 @@ def _stream():
     return torch.cuda.current_stream().cuda_stream
 
 
-def _sigma(ws, restore_full_sigma, with_identity):
+def _sigma(ws, restore_full_sigma, with_identity, fused=False):
+    """S (or S' = S - 2I) from W, Y and the lp products; fused: ws.yw holds
+    X W = YW - W^2 - W^3 (X = Y - W - W^2) and W^2, W^3 are not separate."""
     n = ws.n
     w2y = w2yw = None
     if restore_full_sigma:
         w2y, w2yw = ws.w2y.data_ptr(), ws.w2yw.data_ptr()
+    w2, w3 = (None, None) if fused else (ws.w2.data_ptr(), ws.w3.data_ptr())
     _lib.call("sr_sigma_merged_f64", n, n, ws.w_lp.data_ptr(), ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld,
-              ws.yw.data_ptr(), ws.w2.data_ptr(), ws.w3.data_ptr(), w2y, w2yw, ws.w_lp.shape[1],
+              ws.yw.data_ptr(), w2, w3, w2y, w2yw, ws.w_lp.shape[1],
               ws.sigma.re_ptr(), ws.sigma.im_ptr(), ws.sigma.ld, 1 if with_identity else 0, _stream())
 
 
@@ -143,22 +148,29 @@ class OzakiProducts:
 
     def update(self, restore_full_sigma, sigma_bound=None):
         ws, hp, lp, n = self.ws, self.hp, self.lp, self.ws.n
-        _downcast_y(ws)
         ozaki.encode(ws.w_lp, n, n, "b", lp, out=self.lb)                # W, B role (all lp products)
-        ozaki.encode(ws.y_lp, n, n, "a", lp, out=self.la)
-        self._lp(self.la, self.lb, ws.yw)                                # Y W
         ozaki.encode(ws.w_lp, n, n, "a", lp, out=self.la)
         self._lp(self.la, self.lb, ws.w2, hermitian=True)                # W^2 (W skew-Hermitian)
-        ozaki.encode(ws.w2, n, n, "a", lp, out=self.la)
-        self._lp(self.la, self.lb, ws.w3, hermitian="skew")              # W^3
-        if restore_full_sigma:
+        if not restore_full_sigma:
+            # two lp products instead of three: X W = YW - W^2 - W^3 with X = Y - W - W^2
+            _lib.call("sr_fused_lp_operand_c64", n, ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld, ws.w_lp.data_ptr(),
+                      ws.w2.data_ptr(), ws.w_lp.shape[1], ws.y_lp.data_ptr(), _stream())
+            ozaki.encode(ws.y_lp, n, n, "a", lp, out=self.la)
+            self._lp(self.la, self.lb, ws.yw)                            # X W
+            _sigma(ws, False, False, fused=True)                         # S' = S - 2I
+        else:
+            _downcast_y(ws)
+            ozaki.encode(ws.w2, n, n, "a", lp, out=self.la)
+            self._lp(self.la, self.lb, ws.w3, hermitian="skew")          # W^3
+            ozaki.encode(ws.y_lp, n, n, "a", lp, out=self.la)
+            self._lp(self.la, self.lb, ws.yw)                            # Y W
             ozaki.encode(ws.y_lp, n, n, "b", lp, out=self.lb)
             ozaki.encode(ws.w2, n, n, "a", lp, out=self.la)
             self._lp(self.la, self.lb, ws.w2y)                           # W^2 Y
             ozaki.encode(ws.w_lp, n, n, "b", lp, out=self.lb)
             ozaki.encode(ws.w2y, n, n, "a", lp, out=self.la)
             self._lp(self.la, self.lb, ws.w2yw)                          # W^2 Y W
-        _sigma(ws, restore_full_sigma, False)                             # S' = S - 2I
+            _sigma(ws, True, False)                                      # S' = S - 2I
         pc = hp if sigma_bound is None else self._correction_plan(sigma_bound)
         ozaki.encode(ws.q, n, n, "a", pc, out=self.ea_x)
         ozaki.encode(ws.sigma, n, n, "b", pc, out=self.eb_s)

@@ -75,7 +75,7 @@ def cpu_oracle_sample(steps, n_full):
     a = inputs.gaussian_real(SAMPLE_N, 0)
     q = inputs.cached_qhat("c3_n%d_s0" % SAMPLE_N, a).astype(np.complex128)
     scale = (n_full / SAMPLE_N) ** 3
-    vals = []
+    vals, out = [], None
     for _ in range(steps):
         t0 = time.perf_counter()
         out = refine_template_fp64(a, q, tol_factor=10.0 / SAMPLE_N, max_iters=10)
@@ -95,8 +95,9 @@ def run_reference(args):
     if rank != 0:
         return
     n = args.n
-    vals, out = cpu_oracle_sample(args.warmup, n)
-    vals, out = cpu_oracle_sample(args.steps, n)
+    if args.warmup > 0:
+        cpu_oracle_sample(args.warmup, n)
+    vals, out = cpu_oracle_sample(max(args.steps, 1), n)
     v = float(np.median(vals))
     sample = ("oracle port (oracle/refine_fp64.py: numpy/OpenBLAS hp, C restatement of trisolve.py lp) "
               "full refine at n=%d on the config-3 workload family, %d iterations, scaled by (n/%d)^3"

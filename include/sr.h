@@ -178,6 +178,15 @@ int sr_oz_encode(int rows_out, int K, int kind, const void* re, const double* im
                  const double* im_lo, long long ld, int transposed, int conj, int layout, const int* exps, int beta,
                  int nmod, const int* moduli, void* out, long long kpitch, void* stream);
 
+/* Both operand roles of one matrix X (rows_out = columns of X, K = rows of X,
+   scaled per column of X by exps): the A operand of X^H, layout 0 of the
+   conjugate (re, -im), into out_ah and the B operand of X, layout 1, into out_b
+   — one residue computation for the Q^H / Q pair of every measurement
+   (refine.py:259,265).  Same kpitch for both. */
+int sr_oz_encode_dual(int rows_out, int K, int kind, const void* re, const double* im, const double* re_lo,
+                      const double* im_lo, long long ld, const int* exps, int beta, int nmod, const int* moduli,
+                      void* out_ah, void* out_b, long long kpitch, void* stream);
+
 /* R_l = A_l B_l^T mod p_l on tcgen05 (kind::i8), out [nmod][2][M][out_pitch]
    int8 (re, im).  a_planes = 2; b_planes = 3 (complex B) or 1 (real B).
    moduli is a host array; num_sms <= 0 means 148.  lower_only (M == N):

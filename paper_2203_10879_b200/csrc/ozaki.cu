@@ -126,10 +126,14 @@ __global__ void exps_transposed_kernel(int rows, int cols, Src s, long long ld, 
 }
 
 // ---- encode: residue planes [nmod][planes][rows_out][kpitch] -------------------
-// layout 0: A operand (re, im);  1: B operand (-im, re, im);  2: B operand (re)
+// layout 0: A operand (re, im);  1: B operand (-im, re, im);  2: B operand (re);
+// 3: both roles of one matrix X read column-wise (transposed): the A operand
+//    of X^H (re, -im) into out and the B operand of X (-im, re, im) into out2,
+//    sharing the residue computation (Q^H and Q of every measurement)
 struct EncodeParams {
   int rows_out, K, transposed, conj, layout, beta, nmod, ndig;
   long long ld, kpitch;
+  int8_t* out2;
   float pf[MAXMOD], invf[MAXMOD], hif[MAXMOD], lof[MAXMOD];
   float pow2[MAXMOD][MAXDIG];  // 2^(11 c) mod p, symmetric
 };
@@ -183,9 +187,10 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
     }
   }
   __syncthreads();
-  const int planes = p.layout == 0 ? 2 : (p.layout == 1 ? 3 : 1);
+  const int planes = p.layout == 0 || p.layout == 3 ? 2 : (p.layout == 1 ? 3 : 1);
   const long long plane_stride = (long long)p.rows_out * p.kpitch;
   const long long mod_stride = plane_stride * planes;
+  const long long mod_stride2 = plane_stride * 3;  // layout 3: out2 holds the 3 B planes
   // each thread: one output row i, 4 consecutive k -> one 32-bit word per (modulus, plane)
   for (int g = tid; g < ETI * (ETK / 4); g += 256) {
     const int il = g / (ETK / 4), kl = (g % (ETK / 4)) * 4;
@@ -249,6 +254,13 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
         *reinterpret_cast<uint32_t*>(dm) = wn;
         *reinterpret_cast<uint32_t*>(dm + plane_stride) = wr;
         *reinterpret_cast<uint32_t*>(dm + 2 * plane_stride) = wi;
+      } else if (p.layout == 3) {
+        *reinterpret_cast<uint32_t*>(dm) = wr;  // A operand of X^H: (re, -im)
+        *reinterpret_cast<uint32_t*>(dm + plane_stride) = wn;
+        int8_t* d2 = p.out2 + (size_t)l * mod_stride2 + (size_t)i * p.kpitch + k;  // B operand of X
+        *reinterpret_cast<uint32_t*>(d2) = wn;
+        *reinterpret_cast<uint32_t*>(d2 + plane_stride) = wr;
+        *reinterpret_cast<uint32_t*>(d2 + 2 * plane_stride) = wi;
       } else {
         *reinterpret_cast<uint32_t*>(dm) = wr;
       }
@@ -512,11 +524,11 @@ extern "C" int sr_oz_exponents(int rows, int cols, int kind, const void* re, con
   return SR_OK;
 }
 
-extern "C" int sr_oz_encode(int rows_out, int K, int kind, const void* re, const double* im, const double* re_lo,
-                            const double* im_lo, long long ld, int transposed, int conj, int layout,
-                            const int* exps, int beta, int nmod, const int* moduli, void* out, long long kpitch,
-                            void* stream) {
-  if (rows_out <= 0 || K <= 0 || nmod <= 0 || nmod > MAXMOD || layout < 0 || layout > 2) return SR_EINVAL;
+namespace {
+int encode_launch(int rows_out, int K, int kind, const void* re, const double* im, const double* re_lo,
+                  const double* im_lo, long long ld, int transposed, int conj, int layout, const int* exps, int beta,
+                  int nmod, const int* moduli, void* out, void* out2, long long kpitch, cudaStream_t st) {
+  if (rows_out <= 0 || K <= 0 || nmod <= 0 || nmod > MAXMOD || layout < 0 || layout > 3) return SR_EINVAL;
   if (kind < 0 || kind > SR_MAT_DD || (kind == SR_MAT_DD && (!re_lo || !im_lo || !im))) return SR_EINVAL;
   const int max_beta = kind == SR_MAT_DD ? 106 : 61;
   if (beta < 1 || beta > max_beta || (kpitch & 15) || kpitch < K) return SR_EINVAL;
@@ -531,6 +543,7 @@ extern "C" int sr_oz_encode(int rows_out, int K, int kind, const void* re, const
   p.nmod = nmod;
   p.ld = ld;
   p.kpitch = kpitch;
+  p.out2 = (int8_t*)out2;
   p.ndig = (beta + 2 + 10) / 11;  // digits covering |a| <= 2^beta plus a carry
   if (p.ndig > MAXDIG) p.ndig = MAXDIG;
   for (int l = 0; l < nmod; ++l) {
@@ -549,9 +562,11 @@ extern "C" int sr_oz_encode(int rows_out, int K, int kind, const void* re, const
     }
   }
   // K padding columns of the residue planes must read as zero
-  const int planes = layout == 0 ? 2 : (layout == 1 ? 3 : 1);
-  cudaStream_t st = (cudaStream_t)stream;
-  if (kpitch > K) SR_CUDA_CHECK(cudaMemsetAsync(out, 0, (size_t)nmod * planes * rows_out * kpitch, st));
+  const int planes = layout == 0 || layout == 3 ? 2 : (layout == 1 ? 3 : 1);
+  if (kpitch > K) {
+    SR_CUDA_CHECK(cudaMemsetAsync(out, 0, (size_t)nmod * planes * rows_out * kpitch, st));
+    if (out2) SR_CUDA_CHECK(cudaMemsetAsync(out2, 0, (size_t)nmod * 3 * rows_out * kpitch, st));
+  }
   Src s{(const double*)re, im, re_lo, im_lo, kind};
   const int eti = kind == SR_MAT_DD ? 32 : 64;
   dim3 grid(sr_ceil_div(K, 32), sr_ceil_div(rows_out, eti));
@@ -570,6 +585,25 @@ extern "C" int sr_oz_encode(int rows_out, int K, int kind, const void* re, const
   }
   SR_LAUNCH_CHECK();
   return SR_OK;
+}
+}  // namespace
+
+extern "C" int sr_oz_encode(int rows_out, int K, int kind, const void* re, const double* im, const double* re_lo,
+                            const double* im_lo, long long ld, int transposed, int conj, int layout,
+                            const int* exps, int beta, int nmod, const int* moduli, void* out, long long kpitch,
+                            void* stream) {
+  if (layout > 2) return SR_EINVAL;
+  return encode_launch(rows_out, K, kind, re, im, re_lo, im_lo, ld, transposed, conj, layout, exps, beta, nmod,
+                       moduli, out, nullptr, kpitch, (cudaStream_t)stream);
+}
+
+extern "C" int sr_oz_encode_dual(int rows_out, int K, int kind, const void* re, const double* im,
+                                 const double* re_lo, const double* im_lo, long long ld, const int* exps, int beta,
+                                 int nmod, const int* moduli, void* out_ah, void* out_b, long long kpitch,
+                                 void* stream) {
+  if (!out_ah || !out_b) return SR_EINVAL;
+  return encode_launch(rows_out, K, kind, re, im, re_lo, im_lo, ld, 1, 0, 3, exps, beta, nmod, moduli, out_ah,
+                       out_b, kpitch, (cudaStream_t)stream);
 }
 
 // table (host): [nmod][6] CRT weights, [6] modulus-product chunks, [6] chunk

@@ -166,6 +166,28 @@ def correction_beta(bound, n, hi=HP_BETA, lo=LP_BETA, unit_bits=53):
     return max(lo, min(hi, b))
 
 
+def encode_dual(x, rows, cols, pl, out_ah, out_b):
+    """encode(x, .., "a", conj_t=True, out=out_ah) and encode(x, .., "b", out=out_b)
+    in one pass (sr_oz_encode_dual): both are scaled per column of x, so the
+    residues are computed once and written in both layouts."""
+    kind, re, im, re_lo, im_lo, ld, dev = mat_args(x)
+    if kind == _lib.SR_MAT_F64 and im is None:
+        raise ValueError("encode_dual needs a complex operand")
+    for enc, planes in ((out_ah, 2), (out_b, 3)):
+        if enc.cap < pl.nmod or enc.rows != cols or enc.K != rows or enc.planes != planes:
+            raise ValueError("encoding buffer does not fit this operand / plan")
+    out_ah.beta, out_ah.nmod = pl.beta_a, pl.nmod
+    out_b.beta, out_b.nmod = pl.beta_b, pl.nmod
+    if pl.beta_a != pl.beta_b or out_ah.kp != out_b.kp:
+        raise ValueError("encode_dual needs beta_a == beta_b")
+    st = _stream()
+    _lib.call("sr_oz_exponents", rows, cols, kind, re, im, ld, 1, out_ah.exps.data_ptr(), st)
+    out_b.exps.copy_(out_ah.exps)
+    _lib.call("sr_oz_encode_dual", cols, rows, kind, re, im, re_lo, im_lo, ld, out_ah.exps.data_ptr(), pl.beta_a,
+              pl.nmod, pl.moduli_ptr(), out_ah.buf.data_ptr(), out_b.buf.data_ptr(), out_ah.kp, st)
+    return out_ah, out_b
+
+
 class ResidueBuffer:
     def __init__(self, M, N, nmod, device):
         self.M, self.N, self.nmod = M, N, nmod

@@ -129,8 +129,7 @@ class OzakiProducts:
     def entry(self, qhat):
         """Q = Q^ (3I - G) / 2 = Q^ - Q^ (G - I) / 2 (orthogonal.py:167-169)."""
         ws, hp, n = self.ws, self.hp, self.ws.n
-        ozaki.encode(qhat, n, n, "a", hp, conj_t=True, out=self.ea_qh)
-        ozaki.encode(qhat, n, n, "b", hp, out=self.eb_q)
+        ozaki.encode_dual(qhat, n, n, hp, self.ea_qh, self.eb_q)        # Q^H (A role), Q^ (B role)
         self._hp(self.ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True)  # G - I
         pc = self._correction_plan(ws.fro_norm(ws.y))
         ozaki.encode(qhat, n, n, "a", pc, out=self.ea_x)
@@ -139,8 +138,7 @@ class OzakiProducts:
 
     def measure(self, a):
         ws, hp, n = self.ws, self.hp, self.ws.n
-        ozaki.encode(ws.q, n, n, "a", hp, conj_t=True, out=self.ea_qh)
-        ozaki.encode(ws.q, n, n, "b", hp, out=self.eb_q)
+        ozaki.encode_dual(ws.q, n, n, hp, self.ea_qh, self.eb_q)          # Q^H (A role), Q (B role)
         self._hp(self.ea_qh, self.eb_a, ws.p)                            # P = Q^H A
         ozaki.encode(ws.p, n, n, "a", hp, out=self.ea_x)
         self._hp(self.ea_x, self.eb_q, ws.that)                          # T^ = P Q

@@ -176,3 +176,21 @@ def test_oz_lp_structured_products(dtype, beta, n):
         up[i, (i // 128 + 1) * 128:] = True
     assert np.array_equal(g2[up], g2.conj().T[up])
     assert np.array_equal(g3[up], -g3.conj().T[up])
+
+
+def test_oz_encode_dual_matches_two_encodes():
+    """sr_oz_encode_dual writes exactly the residues (and exponents) of the two
+    separate encodes of Q^H (A role) and Q (B role)."""
+    rng = np.random.default_rng(5)
+    n = 300
+    q = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    q[:, 7] *= 1e-9  # a small column: its own exponent
+    qd = ZPlanar.from_any(q)
+    pl = ozaki.plan(n, ozaki.HP_BETA, ozaki.HP_BETA)
+    ea = ozaki.encode(qd, n, n, "a", pl, conj_t=True)
+    eb = ozaki.encode(qd, n, n, "b", pl)
+    da = ozaki.Encoded(n, n, 2, pl.beta_a, pl.nmod, "cuda")
+    db = ozaki.Encoded(n, n, 3, pl.beta_b, pl.nmod, "cuda")
+    ozaki.encode_dual(qd, n, n, pl, da, db)
+    assert torch.equal(ea.buf, da.buf) and torch.equal(eb.buf, db.buf)
+    assert torch.equal(ea.exps, da.exps) and torch.equal(eb.exps, db.exps)

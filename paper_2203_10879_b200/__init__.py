@@ -13,6 +13,7 @@ from .refine import (
     RefineStatus,
     SchurPair,
     refine_template,
+    VerifyResiduals,
     verify_pair,
 )
 from .trisolve import TriEqProblem, TriEqSolution, solve_block
@@ -23,6 +24,6 @@ __version__ = "0.1.0"
 __all__ = [
     "NonFiniteError", "NormTooLarge", "NotSymmetric", "SeparationError", "counters", "matmul_hp",
     "matmul_lp", "reset_counters", "ZPlanar", "U_FP64", "U_HP", "OrthoStrategy", "RefineConfig",
-    "RefineReport", "RefineStatus", "SchurPair", "refine_template", "verify_pair", "TriEqProblem",
+    "RefineReport", "RefineStatus", "SchurPair", "refine_template", "verify_pair", "VerifyResiduals", "TriEqProblem",
     "TriEqSolution", "solve_block", "refine_continuation", "DDPlanar",
 ]

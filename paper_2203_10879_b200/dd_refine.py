@@ -87,8 +87,7 @@ class DDProducts:
     def entry(self, qhat):
         """Q = Q^ (3I - G) / 2 = Q^ - Q^ (G - I) / 2 in dd (orthogonal.py:167-169)."""
         ws, hp, n = self.ws, self.hp, self.ws.n
-        ozaki.encode(qhat, n, n, "a", hp, conj_t=True, out=self.ea_qh)
-        ozaki.encode(qhat, n, n, "b", hp, out=self.eb_q)
+        ozaki.encode_dual(qhat, n, n, hp, self.ea_qh, self.eb_q)
         self._hp(self.ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True)
         ozaki.encode(qhat, n, n, "a", hp, out=self.ea_x)
         ozaki.encode(ws.y, n, n, "b", hp, out=self.eb_s)
@@ -119,8 +118,7 @@ class DDProducts:
 
     def measure(self):
         ws, hp, n = self.ws, self.hp, self.ws.n
-        ozaki.encode(ws.q, n, n, "a", hp, conj_t=True, out=self.ea_qh)
-        ozaki.encode(ws.q, n, n, "b", hp, out=self.eb_q)
+        ozaki.encode_dual(ws.q, n, n, hp, self.ea_qh, self.eb_q)
         self._hp(self.ea_qh, self.eb_a, ws.p)
         ozaki.encode(ws.p, n, n, "a", hp, out=self.ea_x)
         self._hp(self.ea_x, self.eb_q, ws.that)

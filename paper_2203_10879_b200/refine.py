@@ -20,6 +20,8 @@ import enum
 import math
 import time
 
+from typing import NamedTuple
+
 import numpy as np
 import torch
 
@@ -376,20 +378,79 @@ def refine_template(a, qhat, cfg=None, device=None):
     return pair, report
 
 
-def verify_pair(a, pair, device=None):
-    """verify_pair (refine.py:456-476) in FP64 on the GPU:
-    (||Q^H Q - I||_F, ||stril(Q^H A Q)||_F, ||T - Q^H A Q||_F)."""
+VERIFY_DD_BETA = 106  # every dd entry within 2^-0 of its row maximum keeps 106 bits (30 moduli)
+
+
+class VerifyResiduals(NamedTuple):
+    """refine.py:105-108."""
+
+    ortho_residual: float
+    tri_residual: float
+    similarity_residual: float
+
+
+def verify_pair(a, pair, device=None, precision="dd"):
+    """verify_pair (refine.py:456-476) on the GPU: the three quality residuals
+    (||Q^H Q - I||_F, ||stril(Q^H A Q)||_F, ||T - Q^H A Q||_F) of a Schur pair,
+    measured from scratch.  precision "dd" (the reference's): the products as
+    Ozaki-II double-double products (beta = 102, dd in and out), T - Q^H A Q
+    subtracted in dd; "fp64": FP64 Ozaki-II products.  a, pair.q, pair.t: any
+    matrix refine_template accepts (numpy, torch, 4-plane dd).  Returns
+    VerifyResiduals (floats)."""
+    from . import dd_refine, ozaki
+    from .matrix import DDPlanar
+    if precision not in ("dd", "fp64"):
+        raise ValueError("precision must be 'dd' or 'fp64'")
     device = torch.device("cuda") if device is None else torch.device(device)
-    a = _coerce(a, device)
-    q = ZPlanar.from_any(pair.q, device=device, force_complex=True)
-    t = ZPlanar.from_any(pair.t, device=device, force_complex=True)
-    n = a.rows
-    g = matmul_hp(q, q, trans_a=True, diag_shift=-1.0)
-    that = matmul_hp(matmul_hp(q, a, trans_a=True), q)
-    gz = g.to_complex()
-    tz = that.to_complex()
-    ortho = float(torch.linalg.matrix_norm(gz))
-    tri = float(torch.linalg.matrix_norm(torch.tril(tz, -1)))
-    sim = float(torch.linalg.matrix_norm(t.to_complex() - tz))
-    del n
-    return ortho, tri, sim
+    if precision == "dd":
+        A = dd_refine.coerce_dd(a, device)
+        Q = dd_refine.coerce_dd(pair.q, device)
+        T = dd_refine.coerce_dd(pair.t, device)
+        n = A.rows
+        if Q.rows != n or T.rows != n:
+            raise ValueError("pair dimensions do not match the matrix")
+        pl = ozaki.plan(n, VERIFY_DD_BETA, VERIFY_DD_BETA)
+        mk = lambda: DDPlanar.empty(n, device=device)  # noqa: E731
+    else:
+        A = _coerce(a, device)
+        Q = ZPlanar.from_any(pair.q, device=device, force_complex=True)
+        T = ZPlanar.from_any(pair.t, device=device, force_complex=True)
+        n = A.rows
+        if Q.rows != n or T.rows != n:
+            raise ValueError("pair dimensions do not match the matrix")
+        pl = ozaki.plan(n, ozaki.HP_BETA, ozaki.HP_BETA)
+        mk = lambda: ZPlanar.empty(n, device=device)  # noqa: E731
+    eqh = ozaki.Encoded(n, n, 2, pl.beta_a, pl.nmod, device)
+    eq = ozaki.Encoded(n, n, 3, pl.beta_b, pl.nmod, device)
+    ozaki.encode_dual(Q, n, n, pl, eqh, eq)
+    res = ozaki.ResidueBuffer(n, n, pl.nmod, device)
+    g = mk()
+    ozaki.gemm_residues(eqh, eq, pl, res, lower_only=True)
+    ozaki.decode(res, eqh, eq, pl, g, shift=-1.0, hermitian=True)        # Q^H Q - I
+    eb_a = ozaki.encode(A, n, n, "b", pl)
+    p = mk()
+    ozaki.gemm_residues(eqh, eb_a, pl, res)
+    ozaki.decode(res, eqh, eb_a, pl, p)                                   # Q^H A
+    ea_p = ozaki.encode(p, n, n, "a", pl)
+    that = mk()
+    ozaki.gemm_residues(ea_p, eq, pl, res)
+    ozaki.decode(res, ea_p, eq, pl, that)                                 # (Q^H A) Q
+
+    def planes(x):  # (re, im) float64 values; dd: hi + lo rounded once
+        if precision == "dd":
+            return x.hi.re + x.lo.re, x.hi.im + x.lo.im
+        return x.re, x.im
+
+    def fro(re, im):
+        return float(torch.sqrt((re * re).sum() + (im * im).sum()))
+
+    gr, gi = planes(g)
+    tr, ti = planes(that)
+    low = torch.tril(torch.ones(n, n, dtype=torch.bool, device=device), -1)
+    if precision == "dd":  # T - T^ in dd: the hi parts cancel exactly (Sterbenz) for a refined pair
+        dr = (T.hi.re - that.hi.re) + (T.lo.re - that.lo.re)
+        di = (T.hi.im - that.hi.im) + (T.lo.im - that.lo.im)
+    else:
+        dr, di = T.re - that.re, T.im - that.im
+    return VerifyResiduals(ortho_residual=fro(gr, gi), tri_residual=fro(tr * low, ti * low),
+                           similarity_residual=fro(dr, di))

@@ -123,3 +123,35 @@ def test_refine_dd_config4_failure_mode_parity(golden):
             ortho, tri = verify_dd((a.real.copy(), np.zeros((n, n)), a.imag.copy(), np.zeros((n, n))),
                                    pair.q.to_numpy_cells())
             assert ortho <= 1e-28 and tri <= 10 * n * U_HP * np.linalg.norm(a)
+
+
+def test_verify_pair_dd_matches_cpu_dd_evaluator(golden):
+    """verify_pair (refine.py:456-476) on the GPU in dd against the CPU dd
+    evaluator built on the bit-exact reference dd GEMM: at the dd noise floor
+    for refined pairs (the reference's acceptance bounds), and to 1e-8
+    relative on a pair perturbed well above it."""
+    from paper_2203_10879_b200 import SchurPair, verify_pair
+    meta, arr = golden("refine_dd_ref")
+    c = meta["cases"][0]
+    k, n = c["k"], c["n"]
+    a, qhat = cells(arr, "a", k), cells(arr, "qhat", k)
+    pair, rep = refine_template(a, qhat, RefineConfig(precision="dd"))
+    v = verify_pair(a, pair)
+    norm_a = np.linalg.norm(a[0] + 1j * a[2])
+    assert v.ortho_residual <= 1e-28 and v.tri_residual <= 10 * n * U_HP * norm_a
+    assert v.similarity_residual <= 10 * n * U_HP * norm_a
+    # perturb Q: residuals ~1e-20, far above both evaluators' floors
+    rng = np.random.default_rng(3)
+    qc = list(pair.q.to_numpy_cells())
+    qc[1] = qc[1] + 1e-20 * rng.standard_normal(qc[1].shape)  # in the lo planes: below an ulp of hi
+    qc[3] = qc[3] + 1e-20 * rng.standard_normal(qc[3].shape)
+    qc = tuple(np.ascontiguousarray(x) for x in qc)
+    v2 = verify_pair(a, SchurPair(q=qc, t=pair.t, ortho_residual=0.0))
+    o_cpu, t_cpu = verify_dd(a, qc)
+    assert abs(v2.ortho_residual - o_cpu) <= 1e-8 * o_cpu, (v2.ortho_residual, o_cpu)
+    assert abs(v2.tri_residual - t_cpu) <= 1e-8 * t_cpu, (v2.tri_residual, t_cpu)
+    # FP64 evaluator (the pair rounded to FP64): residuals at the FP64 floor
+    z = lambda c: (c[0] + c[1]) + 1j * (c[2] + c[3])  # noqa: E731
+    v3 = verify_pair(z(a), SchurPair(q=z(qc), t=z(pair.t.to_numpy_cells()), ortho_residual=0.0), precision="fp64")
+    u64 = 2.0 ** -53
+    assert v3.tri_residual <= 10 * n * u64 * norm_a and v3.ortho_residual <= 10 * n * u64

@@ -91,6 +91,20 @@ int sr_trisolve_c64(int n, const void* t, const void* e, long long ld, void* l, 
 int sr_trisolve_c128(int n, const void* t, const void* e, long long ld, void* l, double clip,
                      unsigned long long* d_clipped, int* d_flags, void* ws, size_t ws_bytes, void* stream);
 
+/* Hermitian variant (refine_symmetric, refine.py:409-438).
+   ||striu(X)||_F of planar FP64 X (with the split's ||stril|| the full
+   off-diagonal defect, refine.py:130-131).  The lp solve collapses to
+   l_ij = -e_ij / (t_ii - t_jj) on the strict lower part
+   (_solve_diagonal_correction, refine.py:138-159): clip <= 0 disables
+   clipping, *d_clipped accumulates, *d_flags gets SR_FLAG_SEPARATION on a
+   zero separation and SR_FLAG_NONFINITE on a non-finite quotient. */
+int sr_striu_norm_f64(int n, const double* re, const double* im, long long ld, double* d_out, void* ws,
+                      size_t ws_bytes, void* stream);
+int sr_diag_correction_c64(int n, const void* t, const void* e, long long ld, void* l, float clip,
+                           unsigned long long* d_clipped, int* d_flags, void* stream);
+int sr_diag_correction_c128(int n, const void* t, const void* e, long long ld, void* l, double clip,
+                            unsigned long long* d_clipped, int* d_flags, void* stream);
+
 /* W = L - L^H (complex64), ||W||_F into *d_norm_w, SR_FLAG_NONFINITE into
    *d_flags when L holds a non-finite entry (refine.py:296-297 and
    _check_finite, trisolve.py:116-118). */

@@ -18,6 +18,7 @@ from .refine import (
 )
 from .trisolve import TriEqProblem, TriEqSolution, solve_block
 from .continuation import refine_continuation
+from .symmetric import order_by_random_line, refine_symmetric
 from .matrix import DDPlanar
 
 __version__ = "0.1.0"
@@ -25,5 +26,6 @@ __all__ = [
     "NonFiniteError", "NormTooLarge", "NotSymmetric", "SeparationError", "counters", "matmul_hp",
     "matmul_lp", "reset_counters", "ZPlanar", "U_FP64", "U_HP", "OrthoStrategy", "RefineConfig",
     "RefineReport", "RefineStatus", "SchurPair", "refine_template", "verify_pair", "VerifyResiduals", "TriEqProblem",
-    "TriEqSolution", "solve_block", "refine_continuation", "DDPlanar",
+    "TriEqSolution", "solve_block", "refine_continuation", "DDPlanar", "refine_symmetric",
+    "order_by_random_line",
 ]

@@ -32,6 +32,9 @@ SIGNATURES = {
     "sr_cgemm_c64": (_i, [_i, _i, _i, _i, _p, _ll, _p, _ll, _p, _ll, _p]),
     "sr_split_lp_c64": (_i, [_i, _p, _p, _ll, _p, _p, _ll, _p, _p, _sz, _p]),
     "sr_fro_norm_f64": (_i, [_i, _i, _p, _p, _ll, _p, _p, _sz, _p]),
+    "sr_striu_norm_f64": (_i, [_i, _p, _p, _ll, _p, _p, _sz, _p]),
+    "sr_diag_correction_c64": (_i, [_i, _p, _p, _ll, _p, _f, _p, _p, _p]),
+    "sr_diag_correction_c128": (_i, [_i, _p, _p, _ll, _p, _d, _p, _p, _p]),
     "sr_downcast_c64": (_i, [_i, _i, _p, _p, _ll, _p, _ll, _p]),
     "sr_trisolve_workspace_bytes": (_sz, [_i, _i]),
     "sr_trisolve_c64": (_i, [_i, _p, _p, _ll, _p, _f, _p, _p, _p, _sz, _p]),

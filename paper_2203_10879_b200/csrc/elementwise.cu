@@ -96,6 +96,62 @@ __global__ void fro_norm_kernel(int m, int n, const double* __restrict__ re, con
   finish_norm(acc, partials, counter, out);
 }
 
+// ||striu(X)||_F (strict upper triangle): with the split kernel's ||stril||
+// it gives the full off-diagonal defect of the Hermitian variant
+// (refine.py:130-131, symmetric=True)
+__global__ void striu_norm_kernel(int n, const double* __restrict__ re, const double* __restrict__ im, long long ld,
+                                  double* partials, unsigned int* counter, double* out) {
+  double acc = 0.0;
+  const long long total = (long long)n * n;
+  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    if (j > i) {
+      const double a = re[(size_t)i * ld + j], b = im ? im[(size_t)i * ld + j] : 0.0;
+      acc += a * a + b * b;
+    }
+  }
+  finish_norm(acc, partials, counter, out);
+}
+
+// Hermitian variant's solve (_solve_diagonal_correction, refine.py:138-159):
+// l_ij = -e_ij / (t_ii - t_jj) on the strict lower part, 0 elsewhere; a zero
+// separation sets SR_FLAG_SEPARATION, |l| > clip is zeroed and counted, a
+// non-finite quotient sets SR_FLAG_NONFINITE.
+template <typename C, typename R>
+__global__ void diag_correction_kernel(int n, const C* __restrict__ t, const C* __restrict__ e, long long ld,
+                                       C* __restrict__ l, R clip, unsigned long long* clipped, int* flags) {
+  unsigned int nclip = 0;
+  bool sep = false, bad = false;
+  const long long total = (long long)n * n;
+  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    C v;
+    v.x = 0;
+    v.y = 0;
+    if (i > j) {
+      const C ti = t[(size_t)i * ld + i], tj = t[(size_t)j * ld + j], ev = e[(size_t)i * ld + j];
+      C d;
+      d.x = ti.x - tj.x;
+      d.y = ti.y - tj.y;
+      if (d.x == 0 && d.y == 0) sep = true;
+      C me;
+      me.x = -ev.x;
+      me.y = -ev.y;
+      v = cdiv(me, d);
+      if (clip > 0 && sqrt(v.x * v.x + v.y * v.y) > clip) {
+        v.x = 0;
+        v.y = 0;
+        ++nclip;
+      }
+      if (!isfinite(v.x) || !isfinite(v.y)) bad = true;
+    }
+    l[(size_t)i * ld + j] = v;
+  }
+  if (sep) atomicOr(flags, SR_FLAG_SEPARATION);
+  if (bad) atomicOr(flags, SR_FLAG_NONFINITE);
+  if (nclip) atomicAdd(clipped, (unsigned long long)nclip);
+}
+
 __global__ void downcast_kernel(int m, int n, const double* __restrict__ re, const double* __restrict__ im,
                                 long long ld, float2* __restrict__ out, long long ldo) {
   const long long total = (long long)m * n;
@@ -322,6 +378,35 @@ extern "C" int sr_fro_norm_f64(int m, int n, const double* re, const double* im,
   if (m < 0 || n < 0 || !ws || ws_bytes < sr_reduce_workspace_bytes()) return SR_EINVAL;
   RedWs r = red_ws(ws);
   fro_norm_kernel<<<RBLOCKS, RT, 0, (cudaStream_t)stream>>>(m, n, re, im, ld, r.partials, r.counter, d_out);
+  SR_LAUNCH_CHECK();
+  return SR_OK;
+}
+
+extern "C" int sr_striu_norm_f64(int n, const double* re, const double* im, long long ld, double* d_out, void* ws,
+                                 size_t ws_bytes, void* stream) {
+  if (n < 0 || !ws || ws_bytes < sr_reduce_workspace_bytes()) return SR_EINVAL;
+  RedWs r = red_ws(ws);
+  striu_norm_kernel<<<RBLOCKS, RT, 0, (cudaStream_t)stream>>>(n, re, im, ld, r.partials, r.counter, d_out);
+  SR_LAUNCH_CHECK();
+  return SR_OK;
+}
+
+extern "C" int sr_diag_correction_c64(int n, const void* t, const void* e, long long ld, void* l, float clip,
+                                      unsigned long long* d_clipped, int* d_flags, void* stream) {
+  if (n < 0 || ld < n) return SR_EINVAL;
+  if (n == 0) return SR_OK;
+  diag_correction_kernel<float2, float><<<ew_grid((long long)n * n), RT, 0, (cudaStream_t)stream>>>(
+      n, (const float2*)t, (const float2*)e, ld, (float2*)l, clip, d_clipped, d_flags);
+  SR_LAUNCH_CHECK();
+  return SR_OK;
+}
+
+extern "C" int sr_diag_correction_c128(int n, const void* t, const void* e, long long ld, void* l, double clip,
+                                       unsigned long long* d_clipped, int* d_flags, void* stream) {
+  if (n < 0 || ld < n) return SR_EINVAL;
+  if (n == 0) return SR_OK;
+  diag_correction_kernel<double2, double><<<ew_grid((long long)n * n), RT, 0, (cudaStream_t)stream>>>(
+      n, (const double2*)t, (const double2*)e, ld, (double2*)l, clip, d_clipped, d_flags);
   SR_LAUNCH_CHECK();
   return SR_OK;
 }

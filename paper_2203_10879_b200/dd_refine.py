@@ -93,7 +93,7 @@ class DDProducts:
         ozaki.encode(ws.y, n, n, "b", hp, out=self.eb_s)
         self._hp(self.ea_x, self.eb_s, ws.q, alpha=-0.5, add=qhat)
 
-    def entry_residuals(self):
+    def entry_residuals(self, symmetric=False):
         """history row 0 (refine.py:126-135): (||stril(Q^H A Q)||, ||Q^H Q - I||)
         measured in binary64 on the hi parts of Q and A."""
         ws, n, f = self.ws, self.ws.n, self.f64
@@ -111,6 +111,9 @@ class DDProducts:
         t_lp = ws.t_lp
         _lib.call("sr_split_lp_c128", n, ws.row0.re_ptr(), ws.row0.im_ptr(), ws.row0.ld, t_lp.data_ptr(),
                   ws.e_lp.data_ptr(), t_lp.shape[1], ws.ptr(4), ws.red[4].data_ptr(), ws.red[4].numel(), st)
+        if symmetric:  # + ||striu||: the full off-diagonal defect (refine.py:130-131)
+            _lib.call("sr_striu_norm_f64", n, ws.row0.re_ptr(), ws.row0.im_ptr(), ws.row0.ld, ws.ptr(6),
+                      ws.red[4].data_ptr(), ws.red[4].numel(), st)
         ozaki.gemm_residues(ea, eb_q, f, res, lower_only=True)
         ozaki.decode(res, ea, eb_q, f, ws.row0, shift=-1.0, hermitian=True)  # Q^H Q - I
         _lib.call("sr_fro_norm_f64", n, n, ws.row0.re_ptr(), ws.row0.im_ptr(), ws.row0.ld, ws.ptr(5),
@@ -190,8 +193,9 @@ def coerce_dd(x, device):
     return m
 
 
-def run_dd(a, qhat, cfg, device):
-    """_run in dd mode on DDPlanar inputs."""
+def run_dd(a, qhat, cfg, device, symmetric=False):
+    """_run in dd mode on DDPlanar inputs (symmetric: the Hermitian variant of
+    refine_symmetric — full off-diagonal defect, diagonal-correction solve)."""
     from .refine import RefineReport, RefineStatus, SchurPair, _phase_permutation, _structural_triangle
     n = a.rows
     ws = _workspace(n, device)
@@ -207,15 +211,15 @@ def run_dd(a, qhat, cfg, device):
     prod.entry(qhat)
     _lib.call("sr_fro_norm_f64", n, n, a.hi.re_ptr(), a.hi.im_ptr(), a.ld, ws.ptr(0), ws.red[0].data_ptr(),
               ws.red[0].numel(), st)
-    prod.entry_residuals()
+    prod.entry_residuals(symmetric)
     s = ws.scal.cpu()
     norm_a = float(s[0])
-    history = [(float(s[4]), float(s[5]))]
+    history = [(math.hypot(float(s[4]), float(s[6])) if symmetric else float(s[4]), float(s[5]))]
     tol = cfg.tol_factor * n * U_HP * norm_a
     lo_zero = not (bool(ws.q.lo.re.any()) or bool(ws.q.lo.im.any()))
     perm = _phase_permutation(ws.q.hi) if lo_zero else None
     if perm is not None:
-        t_exact = _structural_triangle(a.hi, ws.q.hi, perm)
+        t_exact = _structural_triangle(a.hi, ws.q.hi, perm, symmetric)
         if t_exact is not None:
             pair = SchurPair(q=ws.q, t=DDPlanar.from_any(t_exact, device=device), ortho_residual=history[0][1],
                              tri_residual=history[0][0])
@@ -235,8 +239,13 @@ def run_dd(a, qhat, cfg, device):
                   ws.e_lp.data_ptr(), ws.t_lp.shape[1], ws.ptr(1), ws.red[1].data_ptr(), ws.red[1].numel(), st)
         _lib.call("sr_fro_norm_f64", n, n, ws.y.hi.re_ptr(), ws.y.hi.im_ptr(), ws.y.ld, ws.ptr(2),
                   ws.red[2].data_ptr(), ws.red[2].numel(), st)
-        s = ws.scal[:3].cpu()
+        if symmetric:
+            _lib.call("sr_striu_norm_f64", n, that.hi.re_ptr(), that.hi.im_ptr(), that.ld, ws.ptr(6),
+                      ws.red[1].data_ptr(), ws.red[1].numel(), st)
+        s = ws.scal[:7].cpu()
         norm_e, norm_y = float(s[1]), float(s[2])
+        if symmetric:
+            norm_e = math.hypot(norm_e, float(s[6]))
         history.append((norm_e, norm_y))
         if not (math.isfinite(norm_e) and math.isfinite(norm_y)):
             status, iterations = RefineStatus.NON_FINITE, it
@@ -247,18 +256,25 @@ def run_dd(a, qhat, cfg, device):
         converged = norm_e <= tol
         ws.solver.clipped.zero_()
         ws.solver.flags.zero_()
-        solve_lp_device(ws.t_lp, ws.e_lp, ws.l_lp, n, cfg.clip_threshold, ws.solver, st)
+        if symmetric:
+            clip = 0.0 if cfg.clip_threshold is None else float(cfg.clip_threshold)
+            _lib.call("sr_diag_correction_c128", n, ws.t_lp.data_ptr(), ws.e_lp.data_ptr(), ws.t_lp.shape[1],
+                      ws.l_lp.data_ptr(), clip, ws.solver.clipped.data_ptr(), ws.solver.flags.data_ptr(), st)
+        else:
+            solve_lp_device(ws.t_lp, ws.e_lp, ws.l_lp, n, cfg.clip_threshold, ws.solver, st)
         _lib.call("sr_skew_c128", n, ws.l_lp.data_ptr(), ws.l_lp.shape[1], ws.w_lp.data_ptr(), ws.ptr(3),
                   ws.solver.flags.data_ptr(), ws.red[3].data_ptr(), ws.red[3].numel(), st)
         norm_w = float(ws.scal[3].cpu())
         flags = int(ws.solver.flags.item())
         nclip = int(ws.solver.clipped.item())
         if flags & _lib.SR_FLAG_SEPARATION:
-            raise SeparationError("t has exactly repeated diagonal entries: diagonal separation is "
+            raise SeparationError("repeated Ritz values: zero diagonal separation" if symmetric else
+                                  "t has exactly repeated diagonal entries: diagonal separation is "
                                   "exactly zero")
         if flags & _lib.SR_FLAG_NONFINITE:
             status, iterations = RefineStatus.NON_FINITE, it
-            detail = "iteration %d: solution contains non-finite entries" % it
+            detail = "iteration %d: %s" % (it, "diagonal correction solve overflowed" if symmetric else
+                                           "solution contains non-finite entries")
             if cfg.clip_threshold is None:
                 detail += "; " + _CLIP_HINT
             break
@@ -279,6 +295,8 @@ def run_dd(a, qhat, cfg, device):
             break
     for z in (ws.that.hi, ws.that.lo):
         _lib.call("sr_triu_inplace_f64", n, z.re_ptr(), z.im_ptr(), z.ld, st)
+        if symmetric:  # T keeps its real parts (refine.py:435-436)
+            z.im.zero_()
     last_e, last_y = history[-1]
     q_out = DDPlanar(ZPlanar.empty(n, device=device), ZPlanar.empty(n, device=device))
     t_out = DDPlanar(ZPlanar.empty(n, device=device), ZPlanar.empty(n, device=device))

@@ -200,25 +200,29 @@ def _phase_permutation(q):
     return perm
 
 
-def _structural_triangle(a, q, perm):
+def _structural_triangle(a, q, perm, symmetric=False):
     """_permuted_part_is_zero + _exact_similarity_triangle (refine.py:192-220):
-    if A[perm][:, perm] is exactly upper triangular, T = conj(q_p) A_pp q_p
-    entrywise (no products); else None."""
+    if A[perm][:, perm] is exactly upper triangular (diagonal when symmetric),
+    T = conj(q_p) A_pp q_p entrywise (no products); else None."""
     sub_re = a.re[perm][:, perm]
     nz = sub_re != 0
     if a.im is not None:
         nz = nz | (a.im[perm][:, perm] != 0)
-    if bool(torch.tril(nz, -1).any()):
+    if bool(torch.tril(nz, -1).any()) or (symmetric and bool(torch.triu(nz, 1).any())):
         return None
     cols = torch.arange(q.cols, device=perm.device)
     ph = torch.complex(q.re[perm, cols], q.im[perm, cols] if q.im is not None else torch.zeros_like(sub_re[0]))
     sub = torch.complex(sub_re, a.im[perm][:, perm] if a.im is not None else torch.zeros_like(sub_re))
     t = torch.triu(ph.conj()[:, None] * sub * ph[None, :])
+    if symmetric:  # the real diagonal only (refine.py:214-219)
+        t = torch.diag(torch.diagonal(t).real).to(t.dtype)
     return t
 
 
-def _run_fp64(a, qhat, cfg, ws):
-    """_run (refine.py:223-329) with hp = FP64, lp = complex64."""
+def _run_fp64(a, qhat, cfg, ws, symmetric=False):
+    """_run (refine.py:223-329) with hp = FP64, lp = complex64.  symmetric
+    (refine_symmetric): the defect is the full off-diagonal part of Q^H A Q
+    and the solve is the entrywise diagonal correction."""
     n = a.rows
     st = _stream()
     hp0 = _counters["hp_calls"]
@@ -234,7 +238,7 @@ def _run_fp64(a, qhat, cfg, ws):
     history = []
     perm = _phase_permutation(ws.q)
     if perm is not None:
-        t_exact = _structural_triangle(a, ws.q, perm)
+        t_exact = _structural_triangle(a, ws.q, perm, symmetric)
         if t_exact is not None:
             # exactly unitary Q, exactly triangular Q^H A Q: zero iterations
             # beyond the entry check (refine.py:239-252)
@@ -259,9 +263,14 @@ def _run_fp64(a, qhat, cfg, ws):
                   ws.e_lp.data_ptr(), ws.t_lp.shape[1], ws.ptr(1), ws.red[1].data_ptr(), ws.red[1].numel(), st)
         _lib.call("sr_fro_norm_f64", n, n, ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld, ws.ptr(2),
                   ws.red[2].data_ptr(), ws.red[2].numel(), st)
+        if symmetric:  # + ||striu(T^)||: the full off-diagonal defect (refine.py:130-131)
+            _lib.call("sr_striu_norm_f64", n, ws.that.re_ptr(), ws.that.im_ptr(), ws.that.ld, ws.ptr(6),
+                      ws.red[1].data_ptr(), ws.red[1].numel(), st)
         _mark("split_norms")
-        s = ws.scal[:3].cpu()  # sync 1
+        s = ws.scal[:7].cpu()  # sync 1
         norm_a, norm_e, norm_y = float(s[0]), float(s[1]), float(s[2])
+        if symmetric:
+            norm_e = math.hypot(norm_e, float(s[6]))
         if tol is None:
             tol = cfg.tol_factor * n * U_FP64 * norm_a
             # row 0: entry state measured in FP64 (see oracle/refine_fp64.py)
@@ -277,7 +286,12 @@ def _run_fp64(a, qhat, cfg, ws):
         # lp solve + W = L - L^H + ||W|| + finiteness
         ws.solver.clipped.zero_()
         ws.solver.flags.zero_()
-        solve_lp_device(ws.t_lp, ws.e_lp, ws.l_lp, n, cfg.clip_threshold, ws.solver, st)
+        if symmetric:
+            clip = 0.0 if cfg.clip_threshold is None else float(cfg.clip_threshold)
+            _lib.call("sr_diag_correction_c64", n, ws.t_lp.data_ptr(), ws.e_lp.data_ptr(), ws.t_lp.shape[1],
+                      ws.l_lp.data_ptr(), clip, ws.solver.clipped.data_ptr(), ws.solver.flags.data_ptr(), st)
+        else:
+            solve_lp_device(ws.t_lp, ws.e_lp, ws.l_lp, n, cfg.clip_threshold, ws.solver, st)
         _mark("solve")
         _lib.call("sr_skew_c64", n, ws.l_lp.data_ptr(), ws.l_lp.shape[1], ws.w_lp.data_ptr(), ws.ptr(3),
                   ws.solver.flags.data_ptr(), ws.red[3].data_ptr(), ws.red[3].numel(), st)
@@ -286,11 +300,13 @@ def _run_fp64(a, qhat, cfg, ws):
         flags = int(ws.solver.flags.item())
         nclip = int(ws.solver.clipped.item())
         if flags & _lib.SR_FLAG_SEPARATION:
-            raise SeparationError("t has exactly repeated diagonal entries: diagonal separation is "
+            raise SeparationError("repeated Ritz values: zero diagonal separation" if symmetric else
+                                  "t has exactly repeated diagonal entries: diagonal separation is "
                                   "exactly zero")
         if flags & _lib.SR_FLAG_NONFINITE:
             status, iterations = RefineStatus.NON_FINITE, it
-            detail = "iteration %d: solution contains non-finite entries" % it
+            detail = "iteration %d: %s" % (it, "diagonal correction solve overflowed" if symmetric else
+                                           "solution contains non-finite entries")
             if cfg.clip_threshold is None:
                 detail += "; " + _CLIP_HINT
             break
@@ -312,6 +328,8 @@ def _run_fp64(a, qhat, cfg, ws):
             status, iterations = RefineStatus.DIVERGED, it
             break
     _lib.call("sr_triu_inplace_f64", n, ws.that.re_ptr(), ws.that.im_ptr(), ws.that.ld, st)
+    if symmetric:  # T keeps its real parts (refine.py:435-436)
+        ws.that.im.zero_()
     last_e, last_y = history[-1]
     pair = SchurPair(q=ws.q.to_complex(), t=ws.that.to_complex(), ortho_residual=last_y,
                      tri_residual=last_e)

@@ -190,9 +190,44 @@ def gen_configs(ref):
                   indent=1)
 
 
+def gen_symmetric(ref):
+    """refine_symmetric (refine.py:409-438) in the reference's dd mode on
+    seeded Hermitian matrices A = (X + X^H) / 2 (Philox), default config:
+    status, iterations, history, hp count, detail, the refined T diagonal
+    (dd) and verify_pair of the result; plus the NotSymmetric rejection."""
+    from ddschur.refine import NotSymmetric, RefineConfig, refine_symmetric, verify_pair
+    out = {}
+    cases = []
+    for k, n in enumerate((12, 24, 40)):
+        rng = np.random.Generator(np.random.Philox(5000 + k))
+        x = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) * np.sqrt(0.5)
+        a = (x + x.conj().T) / 2.0
+        pair, rep = refine_symmetric(a, RefineConfig(seed=k))
+        v = verify_pair(a, pair)
+        out["a_%d" % k] = a
+        for cell, arr in zip(("rh", "rl", "ih", "il"), pair.t.cells()):
+            out["t%s_%d" % (cell, k)] = np.ascontiguousarray(np.diag(arr))
+        cases.append(dict(k=k, n=n, seed=k, iterations=rep.iterations, status=rep.status.value,
+                          residual_history=[list(map(float, r)) for r in rep.residual_history],
+                          hp_matmul_count=rep.hp_matmul_count, skip_fired=bool(rep.skip_fired),
+                          detail=rep.detail, verify=list(map(float, v))))
+    rng = np.random.Generator(np.random.Philox(5100))
+    bad = rng.standard_normal((8, 8))
+    try:
+        refine_symmetric(bad)
+        rejected = ""
+    except NotSymmetric as exc:
+        rejected = str(exc)
+    out["a_nonsym"] = bad
+    np.savez_compressed(os.path.join(HERE, "symmetric_ref.npz"), **out)
+    with open(os.path.join(HERE, "symmetric_ref.json"), "w") as f:
+        json.dump(dict(source="ddschur.refine.refine_symmetric (refine.py:409-438), RefineConfig(seed=k)",
+                       cases=cases, nonsym_message=rejected), f, indent=1)
+
+
 if __name__ == "__main__":
     ref = import_reference()
-    which = sys.argv[1:] or ["trisolve", "ddgemm", "refine_dd", "configs"]
+    which = sys.argv[1:] or ["trisolve", "ddgemm", "refine_dd", "configs", "symmetric"]
     for w in which:
         t0 = time.time()
         globals()["gen_" + w](ref)

@@ -19,6 +19,7 @@ from .refine import (
 from .trisolve import TriEqProblem, TriEqSolution, solve_block
 from .continuation import refine_continuation
 from .symmetric import order_by_random_line, refine_symmetric
+from .mixed import refine_mixed
 from .matrix import DDPlanar
 
 __version__ = "0.1.0"
@@ -27,5 +28,5 @@ __all__ = [
     "matmul_lp", "reset_counters", "ZPlanar", "U_FP64", "U_HP", "OrthoStrategy", "RefineConfig",
     "RefineReport", "RefineStatus", "SchurPair", "refine_template", "verify_pair", "VerifyResiduals", "TriEqProblem",
     "TriEqSolution", "solve_block", "refine_continuation", "DDPlanar", "refine_symmetric",
-    "order_by_random_line",
+    "order_by_random_line", "refine_mixed",
 ]

@@ -225,9 +225,35 @@ def gen_symmetric(ref):
                        cases=cases, nonsym_message=rejected), f, indent=1)
 
 
+def gen_mixed(ref):
+    """refine_mixed (refine.py:383-406) in the reference's dd mode on seeded
+    complex Gaussian matrices (Philox), default config with seed k: status,
+    iterations, history, hp count, the refined T diagonal (dd, in the
+    random-line order) and verify_pair of the result."""
+    from ddschur.refine import RefineConfig, refine_mixed, verify_pair
+    out = {}
+    cases = []
+    for k, n in enumerate((12, 24, 40)):
+        rng = np.random.Generator(np.random.Philox(6000 + k))
+        a = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) * np.sqrt(0.5)
+        pair, rep = refine_mixed(a, RefineConfig(seed=k))
+        v = verify_pair(a, pair)
+        out["a_%d" % k] = a
+        for cell, arr in zip(("rh", "rl", "ih", "il"), pair.t.cells()):
+            out["t%s_%d" % (cell, k)] = np.ascontiguousarray(np.diag(arr))
+        cases.append(dict(k=k, n=n, seed=k, iterations=rep.iterations, status=rep.status.value,
+                          residual_history=[list(map(float, r)) for r in rep.residual_history],
+                          hp_matmul_count=rep.hp_matmul_count, skip_fired=bool(rep.skip_fired),
+                          detail=rep.detail, verify=list(map(float, v))))
+    np.savez_compressed(os.path.join(HERE, "mixed_ref.npz"), **out)
+    with open(os.path.join(HERE, "mixed_ref.json"), "w") as f:
+        json.dump(dict(source="ddschur.refine.refine_mixed (refine.py:383-406), RefineConfig(seed=k)",
+                       cases=cases), f, indent=1)
+
+
 if __name__ == "__main__":
     ref = import_reference()
-    which = sys.argv[1:] or ["trisolve", "ddgemm", "refine_dd", "configs", "symmetric"]
+    which = sys.argv[1:] or ["trisolve", "ddgemm", "refine_dd", "configs", "symmetric", "mixed"]
     for w in which:
         t0 = time.time()
         globals()["gen_" + w](ref)

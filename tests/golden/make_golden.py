@@ -251,9 +251,46 @@ def gen_mixed(ref):
                        cases=cases), f, indent=1)
 
 
+def gen_io(ref):
+    """Matrix Market files written by the reference (mmio.py:179-217) and the
+    planes its reader returns (mmio.py:137-156), plus a coordinate symmetric
+    file and a schema-v1 run record built by the reference (cli.py:83-103)."""
+    from ddschur.ddmatrix import DDMatrix
+    from ddschur.generators import MatrixKind, MatrixSpec
+    from ddschur.mmio import read_matrix_market, write_matrix_market
+    from ddschur.cli import build_run_record, validate_run_record
+    from ddschur.refine import RefineConfig, refine_template, verify_pair
+    rng = np.random.Generator(np.random.Philox(7000))
+    out = {}
+    n = 5
+    hi = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    lo = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) * 1e-17
+    dd = DDMatrix.from_lp(hi) + DDMatrix.from_lp(lo)
+    write_matrix_market(os.path.join(HERE, "mm_dd_complex.mtx"), dd, comment="reference writer, dd")
+    write_matrix_market(os.path.join(HERE, "mm_f64_real.mtx"), rng.standard_normal((3, 4)), comment="binary64")
+    with open(os.path.join(HERE, "mm_coord_sym.mtx"), "w") as f:
+        f.write("%%MatrixMarket matrix coordinate real symmetric\n% hand-written\n4 4 5\n"
+                "1 1 2.5\n2 1 -1\n3 2 0.1\n4 4 1e-300\n4 3 3.14159265358979323846264338327950288\n")
+    for tag in ("dd_complex", "f64_real", "coord_sym"):
+        m = read_matrix_market(os.path.join(HERE, "mm_%s.mtx" % tag))
+        for cell, arr in zip(("rh", "rl", "ih", "il"), m.cells()):
+            out["%s_%s" % (tag, cell)] = np.ascontiguousarray(arr)
+    for cell, arr in zip(("rh", "rl", "ih", "il"), dd.cells()):
+        out["src_%s" % cell] = np.ascontiguousarray(arr)
+    np.savez_compressed(os.path.join(HERE, "io_ref.npz"), **out)
+    # a run record of a real refinement
+    a = (rng.standard_normal((8, 8)) + 1j * rng.standard_normal((8, 8)))
+    from ddschur.refine import refine_mixed
+    pair, rep = refine_mixed(a, RefineConfig(seed=1))
+    spec = MatrixSpec(kind=MatrixKind.RANDN_COMPLEX, n=8, seed=1)
+    rec = validate_run_record(build_run_record(spec, RefineConfig(seed=1), rep, verify_pair(a, pair)))
+    with open(os.path.join(HERE, "run_record_ref.json"), "w") as f:
+        json.dump(rec, f, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
     ref = import_reference()
-    which = sys.argv[1:] or ["trisolve", "ddgemm", "refine_dd", "configs", "symmetric", "mixed"]
+    which = sys.argv[1:] or ["trisolve", "ddgemm", "refine_dd", "configs", "symmetric", "mixed", "io"]
     for w in which:
         t0 = time.time()
         globals()["gen_" + w](ref)

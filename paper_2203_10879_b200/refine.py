@@ -219,7 +219,51 @@ def _structural_triangle(a, q, perm, symmetric=False):
     return t
 
 
-def _run_fp64(a, qhat, cfg, ws, symmetric=False):
+class _HostResult:
+    """Device->host delivery of the result into caller-provided pinned host
+    tensors (refine_template(out=(q_host, t_host))):
+    the Q each measurement sees is copied to pinned host memory on a side
+    stream while that measurement runs — the last one is the returned Q
+    whenever the loop ends without a further update (convergence with the
+    skip rule, the config-3 case) — and T is copied at the end."""
+
+    def __init__(self, n, device, q_host, t_host):
+        for h in (q_host, t_host):
+            if not (isinstance(h, torch.Tensor) and h.device.type == "cpu" and h.dtype == torch.complex128
+                    and tuple(h.shape) == (n, n) and h.is_contiguous()):
+                raise ValueError("out must be two contiguous (n, n) complex128 CPU tensors")
+        self.n = n
+        self.stream = torch.cuda.Stream(device=device)
+        self.buf = torch.empty((n, n), dtype=torch.complex128, device=device)
+        self.done = torch.cuda.Event()
+        self.q_host, self.t_host = q_host, t_host
+        self.copied_version = -1
+        self.started = False
+
+    def copy_q(self, q, version):
+        main = torch.cuda.current_stream()
+        if self.started:
+            main.wait_event(self.done)  # the previous D2H has left buf
+        self.buf.copy_(q.to_complex())
+        ready = torch.cuda.Event()
+        ready.record(main)
+        self.stream.wait_event(ready)
+        with torch.cuda.stream(self.stream):
+            self.q_host.copy_(self.buf, non_blocking=True)
+            self.done.record(self.stream)
+        self.started = True
+        self.copied_version = version
+
+    def finish(self, q, version, t):
+        if self.copied_version != version:
+            self.copy_q(q, version)
+        self.t_host.copy_(t.to_complex(), non_blocking=True)
+        self.done.synchronize()
+        torch.cuda.current_stream().synchronize()
+        return self.q_host, self.t_host
+
+
+def _run_fp64(a, qhat, cfg, ws, symmetric=False, host=None):
     """_run (refine.py:223-329) with hp = FP64, lp = complex64.  symmetric
     (refine_symmetric): the defect is the full off-diagonal part of Q^H A Q
     and the solve is the entrywise diagonal correction."""
@@ -243,7 +287,12 @@ def _run_fp64(a, qhat, cfg, ws, symmetric=False):
             # exactly unitary Q, exactly triangular Q^H A Q: zero iterations
             # beyond the entry check (refine.py:239-252)
             history.append((0.0, 0.0))
-            pair = SchurPair(q=ws.q.to_complex(), t=t_exact, ortho_residual=0.0, tri_residual=0.0)
+            q_out = ws.q.to_complex()
+            if host is not None:
+                host.q_host.copy_(q_out)
+                host.t_host.copy_(t_exact)
+                q_out, t_exact = host.q_host, host.t_host
+            pair = SchurPair(q=q_out, t=t_exact, ortho_residual=0.0, tri_residual=0.0)
             report = RefineReport(iterations=0, residual_history=history,
                                   hp_matmul_count=_counters["hp_calls"] - hp0, clipped_total=0,
                                   status=RefineStatus.CONVERGED, wall_time=0.0)
@@ -255,7 +304,10 @@ def _run_fp64(a, qhat, cfg, ws, symmetric=False):
     iterations = cfg.max_iters
     streak = 0
     tol = None
+    q_version = 0
     for it in range(1, cfg.max_iters + 1):
+        if host is not None:  # this Q is the result if the loop stops without another update
+            host.copy_q(ws.q, q_version)
         # T^ = (Q^H A) Q; split + lp downcast + ||E||; Y = Q^H Q - I; ||Y||
         prod.measure(a)
         _mark("measure")
@@ -316,6 +368,7 @@ def _run_fp64(a, qhat, cfg, ws, symmetric=False):
         if not skip:
             prod.update(cfg.restore_full_sigma,
                         sigma_bound=products.sigma_prime_bound(norm_y, norm_w, cfg.restore_full_sigma))
+            q_version += 1
             _mark("update")
         if converged:
             status, iterations, skip_fired = RefineStatus.CONVERGED, it, skip
@@ -331,8 +384,11 @@ def _run_fp64(a, qhat, cfg, ws, symmetric=False):
     if symmetric:  # T keeps its real parts (refine.py:435-436)
         ws.that.im.zero_()
     last_e, last_y = history[-1]
-    pair = SchurPair(q=ws.q.to_complex(), t=ws.that.to_complex(), ortho_residual=last_y,
-                     tri_residual=last_e)
+    if host is not None:
+        q_out, t_out = host.finish(ws.q, q_version, ws.that)
+    else:
+        q_out, t_out = ws.q.to_complex(), ws.that.to_complex()
+    pair = SchurPair(q=q_out, t=t_out, ortho_residual=last_y, tri_residual=last_e)
     report = RefineReport(iterations=iterations, residual_history=history,
                           hp_matmul_count=_counters["hp_calls"] - hp0, clipped_total=clipped_total,
                           status=status, wall_time=0.0, skip_fired=skip_fired, detail=detail)
@@ -360,11 +416,15 @@ def _workspace(n, device):
     return ws
 
 
-def refine_template(a, qhat, cfg=None, device=None):
+def refine_template(a, qhat, cfg=None, device=None, out=None):
     """Refine a user-supplied candidate Q toward a Schur pair of A
     (refine.py:357-380).  a, qhat: numpy arrays, torch tensors (any device)
     or ZPlanar device matrices; real A is kept real.  Returns
-    (SchurPair, RefineReport) with q, t as complex128 CUDA tensors."""
+    (SchurPair, RefineReport) with q, t as complex128 CUDA tensors, or (FP64
+    mode, out=(q_host, t_host): two (n, n) complex128 CPU tensors, pinned for
+    asynchronous copies) written into those host tensors — like the
+    reference's host DDMatrix result — with Q's device->host copy overlapped
+    with the final measurement."""
     cfg = RefineConfig() if cfg is None else cfg
     if cfg.ortho is not OrthoStrategy.NEWTON_SCHULZ:
         raise NotImplementedError("QR retraction is not on the B200 path (no CPU fallback)")
@@ -390,7 +450,8 @@ def refine_template(a, qhat, cfg=None, device=None):
         qhat = ZPlanar.from_any(qhat.re, device=device, force_complex=True)
     if True:
         ws = _workspace(a.rows, device)
-        pair, report = _run_fp64(a, qhat, cfg, ws)
+        host = _HostResult(a.rows, device, *out) if out is not None else None
+        pair, report = _run_fp64(a, qhat, cfg, ws, host=host)
     torch.cuda.current_stream().synchronize()
     report.wall_time = time.perf_counter() - t0
     return pair, report

@@ -148,3 +148,26 @@ def test_config5_continuation_matches_oracle_chain():
         assert abs(rep.iterations - ref["iterations"]) <= 1
         rel_e, ortho = residuals_fp64(a, pair.q.cpu().numpy())
         assert rel_e <= 15 * U and ortho <= 2 * max(residuals_fp64(a, ref["q"])[1], 10 * np.sqrt(n) * U)
+
+
+def test_host_result_matches_device_result():
+    """refine_template(out=(q_host, t_host)): host Q, T identical to the
+    device result (the speculative Q copy is the final Q)."""
+    from paper_2203_10879_b200 import inputs
+    n = 300
+    a = inputs.gaussian_complex(n, 4)
+    q = inputs.schur_vectors(a).astype(np.complex128)
+    cfg = RefineConfig(precision="fp64", tol_factor=10.0 / n, max_iters=10)
+    p1, r1 = refine_template(a, q, cfg)
+    host = lambda: (torch.empty((n, n), dtype=torch.complex128, pin_memory=True),  # noqa: E731
+                    torch.empty((n, n), dtype=torch.complex128, pin_memory=True))
+    out = host()
+    p2, r2 = refine_template(a, q, cfg, out=out)
+    assert p2.q is out[0] and p2.t is out[1]
+    assert torch.equal(p1.q.cpu(), p2.q) and torch.equal(p1.t.cpu(), p2.t)
+    assert r1.iterations == r2.iterations and r1.residual_history == r2.residual_history
+    # a run whose last step is an update (no skip): the final Q is the updated one
+    cfg2 = RefineConfig(precision="fp64", tol_factor=10.0 / n, max_iters=10, skip_final_ortho=False)
+    p3, _ = refine_template(a, q, cfg2)
+    p4, _ = refine_template(a, q, cfg2, out=host())
+    assert torch.equal(p3.q.cpu(), p4.q) and torch.equal(p3.t.cpu(), p4.t)

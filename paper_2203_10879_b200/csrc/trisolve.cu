@@ -165,6 +165,23 @@ __device__ __forceinline__ void tile_mac(C (&acc)[2][4], const C* sA, const C* s
   }
 }
 
+// 1 / d for the reciprocal pivots: Smith-scaled (no overflow for |d| near the
+// range limits), one reciprocal instead of cdiv's four divisions
+__device__ __forceinline__ float2 crecip(float2 d) {
+  const float s = fmaxf(fabsf(d.x), fabsf(d.y));
+  const float is = 1.0f / s;
+  const float a = d.x * is, b = d.y * is;
+  const float r = is / (a * a + b * b);
+  return make_float2(a * r, -b * r);
+}
+__device__ __forceinline__ double2 crecip(double2 d) {
+  const double s = fmax(fabs(d.x), fabs(d.y));
+  const double is = 1.0 / s;
+  const double a = d.x * is, b = d.y * is;
+  const double r = is / (a * a + b * b);
+  return make_double2(a * r, -b * r);
+}
+
 // In-tile solve by warp 0: T2 X - X T1 = R (strict lower part only when DIAG).
 // sP[i][j] = 1 / (T2_ii - T1_jj); sD[d][j] = T1[j][j + d].
 template <typename C, bool DIAG>
@@ -286,10 +303,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SweepArgs p, const C* __restr
       C d;
       d.x = sT2[i * LD + i].x - sT1[j * LD + j].x;
       d.y = sT2[i * LD + i].y - sT1[j * LD + j].y;
-      C one;
-      one.x = 1;
-      one.y = 0;
-      sP[i * LD + j] = cdiv(one, d);
+      sP[i * LD + j] = crecip(d);
       // idx = dd * NB + jj: sD[dd][jj] = T1[jj][jj + dd]
       sD[idx] = (i + j < NB) ? sT1[j * LD + j + i] : czero<C>();
     }

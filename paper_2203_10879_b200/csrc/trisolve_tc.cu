@@ -337,44 +337,53 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       __syncwarp();
       eb_s[ew][lane] = jl < n ? line_exp(max4(p.b_max, (size_t)n, jl)) : 0;
       __syncwarp();
+      const int tgt = t0 + ew;  // target tile index along the line
+      const bool live = tgt < p.h;
+      // prefetch this unit's Rf block into registers before waiting for the
+      // accumulator: the loads overlap the unit's MMAs (targets of different
+      // units never overlap, so nothing in flight writes them)
+      float2 q[NB];
+      if (!ROW) {
+        const int c0 = line * NB, row0 = a_row0 + ew * 32;
+        const bool ok = live && c0 + lane < n;
+#pragma unroll
+        for (int r = 0; r < NB; ++r)
+          q[r] = (ok && row0 + r < n) ? Rf[(size_t)(row0 + r) * ld + c0 + lane] : make_float2(0.f, 0.f);
+      } else {
+        const int r0 = line * NB;
+        const bool ok = live && idx < n;
+#pragma unroll
+        for (int i = 0; i < NB; ++i)
+          q[i] = (ok && r0 + i < n) ? Rf[(size_t)(r0 + i) * ld + idx] : make_float2(0.f, 0.f);
+      }
       mbar_wait(tfull_bar(acc), (k >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       uint32_t v[64];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t (&vq)[16] = *reinterpret_cast<uint32_t(*)[16]>(&v[16 * q]);
-        tmem_ld16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * 64 + 16 * q), vq);
+      for (int qq = 0; qq < 4; ++qq) {
+        uint32_t (&vq)[16] = *reinterpret_cast<uint32_t(*)[16]>(&v[16 * qq]);
+        tmem_ld16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * 64 + 16 * qq), vq);
       }
       asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       mbar_arrive(tempty_bar(acc));  // the accumulator is in registers: release it to the MMA warp
-      const int tgt = t0 + ew;       // target tile index along the line
-      if (tgt < p.h) {
+      if (live) {
         if (!ROW) {
           // stage the warp's 32 x 32 block, then update Rf row by row with
-          // coalesced 256-byte accesses
+          // coalesced 256-byte stores
 #pragma unroll
           for (int c = 0; c < NB; ++c) {
             const float sc = ldexpf(1.f, ea + eb_s[ew][c]);
             buf[lane * 33 + c] = make_float2(__uint_as_float(v[2 * c]) * sc, __uint_as_float(v[2 * c + 1]) * sc);
           }
           __syncwarp();
-          // read-modify-write in groups of 16 rows: the 16 loads are independent
-          // and in flight together (one dependent load per row would serialise
-          // the epilogue on the memory latency)
           const int c0 = line * NB, row0 = a_row0 + ew * 32;
-          const bool colok = c0 + lane < n;
+          if (c0 + lane < n) {
 #pragma unroll
-          for (int g = 0; g < 32; g += 16) {
-            float2 q[16];
-#pragma unroll
-            for (int r = 0; r < 16; ++r)
-              q[r] = (colok && row0 + g + r < n) ? Rf[(size_t)(row0 + g + r) * ld + c0 + lane] : make_float2(0.f, 0.f);
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-              if (colok && row0 + g + r < n) {
-                const float2 a = buf[(g + r) * 33 + lane];
-                Rf[(size_t)(row0 + g + r) * ld + c0 + lane] = make_float2(q[r].x - a.x, q[r].y - a.y);
+            for (int r = 0; r < NB; ++r) {
+              if (row0 + r < n) {
+                const float2 a = buf[r * 33 + lane];
+                Rf[(size_t)(row0 + r) * ld + c0 + lane] = make_float2(q[r].x - a.x, q[r].y - a.y);
               }
             }
           }
@@ -382,19 +391,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         } else if (idx < n) {
           const int r0 = line * NB;
 #pragma unroll
-          for (int g = 0; g < NB; g += 16) {
-            float2 q[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              q[i] = r0 + g + i < n ? Rf[(size_t)(r0 + g + i) * ld + idx] : make_float2(0.f, 0.f);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              if (r0 + g + i < n) {
-                const float sc = ldexpf(1.f, ea + eb_s[ew][g + i]);
-                Rf[(size_t)(r0 + g + i) * ld + idx] =
-                    make_float2(q[i].x + __uint_as_float(v[2 * (g + i)]) * sc,
-                                q[i].y + __uint_as_float(v[2 * (g + i) + 1]) * sc);
-              }
+          for (int i = 0; i < NB; ++i) {
+            if (r0 + i < n) {
+              const float sc = ldexpf(1.f, ea + eb_s[ew][i]);
+              Rf[(size_t)(r0 + i) * ld + idx] = make_float2(q[i].x + __uint_as_float(v[2 * i]) * sc,
+                                                            q[i].y + __uint_as_float(v[2 * i + 1]) * sc);
             }
           }
         }

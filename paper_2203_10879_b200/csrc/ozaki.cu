@@ -136,6 +136,9 @@ struct EncodeParams {
   int8_t* out2;
   float pf[MAXMOD], invf[MAXMOD], hif[MAXMOD], lof[MAXMOD];
   float pow2[MAXMOD][MAXDIG];  // 2^(11 c) mod p, symmetric
+  int pi[MAXMOD];              // the moduli as ints
+  int wb[MAXMOD][2];           // 2^(8 c) mod p, c = 0..7, symmetric int8, packed 4 per word
+  int c64[MAXMOD];             // 2^64 mod p, symmetric
 };
 
 // balanced 11-bit digits of an integer-valued double (error-free, top-down)
@@ -147,6 +150,36 @@ __device__ __forceinline__ void digits(double a, float (&d)[ND]) {
     const double q = rint(a * (1.0 / sc));
     a = fma(-q, sc, a);
     d[c] = (float)q;
+  }
+}
+
+__device__ __forceinline__ int dp4a_us(uint32_t a, int b, int c) {  // unsigned bytes . signed bytes + c
+  int d;
+  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// the residue words of 4 consecutive k of row i, modulus l, in the layout's planes
+__device__ __forceinline__ void store_planes(const EncodeParams& p, int8_t* dst, int l, long long mod_stride,
+                                             long long mod_stride2, long long plane_stride, int i, int k,
+                                             uint32_t wr, uint32_t wi, uint32_t wn) {
+  int8_t* dm = dst + (size_t)l * mod_stride;
+  if (p.layout == 0) {
+    *reinterpret_cast<uint32_t*>(dm) = wr;
+    *reinterpret_cast<uint32_t*>(dm + plane_stride) = wi;
+  } else if (p.layout == 1) {
+    *reinterpret_cast<uint32_t*>(dm) = wn;
+    *reinterpret_cast<uint32_t*>(dm + plane_stride) = wr;
+    *reinterpret_cast<uint32_t*>(dm + 2 * plane_stride) = wi;
+  } else if (p.layout == 3) {
+    *reinterpret_cast<uint32_t*>(dm) = wr;  // A operand of X^H: (re, -im)
+    *reinterpret_cast<uint32_t*>(dm + plane_stride) = wn;
+    int8_t* d2 = p.out2 + (size_t)l * mod_stride2 + (size_t)i * p.kpitch + k;  // B operand of X
+    *reinterpret_cast<uint32_t*>(d2) = wn;
+    *reinterpret_cast<uint32_t*>(d2 + plane_stride) = wr;
+    *reinterpret_cast<uint32_t*>(d2 + 2 * plane_stride) = wi;
+  } else {
+    *reinterpret_cast<uint32_t*>(dm) = wr;
   }
 }
 
@@ -197,7 +230,51 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
     const int i = i0 + il, k = k0 + kl;
     if (i >= p.rows_out || k >= p.K) continue;
     const int sh = p.beta - exps[i];
-    // exact 11-bit digit expansions of the scaled integers (FP64, error-free)
+    int8_t* dst = out + (size_t)i * p.kpitch + k;
+    if constexpr (!DD) {
+      // |scaled| <= 2^61: exact int64.  Its two's-complement bytes u_c give
+      // x mod p = sum_c u_c (2^(8c) mod p) - [x < 0] (2^64 mod p): two byte dot
+      // products (dp4a) per value and modulus, one reduction
+      uint32_t lo_r[4], hi_r[4], lo_i[4], hi_i[4];
+      bool ng_r[4], ng_i[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        double xi = s_im[il][kl + e];
+        if (p.conj) xi = -xi;
+        const long long a = __double2ll_rn(scale2(s_re[il][kl + e], sh));
+        const long long b = __double2ll_rn(scale2(xi, sh));
+        lo_r[e] = (uint32_t)a;
+        hi_r[e] = (uint32_t)((unsigned long long)a >> 32);
+        lo_i[e] = (uint32_t)b;
+        hi_i[e] = (uint32_t)((unsigned long long)b >> 32);
+        ng_r[e] = a < 0;
+        ng_i[e] = b < 0;
+      }
+      for (int l = 0; l < p.nmod; ++l) {
+        const int pm = p.pi[l];
+        const float inv = p.invf[l];
+        const int hi = ((pm + 1) >> 1) - 1, lo = -(pm >> 1);
+        const int w0 = p.wb[l][0], w1 = p.wb[l][1], c64 = p.c64[l];
+        uint32_t wr = 0, wi = 0, wn = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          int vr = dp4a_us(hi_r[e], w1, dp4a_us(lo_r[e], w0, 0)) - (ng_r[e] ? c64 : 0);
+          int vi = dp4a_us(hi_i[e], w1, dp4a_us(lo_i[e], w0, 0)) - (ng_i[e] ? c64 : 0);
+          int rr = vr - __float2int_rn((float)vr * inv) * pm;  // |v| < 2^19: float exact
+          int ri = vi - __float2int_rn((float)vi * inv) * pm;
+          rr = rr > hi ? rr - pm : (rr < lo ? rr + pm : rr);
+          ri = ri > hi ? ri - pm : (ri < lo ? ri + pm : ri);
+          int rn = -ri;
+          rn = rn > hi ? rn - pm : rn;
+          wr |= ((uint32_t)rr & 0xFFu) << (8 * e);
+          wi |= ((uint32_t)ri & 0xFFu) << (8 * e);
+          wn |= ((uint32_t)rn & 0xFFu) << (8 * e);
+        }
+        store_planes(p, dst, l, mod_stride, mod_stride2, plane_stride, i, k, wr, wi, wn);
+      }
+      continue;
+    }
+    // dd operands (beta up to 106): exact 11-bit digit expansions of hi and lo
     float dr[4][ND], di[4][ND];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -218,7 +295,6 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
         }
       }
     }
-    int8_t* dst = out + (size_t)i * p.kpitch + k;
     for (int l = 0; l < p.nmod; ++l) {
       const float pm = p.pf[l], inv = p.invf[l], hi = p.hif[l], lo = p.lof[l];
       uint32_t wr = 0, wi = 0, wn = 0;
@@ -246,24 +322,7 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
         wi |= (__float_as_uint(ri + 12582912.f) & 0xFFu) << (8 * e);
         wn |= (__float_as_uint(rn + 12582912.f) & 0xFFu) << (8 * e);
       }
-      int8_t* dm = dst + (size_t)l * mod_stride;
-      if (p.layout == 0) {
-        *reinterpret_cast<uint32_t*>(dm) = wr;
-        *reinterpret_cast<uint32_t*>(dm + plane_stride) = wi;
-      } else if (p.layout == 1) {
-        *reinterpret_cast<uint32_t*>(dm) = wn;
-        *reinterpret_cast<uint32_t*>(dm + plane_stride) = wr;
-        *reinterpret_cast<uint32_t*>(dm + 2 * plane_stride) = wi;
-      } else if (p.layout == 3) {
-        *reinterpret_cast<uint32_t*>(dm) = wr;  // A operand of X^H: (re, -im)
-        *reinterpret_cast<uint32_t*>(dm + plane_stride) = wn;
-        int8_t* d2 = p.out2 + (size_t)l * mod_stride2 + (size_t)i * p.kpitch + k;  // B operand of X
-        *reinterpret_cast<uint32_t*>(d2) = wn;
-        *reinterpret_cast<uint32_t*>(d2 + plane_stride) = wr;
-        *reinterpret_cast<uint32_t*>(d2 + 2 * plane_stride) = wi;
-      } else {
-        *reinterpret_cast<uint32_t*>(dm) = wr;
-      }
+      store_planes(p, dst, l, mod_stride, mod_stride2, plane_stride, i, k, wr, wi, wn);
     }
   }
 }
@@ -560,6 +619,17 @@ int encode_launch(int rows_out, int K, int kind, const void* re, const double* i
       p.pow2[l][c] = (float)r;
       pw = (pw << 11) % m;
     }
+    p.pi[l] = m;
+    auto sym = [m](long long r) { r %= m; return r > ((m + 1) >> 1) - 1 ? r - m : r; };
+    long long pb = 1;  // 2^(8c) mod m
+    uint32_t words[2] = {0, 0};
+    for (int c = 0; c < 8; ++c) {
+      words[c / 4] |= ((uint32_t)(sym(pb) & 0xFF)) << (8 * (c % 4));
+      pb = (pb << 8) % m;
+    }
+    p.wb[l][0] = (int)words[0];
+    p.wb[l][1] = (int)words[1];
+    p.c64[l] = (int)sym(pb);  // after 8 steps pb = 2^64 mod m
   }
   // K padding columns of the residue planes must read as zero
   const int planes = layout == 0 || layout == 3 ? 2 : (layout == 1 ? 3 : 1);

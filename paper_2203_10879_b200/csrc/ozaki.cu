@@ -139,6 +139,8 @@ struct EncodeParams {
   int pi[MAXMOD];              // the moduli as ints
   int wb[MAXMOD][2];           // 2^(8 c) mod p, c = 0..7, symmetric int8, packed 4 per word
   int c64[MAXMOD];             // 2^64 mod p, symmetric
+  uint32_t bm[MAXMOD];         // Barrett multiplier floor(2^32 / p) + 1
+  int off0[MAXMOD], off1[MAXMOD];  // positive shift (a multiple of p), and it minus 2^64 mod p
 };
 
 // balanced 11-bit digits of an integer-valued double (error-free, top-down)
@@ -250,25 +252,35 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
         ng_r[e] = a < 0;
         ng_i[e] = b < 0;
       }
+      const bool need_neg = p.layout == 1 || p.layout == 3;  // planes with -im
       for (int l = 0; l < p.nmod; ++l) {
         const int pm = p.pi[l];
-        const float inv = p.invf[l];
-        const int hi = ((pm + 1) >> 1) - 1, lo = -(pm >> 1);
-        const int w0 = p.wb[l][0], w1 = p.wb[l][1], c64 = p.c64[l];
-        uint32_t wr = 0, wi = 0, wn = 0;
+        const uint32_t bm = p.bm[l];
+        const int lo = -(pm >> 1), hi = ((pm + 1) >> 1) - 1;
+        const int w0 = p.wb[l][0], w1 = p.wb[l][1], o0 = p.off0[l], c64 = p.c64[l];
+        int rr[4], ri[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          int vr = dp4a_us(hi_r[e], w1, dp4a_us(lo_r[e], w0, 0)) - (ng_r[e] ? c64 : 0);
-          int vi = dp4a_us(hi_i[e], w1, dp4a_us(lo_i[e], w0, 0)) - (ng_i[e] ? c64 : 0);
-          int rr = vr - __float2int_rn((float)vr * inv) * pm;  // |v| < 2^19: float exact
-          int ri = vi - __float2int_rn((float)vi * inv) * pm;
-          rr = rr > hi ? rr - pm : (rr < lo ? rr + pm : rr);
-          ri = ri > hi ? ri - pm : (ri < lo ? ri + pm : ri);
-          int rn = -ri;
-          rn = rn > hi ? rn - pm : rn;
-          wr |= ((uint32_t)rr & 0xFFu) << (8 * e);
-          wi |= ((uint32_t)ri & 0xFFu) << (8 * e);
-          wn |= ((uint32_t)rn & 0xFFu) << (8 * e);
+          // v = byte dot products + a positive multiple of p - lo (- 2^64 mod p when
+          // negative): 0 <= v < 2^20; u = v mod p by Barrett, r = u + lo symmetric
+          const int vr = dp4a_us(hi_r[e], w1, dp4a_us(lo_r[e], w0, o0 - (int)ng_r[e] * c64));
+          const int vi = dp4a_us(hi_i[e], w1, dp4a_us(lo_i[e], w0, o0 - (int)ng_i[e] * c64));
+          int a = vr - (int)__umulhi((uint32_t)vr, bm) * pm;  // in [-p, p)
+          int b = vi - (int)__umulhi((uint32_t)vi, bm) * pm;
+          a = a - (a >> 31) * pm + lo;  // [0, p) + lo
+          b = b - (b >> 31) * pm + lo;
+          rr[e] = a;
+          ri[e] = b;
+        }
+        // pack the four low bytes per plane (two byte permutes each)
+        const uint32_t wr = __byte_perm(__byte_perm(rr[0], rr[1], 0x0040), __byte_perm(rr[2], rr[3], 0x0040), 0x5410);
+        const uint32_t wi = __byte_perm(__byte_perm(ri[0], ri[1], 0x0040), __byte_perm(ri[2], ri[3], 0x0040), 0x5410);
+        uint32_t wn = 0;
+        if (need_neg) {
+          int rn[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) rn[e] = -ri[e] > hi ? -ri[e] - pm : -ri[e];
+          wn = __byte_perm(__byte_perm(rn[0], rn[1], 0x0040), __byte_perm(rn[2], rn[3], 0x0040), 0x5410);
         }
         store_planes(p, dst, l, mod_stride, mod_stride2, plane_stride, i, k, wr, wi, wn);
       }
@@ -630,6 +642,10 @@ int encode_launch(int rows_out, int K, int kind, const void* re, const double* i
     p.wb[l][0] = (int)words[0];
     p.wb[l][1] = (int)words[1];
     p.c64[l] = (int)sym(pb);  // after 8 steps pb = 2^64 mod m
+    p.bm[l] = (uint32_t)((1ull << 32) / (unsigned long long)m + 1);
+    const int shift = (8 * 255 * 128 + 256 + m - 1) / m * m;  // > |byte dot products| + |2^64 mod m|
+    p.off0[l] = shift + (m >> 1);  // + (-lo): the residue comes out in [0, m), then shifted by lo
+    p.off1[l] = 0;
   }
   // K padding columns of the residue planes must read as zero
   const int planes = layout == 0 || layout == 3 ? 2 : (layout == 1 ? 3 : 1);

@@ -32,7 +32,8 @@
 namespace {
 
 constexpr int TM = 128, TN = 128, TK = 64;  // tile: 128 rows x 128 cols, 64-byte k blocks
-constexpr int STAGES = 5;
+constexpr int MAX_STAGES = 8;                 // ring slots (complex: 5 x 40 KB, real: 8 x 24 KB)
+constexpr int SMEM_RING = 200 * 1024;
 constexpr int PLANE_BYTES = TM * TK;        // 8 KB per 128-row, 64-byte plane
 constexpr int NUM_THREADS = 192;
 constexpr int GROUP_M = 8;  // M-tiles per rasterisation group (measured best with 2-CTA clusters)
@@ -44,6 +45,8 @@ struct OzParams {
   int tiles_m, tiles_n;
   int lower_only;               // Hermitian product: only tiles with nt <= mt
   int group_m;                  // work units per rasterisation group (L2 reuse of the A panel)
+  int real;                     // real x real product, 256-column tiles, one N = 256 MMA per k-step
+  int stages;                   // ring slots in use
   long long out_pitch;          // bytes between output rows
   long long out_plane;          // bytes between output planes (re / im)
   long long out_mod;            // bytes between moduli
@@ -104,17 +107,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int a_bytes = p.a_planes * PLANE_BYTES;
-  const int b_bytes = p.b_planes * PLANE_BYTES;
+  const int b_bytes = (p.real ? 2 : p.b_planes) * PLANE_BYTES;  // real: one 256-row B plane
   const int stage_bytes = a_bytes + b_bytes;
-  uint64_t* bars = (uint64_t*)(smem + STAGES * stage_bytes);
-  // bars: full[STAGES], empty[STAGES], tfull[2], tempty[2]; then tmem base slot
-  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
+  const int STAGES = p.stages;
+  const int tn = p.real ? 2 * TN : TN;
+  uint64_t* bars = (uint64_t*)(smem + SMEM_RING);
+  // bars: full[MAX_STAGES], empty[MAX_STAGES], tfull[2], tempty[2]; then tmem base slot
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * MAX_STAGES + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
-  auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
-  auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * STAGES + b); };
-  auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * STAGES + 2 + b); };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (MAX_STAGES + s); };
+  auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * MAX_STAGES + b); };
+  auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * MAX_STAGES + 2 + b); };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -169,12 +174,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_expect_tx(full_bar(stage), stage_bytes);
           tma_load_4d(smem_u32(st), &tmap_a, full_bar(stage), kb * TK, mt * TM, 0, l);
           if (CM == 1) {
-            tma_load_4d(smem_u32(st + a_bytes), &tmap_b, full_bar(stage), kb * TK, nt * TN, 0, l);
+            tma_load_4d(smem_u32(st + a_bytes), &tmap_b, full_bar(stage), kb * TK, nt * tn, 0, l);
+          } else if (p.real) {
+            // this CTA's 128 of the tile's 256 B rows, multicast to the pair
+            tma_load_4d_mc(smem_u32(st + a_bytes + crank * (2 * PLANE_BYTES / CM)), &tmap_b, full_bar(stage),
+                           kb * TK, nt * tn + crank * (tn / CM), 0, l, (uint16_t)((1 << CM) - 1));
           } else {
             // this CTA's half of every B plane, multicast to the pair
             for (int pl = 0; pl < p.b_planes; ++pl)
-              tma_load_4d_mc(smem_u32(st + a_bytes + pl * PLANE_BYTES + crank * (PLANE_BYTES / 2)), &tmap_b,
-                             full_bar(stage), kb * TK, nt * TN + crank * (TN / 2), pl, l, (uint16_t)0x3);
+              tma_load_4d_mc(smem_u32(st + a_bytes + pl * PLANE_BYTES + crank * (PLANE_BYTES / CM)), &tmap_b,
+                             full_bar(stage), kb * TK, nt * TN + crank * (TN / CM), pl, l, (uint16_t)((1 << CM) - 1));
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -209,8 +218,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int ks = 0; ks < TK / 32; ++ks) {
             const uint32_t acc_flag = (kb | ks) != 0;
             const uint64_t are = umma_desc_sw64(sa + ks * 32);
-            const uint64_t aim = umma_desc_sw64(sa + PLANE_BYTES + ks * 32);
-            if (cplx) {
+            const uint64_t aim = umma_desc_sw64(sa + (p.real ? 0 : PLANE_BYTES) + ks * 32);
+            if (p.real) {
+              umma_i8(d, are, umma_desc_sw64(sb + ks * 32), id256, acc_flag);
+            } else if (cplx) {
               const uint64_t b1 = umma_desc_sw64(sb + PLANE_BYTES + ks * 32);  // [B_re | B_im]
               const uint64_t b2 = umma_desc_sw64(sb + ks * 32);                // [-B_im | B_re]
               umma_i8(d, are, b1, id256, acc_flag);
@@ -224,7 +235,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (CM == 1)
             umma_commit(empty_bar(stage));
           else
-            umma_commit_mc(empty_bar(stage), (uint16_t)0x3);  // release the slot in both CTAs
+            umma_commit_mc(empty_bar(stage), (uint16_t)((1 << CM) - 1));  // release the slot in every CTA
           if (kb == kblocks - 1) umma_commit(tfull_bar(acc));
         }
         __syncwarp();
@@ -255,8 +266,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t v[16];
         tmem_ld16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * 256 + chunk * 16), v);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        const int plane = chunk >> 3;
-        const int col0 = nt * TN + (chunk & 7) * 16;
+        const int plane = p.real ? 0 : chunk >> 3;
+        const int col0 = nt * tn + (p.real ? chunk : (chunk & 7)) * 16;
         uint32_t packed[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -318,18 +329,27 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
   if (((uintptr_t)a | (uintptr_t)b | (uintptr_t)out) & 15) return SR_EINVAL;
   OzParams p;
   memset(&p, 0, sizeof(p));
-  p.M = M;
+  // complex x real: [C_re; C_im] = [A_re; A_im] B^T is one real product with
+  // 2M stacked rows (the A planes and the output planes are stacked row blocks)
+  const bool real = (b_planes == 1 && !lower_only && !getenv("SR_OZ_NO_REAL"));
+  p.M = real ? 2 * M : M;
   p.N = N;
   p.K = K;
   p.nmod = nmod;
-  p.a_planes = a_planes;
+  p.real = real ? 1 : 0;
+  p.a_planes = real ? 1 : a_planes;
   p.b_planes = b_planes;
-  p.tiles_m = (M + TM - 1) / TM;
-  p.tiles_n = (N + TN - 1) / TN;
+  p.tiles_m = (p.M + TM - 1) / TM;
+  p.tiles_n = (N + (real ? 2 * TN : TN) - 1) / (real ? 2 * TN : TN);
   p.lower_only = lower_only;
   p.out_pitch = out_pitch;
   p.out_plane = out_pitch * M;
-  p.out_mod = p.out_plane * 2;
+  p.out_mod = out_pitch * M * 2;
+  {
+    const int stage_bytes = (p.a_planes + (real ? 2 : b_planes)) * PLANE_BYTES;
+    p.stages = SMEM_RING / stage_bytes;
+    if (p.stages > MAX_STAGES) p.stages = MAX_STAGES;
+  }
   for (int i = 0; i < nmod; ++i) {
     if (moduli[i] < 3 || moduli[i] > 256) return SR_EINVAL;
     p.moduli[i] = moduli[i];
@@ -338,7 +358,10 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
   const int tiles = nmod * p.tiles_m * p.tiles_n;
   int grid = num_sms > 0 ? num_sms : 148;
   // clusters of two CTAs sharing the B tile whenever there are M-tile pairs to share
-  const int cm = (p.tiles_m >= 2 && grid >= 2 && !getenv("SR_OZ_NO_CLUSTER")) ? 2 : 1;
+  int cm = (p.tiles_m >= 2 && grid >= 2 && !getenv("SR_OZ_NO_CLUSTER")) ? 2 : 1;
+  if (getenv("SR_OZ_CM")) cm = atoi(getenv("SR_OZ_CM"));
+  if (cm != 1 && cm != 2 && cm != 4) cm = 2;
+  if (p.tiles_m < cm) cm = 1;
   // 16 M-tiles (a 2 x 128 x K byte A panel each) per group keep the panel
   // inside one die's half of the L2 while every N-tile streams past it
   p.group_m = (getenv("SR_OZ_GROUP_M") ? atoi(getenv("SR_OZ_GROUP_M")) : GROUP_M) / cm;
@@ -347,15 +370,16 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
   grid -= grid % cm;
   if (grid < cm) grid = cm;
   CUtensorMap ma, mb;
-  if (make_map(&ma, a, K, M, a_planes, nmod, a_kpitch, TM, a_planes) != SR_OK)
+  if (make_map(&ma, a, K, p.M, p.a_planes, nmod, a_kpitch, TM, p.a_planes) != SR_OK)
     return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(A)");
-  if (make_map(&mb, b, K, N, b_planes, nmod, b_kpitch, TN / cm, cm == 1 ? b_planes : 1) != SR_OK)
+  if (make_map(&mb, b, K, N, b_planes, nmod, b_kpitch, (real ? 2 * TN : TN) / cm, cm == 1 ? b_planes : 1) != SR_OK)
     return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(B)");
-  const size_t smem = 1024 + (size_t)STAGES * (a_planes + b_planes) * PLANE_BYTES + 256;
+  const size_t smem = 1024 + (size_t)SMEM_RING + 256;
   static bool configured = false;
   if (!configured) {
     SR_CUDA_CHECK(cudaFuncSetAttribute(oz_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     SR_CUDA_CHECK(cudaFuncSetAttribute(oz_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    SR_CUDA_CHECK(cudaFuncSetAttribute(oz_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
   cudaLaunchConfig_t cfg;
@@ -371,7 +395,15 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  if (cm == 2)
+  if (cm == 4) {
+    // persistent clusters: never more than can be co-resident
+    int ncl = 0;
+    cfg.gridDim = dim3(cm);
+    SR_CUDA_CHECK(cudaOccupancyMaxActiveClusters(&ncl, oz_gemm_kernel<4>, &cfg));
+    if (ncl > 0 && ncl * cm < grid) grid = ncl * cm;
+    cfg.gridDim = dim3(grid);
+    SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<4>, ma, mb, p, (int8_t*)out));
+  } else if (cm == 2)
     SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<2>, ma, mb, p, (int8_t*)out));
   else
     SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<1>, ma, mb, p, (int8_t*)out));

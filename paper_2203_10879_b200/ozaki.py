@@ -153,6 +153,22 @@ def encode(x, rows, cols, role, pl, conj_t=False, out=None):
     return enc
 
 
+LP_MIN_BETA = 8  # floor for the magnitude-adaptive lp products (4 moduli at K = 8192)
+
+
+def lp_product_beta(scale, n, hi=LP_BETA, lo=LP_MIN_BETA, slack_bits=26):
+    """Operand precision for an lp product whose absolute error only has to
+    stay below the lp solve's own error in W (>= u32 ||W||_F): truncating both
+    operands of X Y to beta bits per row / column changes the product by
+    <= 2 sqrt(n) 2^-beta ||X||_F ||Y||_F, so with scale = ||X||_F ||Y||_F /
+    ||W||_F (the error allowed, in units of 2^-slack_bits ||W||_F) beta =
+    slack_bits + 1 + log2(n)/2 + log2(scale).  Clamped to [lo, hi]."""
+    if not (scale > 0.0) or not math.isfinite(scale):
+        return hi if not (scale == 0.0) else lo
+    b = slack_bits + 1 + math.ceil(0.5 * math.log2(max(n, 2))) + math.ceil(math.log2(scale))
+    return max(lo, min(hi, b))
+
+
 def correction_beta(bound, n, hi=HP_BETA, lo=LP_BETA, unit_bits=53):
     """Operand precision for a correction product X S whose result is added to
     an O(1) matrix before one rounding (Q + Q S'/2, Q^ - Q^ (G - I)/2):

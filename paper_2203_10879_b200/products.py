@@ -65,7 +65,7 @@ class DmmaProducts:
         matmul_hp(ws.p, ws.q, out=ws.that)
         matmul_hp(ws.q, ws.q, trans_a=True, diag_shift=-1.0, out=ws.y)
 
-    def update(self, restore_full_sigma, sigma_bound=None):
+    def update(self, restore_full_sigma, sigma_bound=None, norm_y=None, norm_w=None):
         ws = self.ws
         n = ws.n
         _downcast_y(ws)
@@ -111,8 +111,11 @@ class OzakiProducts:
         _counters["hp_calls"] += 1
 
     def _lp(self, ea, eb, out, hermitian=False):
-        ozaki.gemm_residues(ea, eb, self.lp, self.lres, lower_only=bool(hermitian))
-        ozaki.decode(self.lres, ea, eb, self.lp, out, hermitian=hermitian)
+        self._lp_with(self.lp, ea, eb, out, hermitian)
+
+    def _lp_with(self, pl, ea, eb, out, hermitian=False):
+        ozaki.gemm_residues(ea, eb, pl, self.lres, lower_only=bool(hermitian))
+        ozaki.decode(self.lres, ea, eb, pl, out, hermitian=hermitian)
         _counters["lp_calls"] += 1
 
     def _correction_plan(self, bound):
@@ -144,19 +147,38 @@ class OzakiProducts:
         self._hp(self.ea_x, self.eb_q, ws.that)                          # T^ = P Q
         self._hp(self.ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True)  # Y = Q^H Q - I
 
-    def update(self, restore_full_sigma, sigma_bound=None):
+    def _lp_plans(self, norm_y, norm_w):
+        """Plans for the fused update's W^2 and X W (X = Y - W - W^2) from
+        ||Y||_F, ||W||_F: the products only enter S' multiplied by W (W^2,
+        through X W) or as X W itself, so their allowed absolute error is the
+        lp solve's own error in W (ozaki.lp_product_beta)."""
+        lp, n = self.lp, self.ws.n
+        if norm_y is None or norm_w is None or not (norm_w > 0.0):
+            return lp, lp
+        nx = norm_y + norm_w + norm_w * norm_w
+        b_w2 = ozaki.lp_product_beta(norm_w * norm_w, n)      # W^2 error x ||W|| vs u ||W||
+        b_xw = ozaki.lp_product_beta(nx, n)                   # (X W) error vs u ||W||
+        return ozaki.plan(n, b_w2, b_w2), ozaki.plan(n, b_xw, b_xw)
+
+    def update(self, restore_full_sigma, sigma_bound=None, norm_y=None, norm_w=None):
         ws, hp, lp, n = self.ws, self.hp, self.lp, self.ws.n
-        ozaki.encode(ws.w_lp, n, n, "b", lp, out=self.lb)                # W, B role (all lp products)
-        ozaki.encode(ws.w_lp, n, n, "a", lp, out=self.la)
-        self._lp(self.la, self.lb, ws.w2, hermitian=True)                # W^2 (W skew-Hermitian)
         if not restore_full_sigma:
+            p_w2, p_xw = self._lp_plans(norm_y, norm_w)
             # two lp products instead of three: X W = YW - W^2 - W^3 with X = Y - W - W^2
+            ozaki.encode(ws.w_lp, n, n, "b", p_w2, out=self.lb)           # W, B role
+            ozaki.encode(ws.w_lp, n, n, "a", p_w2, out=self.la)
+            self._lp_with(p_w2, self.la, self.lb, ws.w2, hermitian=True)  # W^2 (W skew-Hermitian)
             _lib.call("sr_fused_lp_operand_c64", n, ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld, ws.w_lp.data_ptr(),
                       ws.w2.data_ptr(), ws.w_lp.shape[1], ws.y_lp.data_ptr(), _stream())
-            ozaki.encode(ws.y_lp, n, n, "a", lp, out=self.la)
-            self._lp(self.la, self.lb, ws.yw)                            # X W
+            if p_xw is not p_w2:
+                ozaki.encode(ws.w_lp, n, n, "b", p_xw, out=self.lb)
+            ozaki.encode(ws.y_lp, n, n, "a", p_xw, out=self.la)
+            self._lp_with(p_xw, self.la, self.lb, ws.yw)                 # X W
             _sigma(ws, False, False, fused=True)                         # S' = S - 2I
         else:
+            ozaki.encode(ws.w_lp, n, n, "b", lp, out=self.lb)            # W, B role (all lp products)
+            ozaki.encode(ws.w_lp, n, n, "a", lp, out=self.la)
+            self._lp(self.la, self.lb, ws.w2, hermitian=True)            # W^2 (W skew-Hermitian)
             _downcast_y(ws)
             ozaki.encode(ws.w2, n, n, "a", lp, out=self.la)
             self._lp(self.la, self.lb, ws.w3, hermitian="skew")          # W^3

@@ -367,7 +367,8 @@ def _run_fp64(a, qhat, cfg, ws, symmetric=False, host=None):
                 and norm_w <= math.sqrt(U_FP64))
         if not skip:
             prod.update(cfg.restore_full_sigma,
-                        sigma_bound=products.sigma_prime_bound(norm_y, norm_w, cfg.restore_full_sigma))
+                        sigma_bound=products.sigma_prime_bound(norm_y, norm_w, cfg.restore_full_sigma),
+                        norm_y=norm_y, norm_w=norm_w)
             q_version += 1
             _mark("update")
         if converged:

@@ -36,7 +36,7 @@ def run(tag, a, b, out, beta):
             for i in range(4):
                 times[i].append(ev[i].elapsed_time(ev[i + 1]))
     t = [statistics.median(x) for x in times]
-    ops = 2.0 * 4 * pl.nmod * n ** 3
+    ops = 2.0 * (2 if eb.planes == 1 else 4) * pl.nmod * n ** 3
     print("%s n=%d nmod=%d: encA %.3f encB %.3f gemm %.3f (%.0f TOP/s) decode %.3f ms; total %.3f ms" % (
         tag, n, pl.nmod, t[0], t[1], t[2], ops / t[2] / 1e9, t[3], sum(t)), flush=True)
 
@@ -44,6 +44,7 @@ def run(tag, a, b, out, beta):
 a = ZPlanar.from_any(torch.randn(n, n, dtype=torch.complex128))
 b = ZPlanar.from_any(torch.randn(n, n, dtype=torch.complex128))
 run("hp", a, b, ZPlanar.empty(n), ozaki.HP_BETA)
+run("hp-realB", a, ZPlanar.from_any(torch.randn(n, n, dtype=torch.float64)), ZPlanar.empty(n), ozaki.HP_BETA)
 al, bl, ol = lp_empty(n), lp_empty(n), lp_empty(n)
 al[:, :n] = torch.randn(n, n, dtype=torch.complex64)
 bl[:, :n] = torch.randn(n, n, dtype=torch.complex64)

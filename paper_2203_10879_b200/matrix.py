@@ -51,10 +51,21 @@ class ZPlanar:
         rows, cols = x.shape
         real = not (x.is_complex() or force_complex)
         m = cls.empty(rows, cols, device=device, real=real)
+        return cls.fill_from(m, x)
+
+    @staticmethod
+    def fill_from(m, x):
+        """Copy a (rows, cols) torch matrix into the planes of m (on the current stream)."""
+        device = m.re_buf.device
+        cols = x.shape[1]
         if x.is_complex():
             xd = x.to(device=device, dtype=torch.complex128, non_blocking=True)
             m.re_buf[:, :cols].copy_(xd.real)
             m.im_buf[:, :cols].copy_(xd.imag)
+        elif x.dtype == torch.float64:
+            m.re_buf[:, :cols].copy_(x, non_blocking=True)
+            if m.im_buf is not None:
+                m.im_buf.zero_()
         else:
             m.re_buf[:, :cols].copy_(x.to(device=device, dtype=torch.float64, non_blocking=True))
             if m.im_buf is not None:
@@ -87,9 +98,11 @@ class ZPlanar:
     def im_ptr(self):
         return None if self.im_buf is None else self.im_buf.data_ptr()
 
-    def to_complex(self):
-        """complex128 (rows, cols) torch tensor on the same device."""
+    def to_complex(self, out=None):
+        """complex128 (rows, cols) torch tensor on the same device (into out when given)."""
         im = self.im if self.im is not None else torch.zeros_like(self.re)
+        if out is not None:
+            return torch.complex(self.re, im, out=out)
         return torch.complex(self.re.contiguous(), im.contiguous())
 
     def to_numpy(self):

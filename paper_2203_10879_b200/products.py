@@ -102,8 +102,10 @@ class OzakiProducts:
         self.la = ozaki.Encoded(n, n, 2, lp.beta_a, lp.nmod, dev)      # Y_lp / W / W^2, A role
         self.lb = ozaki.Encoded(n, n, 3, lp.beta_b, lp.nmod, dev)      # W, B role
         self.lres = ozaki.ResidueBuffer(n, n, lp.nmod, dev)
-        # the constant matrix A, B role (real A keeps one plane)
-        self.eb_a = ozaki.encode(a, n, n, "b", hp)
+        # the constant matrix A, B role (real A keeps one plane), encoded at the
+        # first measurement so an asynchronous upload of A overlaps the entry step
+        self.a = a
+        self.eb_a = None
 
     def _hp(self, ea, eb, out, hermitian=False, **kw):
         ozaki.gemm_residues(ea, eb, self.hp, self.res, lower_only=hermitian)
@@ -142,6 +144,8 @@ class OzakiProducts:
     def measure(self, a):
         ws, hp, n = self.ws, self.hp, self.ws.n
         ozaki.encode_dual(ws.q, n, n, hp, self.ea_qh, self.eb_q)          # Q^H (A role), Q (B role)
+        if self.eb_a is None:
+            self.eb_a = ozaki.encode(self.a, n, n, "b", hp)
         self._hp(self.ea_qh, self.eb_a, ws.p)                            # P = Q^H A
         ozaki.encode(ws.p, n, n, "a", hp, out=self.ea_x)
         self._hp(self.ea_x, self.eb_q, ws.that)                          # T^ = P Q

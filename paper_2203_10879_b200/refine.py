@@ -134,6 +134,16 @@ class _Fp64Workspace:
         red = _lib.load().sr_reduce_workspace_bytes()
         self.red = [torch.zeros(red, dtype=torch.uint8, device=device) for _ in range(4)]
         self.solver = SolverWorkspace(n, torch.complex64, device)
+        self.staging = None
+        self.device = device
+
+    def host_staging(self):
+        """Interleaved complex128 device staging buffers for Q and T when the
+        result goes to host tensors (allocated on first use)."""
+        if self.staging is None:
+            self.staging = tuple(torch.empty((self.n, self.n), dtype=torch.complex128, device=self.device)
+                                 for _ in range(2))
+        return self.staging
 
     def ptr(self, i):
         return self.scal.data_ptr() + 8 * i
@@ -168,7 +178,46 @@ def _coerce(x, device):
     return m
 
 
-def _newton_schulz_entry(qhat, ws, prod):
+def _is_host_matrix(x):
+    return isinstance(x, np.ndarray) or (isinstance(x, torch.Tensor) and x.device.type == "cpu")
+
+
+class _AsyncUpload:
+    """A host matrix copied to the device on a side stream, so the copy
+    overlaps the entry step (A is first needed by the first measurement);
+    the finiteness check (_coerce_hp, refine.py:341-350) is evaluated on the
+    device and raised as soon as A is needed."""
+
+    def __init__(self, x, device):
+        if isinstance(x, np.ndarray):
+            if x.ndim != 2:
+                raise ValueError("expected a 2-d array")
+            x = torch.from_numpy(np.ascontiguousarray(x))
+        if x.dim() != 2:
+            raise ValueError("expected a 2-d array")
+        rows, cols = x.shape
+        if rows != cols:
+            raise ValueError("refinement needs a square matrix")
+        main = torch.cuda.current_stream(device)
+        self.m = ZPlanar.empty(rows, cols, device=device, real=not x.is_complex())  # allocated on main
+        self.stream = torch.cuda.Stream(device=device)
+        self.stream.wait_stream(main)
+        with torch.cuda.stream(self.stream):
+            ZPlanar.fill_from(self.m, x)
+            fin = torch.isfinite(self.m.re).all()
+            if self.m.im is not None:
+                fin = fin & torch.isfinite(self.m.im).all()
+            self.fin = fin
+            self.ready = torch.cuda.Event()
+            self.ready.record(self.stream)
+        self.host = x  # pinned source stays alive until the copy has run
+
+    def check(self):
+        if not bool(self.fin):
+            raise ValueError("input matrix has non-finite entries")
+
+
+def _newton_schulz_entry(qhat, ws, prod, a_upload=None):
     """newton_schulz_step (orthogonal.py:153-169): guard ||Q^||_2 < sqrt(3)
     by lp power iteration, then Q = Q^ (3I - Q^H Q^) / 2 in hp."""
     n = ws.n
@@ -176,6 +225,8 @@ def _newton_schulz_entry(qhat, ws, prod):
               ws.y_lp.shape[1], _stream())
     est = spectral_norm_estimate(ws.y_lp, n)
     if not est < math.sqrt(3.0):
+        if a_upload is not None:  # the reference validates A before the entry step
+            a_upload.check()
         raise NormTooLarge("spectral norm estimate %.6f is not below sqrt(3)" % est)
     prod.entry(qhat)
 
@@ -227,24 +278,25 @@ class _HostResult:
     whenever the loop ends without a further update (convergence with the
     skip rule, the config-3 case) — and T is copied at the end."""
 
-    def __init__(self, n, device, q_host, t_host):
+    def __init__(self, n, device, q_host, t_host, bufs):
         for h in (q_host, t_host):
             if not (isinstance(h, torch.Tensor) and h.device.type == "cpu" and h.dtype == torch.complex128
                     and tuple(h.shape) == (n, n) and h.is_contiguous()):
                 raise ValueError("out must be two contiguous (n, n) complex128 CPU tensors")
         self.n = n
         self.stream = torch.cuda.Stream(device=device)
-        self.buf = torch.empty((n, n), dtype=torch.complex128, device=device)
+        self.buf, self.tbuf = bufs  # device staging for Q and T (kept in the workspace)
         self.done = torch.cuda.Event()
         self.q_host, self.t_host = q_host, t_host
         self.copied_version = -1
         self.started = False
+        self.t_copied = False
 
     def copy_q(self, q, version):
         main = torch.cuda.current_stream()
         if self.started:
             main.wait_event(self.done)  # the previous D2H has left buf
-        self.buf.copy_(q.to_complex())
+        q.to_complex(out=self.buf)
         ready = torch.cuda.Event()
         ready.record(main)
         self.stream.wait_event(ready)
@@ -254,16 +306,34 @@ class _HostResult:
         self.started = True
         self.copied_version = version
 
+    def copy_t(self, t):
+        t.to_complex(out=self.tbuf)
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream())
+        self.stream.wait_event(ready)
+        with torch.cuda.stream(self.stream):
+            self.t_host.copy_(self.tbuf, non_blocking=True)
+            self.done.record(self.stream)
+        self.t_copied = True
+
     def finish(self, q, version, t):
         if self.copied_version != version:
             self.copy_q(q, version)
-        self.t_host.copy_(t.to_complex(), non_blocking=True)
+        if not self.t_copied:
+            self.t_host.copy_(t.to_complex(out=self.tbuf), non_blocking=True)
         self.done.synchronize()
         torch.cuda.current_stream().synchronize()
         return self.q_host, self.t_host
 
 
-def _run_fp64(a, qhat, cfg, ws, symmetric=False, host=None):
+def _finalize_t(ws, symmetric, st):
+    """T = triu(T^) in place (real diagonal parts only when symmetric); idempotent."""
+    _lib.call("sr_triu_inplace_f64", ws.n, ws.that.re_ptr(), ws.that.im_ptr(), ws.that.ld, st)
+    if symmetric:  # T keeps its real parts (refine.py:435-436)
+        ws.that.im.zero_()
+
+
+def _run_fp64(a, qhat, cfg, ws, symmetric=False, host=None, a_upload=None):
     """_run (refine.py:223-329) with hp = FP64, lp = complex64.  symmetric
     (refine_symmetric): the defect is the full off-diagonal part of Q^H A Q
     and the solve is the entrywise diagonal correction."""
@@ -275,8 +345,11 @@ def _run_fp64(a, qhat, cfg, ws, symmetric=False, host=None):
     if cfg.restore_full_sigma:
         products.ensure_full_sigma_buffers(ws)
     _mark("setup")
-    _newton_schulz_entry(qhat, ws, prod)
+    _newton_schulz_entry(qhat, ws, prod, a_upload)
     _mark("entry")
+    if a_upload is not None:  # A's host->device copy ran on a side stream during the entry
+        torch.cuda.current_stream().wait_event(a_upload.ready)
+        a_upload.check()
     _lib.call("sr_fro_norm_f64", n, n, a.re_ptr(), a.im_ptr(), a.ld, ws.ptr(0), ws.red[0].data_ptr(),
               ws.red[0].numel(), st)
     history = []
@@ -335,6 +408,10 @@ def _run_fp64(a, qhat, cfg, ws, symmetric=False, host=None):
                 detail += "; " + _CLIP_HINT
             break
         converged = norm_e <= tol
+        if converged and host is not None:
+            # this measurement's T is the result: its device->host copy overlaps the solve
+            _finalize_t(ws, symmetric, st)
+            host.copy_t(ws.that)
         # lp solve + W = L - L^H + ||W|| + finiteness
         ws.solver.clipped.zero_()
         ws.solver.flags.zero_()
@@ -381,9 +458,7 @@ def _run_fp64(a, qhat, cfg, ws, symmetric=False, host=None):
         if streak >= DIVERGENCE_STREAK:
             status, iterations = RefineStatus.DIVERGED, it
             break
-    _lib.call("sr_triu_inplace_f64", n, ws.that.re_ptr(), ws.that.im_ptr(), ws.that.ld, st)
-    if symmetric:  # T keeps its real parts (refine.py:435-436)
-        ws.that.im.zero_()
+    _finalize_t(ws, symmetric, st)
     last_e, last_y = history[-1]
     if host is not None:
         q_out, t_out = host.finish(ws.q, q_version, ws.that)
@@ -443,16 +518,21 @@ def refine_template(a, qhat, cfg=None, device=None, out=None):
         torch.cuda.current_stream().synchronize()
         report.wall_time = time.perf_counter() - t0
         return pair, report
-    a = _coerce(a, device)
     qhat = _coerce(qhat, device)
+    a_upload = None
+    if _is_host_matrix(a):
+        a_upload = _AsyncUpload(a, device)
+        a = a_upload.m
+    else:
+        a = _coerce(a, device)
     if a.shape != qhat.shape:
         raise ValueError("matrix and candidate shapes differ")
     if qhat.is_real:
         qhat = ZPlanar.from_any(qhat.re, device=device, force_complex=True)
     if True:
         ws = _workspace(a.rows, device)
-        host = _HostResult(a.rows, device, *out) if out is not None else None
-        pair, report = _run_fp64(a, qhat, cfg, ws, host=host)
+        host = _HostResult(a.rows, device, *out, bufs=ws.host_staging()) if out is not None else None
+        pair, report = _run_fp64(a, qhat, cfg, ws, host=host, a_upload=a_upload)
     torch.cuda.current_stream().synchronize()
     report.wall_time = time.perf_counter() - t0
     return pair, report

@@ -12,7 +12,7 @@ import pytest
 import torch
 
 from oracle.refine_fp64 import refine_template_fp64, residuals_fp64
-from paper_2203_10879_b200 import RefineConfig, RefineStatus, SeparationError, inputs, refine_template
+from paper_2203_10879_b200 import NormTooLarge, RefineConfig, RefineStatus, SeparationError, inputs, refine_template
 
 pytestmark = pytest.mark.gpu
 U = 2.0 ** -53
@@ -116,6 +116,10 @@ def test_exact_candidate_and_errors():
         bad = np.eye(3)
         bad[0, 0] = np.nan
         refine_template(bad, np.eye(3), RefineConfig(precision="fp64"))
+    with pytest.raises(ValueError):  # A is validated before the candidate's norm guard
+        refine_template(bad, 4.0 * np.eye(3), RefineConfig(precision="fp64"))
+    with pytest.raises(NormTooLarge):
+        refine_template(np.eye(3), 4.0 * np.eye(3), RefineConfig(precision="fp64"))
 
 
 def test_seed_determinism():

@@ -59,3 +59,22 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
+
+// Kernel timeline for diagnostics (tools/solve_timeline.py builds with
+// -DSR_TIMELINE): per (kind, slot) the earliest CTA start and the latest CTA
+// end in %globaltimer ns.  Compiled out of the product library.
+#ifdef SR_TIMELINE
+#define SR_TL_DECLARE(name) __device__ unsigned long long name[8][1024][2];
+#define SR_TL_MARK(name, kind, slot, end)                                              \
+  do {                                                                                  \
+    unsigned long long t_;                                                              \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
+    if (end) atomicMax(&name[(kind)][(slot)&1023][1], t_);                              \
+    else atomicMin(&name[(kind)][(slot)&1023][0], t_);                                  \
+  } while (0)
+#else
+#define SR_TL_DECLARE(name)
+#define SR_TL_MARK(name, kind, slot, end) \
+  do {                                    \
+  } while (0)
+#endif

@@ -57,6 +57,8 @@
 
 namespace {
 
+SR_TL_DECLARE(g_tl_solve)  // kinds: 0 SOLVE, 1 NEAR (slot = level)
+
 constexpr int NB = 32;
 constexpr int NT = 128;   // SOLVE / NEAR CTAs: 16 x 8 threads, each a 2 x 4 block of the tile
 constexpr int LD = NB + 1;
@@ -263,6 +265,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SweepArgs p, const C* __restr
   const bool has_col = lev >= 1 && M <= lev - 1;
   const bool has_row = lev >= 1 && I >= N - lev;
   const int tid = threadIdx.x;
+  if (tid == 0) SR_TL_MARK(g_tl_solve, 0, lev, 0);
   load_tile_async(sR, Rn, ld, I * NB, M * NB, n);
   load_tile_async(sRf, Rf, ld, I * NB, M * NB, n);
   if (has_col) {
@@ -325,6 +328,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(SweepArgs p, const C* __restr
   }
   nclip = __reduce_add_sync(0xffffffffu, nclip);
   if (tid == 0 && nclip) atomicAdd(clipped, (unsigned long long)nclip);
+  if (tid == 0) SR_TL_MARK(g_tl_solve, 0, lev, 1);
 }
 
 // NEAR launch of level `lev` (sources: the tiles solved at level lev-1): one
@@ -349,6 +353,7 @@ __global__ void __launch_bounds__(NT) near_kernel(SweepArgs p, const C* __restri
   const bool has_row = I >= N - lev;   // source (I, J), J = I - N + lev
   if (!has_col && !has_row) return;
   const int tid = threadIdx.x;
+  if (tid == 0) SR_TL_MARK(g_tl_solve, 1, lev, 0);
   load_tile_async(s0, Rn, ld, I * NB, M * NB, n);
   if (has_col) {
     const int K = M + N - lev;
@@ -378,6 +383,7 @@ __global__ void __launch_bounds__(NT) near_kernel(SweepArgs p, const C* __restri
       const int gi = I * NB + 2 * ty + a, gj = M * NB + 4 * tx + c;
       if (gi < n && gj < n) Rn[(size_t)gi * ld + gj] = acc[a][c];
     }
+  if (tid == 0) SR_TL_MARK(g_tl_solve, 1, lev, 1);
 }
 
 struct FarArgs {
@@ -756,6 +762,18 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
 }
 
 }  // namespace
+
+#ifdef SR_TIMELINE
+extern "C" int sr_timeline_solve(void* host, int reset) {
+  if (reset) {
+    static unsigned long long init[8][1024][2];
+    for (int k = 0; k < 8; ++k)
+      for (int s = 0; s < 1024; ++s) init[k][s][0] = ~0ull, init[k][s][1] = 0;
+    return cudaMemcpyToSymbol(g_tl_solve, init, sizeof(init)) == cudaSuccess ? 0 : 4;
+  }
+  return cudaMemcpyFromSymbol(host, g_tl_solve, sizeof(g_tl_solve)) == cudaSuccess ? 0 : 4;
+}
+#endif
 
 extern "C" size_t sr_trisolve_workspace_bytes(int n, int lp_is_c64) {
   const size_t elt = lp_is_c64 ? 8 : 16;

@@ -39,6 +39,9 @@
 
 namespace {
 
+SR_TL_DECLARE(g_tl_tc)  // kinds: 2 far COL, 3 far ROW, 4 lforms, 5 lmax (slot = batch)
+
+
 constexpr int NB = 32;
 constexpr int BW = 4;
 constexpr int KB_H = 32;                           // fp16 per 64-byte K block
@@ -129,6 +132,7 @@ __global__ void __launch_bounds__(256) lmax_kernel(int n, int N, int b, const fl
   __shared__ float s[NB][NB + 1];
   const int level = BW * b + blockIdx.y;
   const int M = blockIdx.x;
+  if (threadIdx.x == 0) SR_TL_MARK(g_tl_tc, 5, b, 0);
   if (level > N - 1 || M > level) return;
   const int I = M + N - 1 - level;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -151,6 +155,7 @@ __global__ void __launch_bounds__(256) lmax_kernel(int n, int N, int b, const fl
     for (int c = 0; c < NB; ++c) m = fmaxf(m, s[tx][c]);
     if (I * NB + tx < n) lmax_r[(size_t)blockIdx.y * n + I * NB + tx] = m;
   }
+  if (threadIdx.x == 0) SR_TL_MARK(g_tl_tc, 5, b, 1);
 }
 
 // L forms of the tiles on levels 4b .. 4b+3 (blockIdx.y = level - 4b, blockIdx.x = M)
@@ -162,6 +167,7 @@ __global__ void __launch_bounds__(256) lforms_kernel(int n, int N, int b, const 
   __shared__ int ec[NB], er[NB];
   const int level = BW * b + blockIdx.y;
   const int M = blockIdx.x;
+  if (threadIdx.x == 0) SR_TL_MARK(g_tl_tc, 4, b, 0);
   if (level > N - 1 || M > level) return;
   const int I = M + N - 1 - level;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -191,6 +197,7 @@ __global__ void __launch_bounds__(256) lforms_kernel(int n, int N, int b, const 
       put_h2(lc, plane, (size_t)(2 * R + 1) * P + 2 * K, y, x);
     }
   }
+  if (threadIdx.x == 0) SR_TL_MARK(g_tl_tc, 4, b, 1);
 }
 
 __device__ __forceinline__ constexpr uint32_t idesc_f16(int m, int n) {
@@ -237,6 +244,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const int N = p.N, b = p.b;
   const int units = p.lines * p.strips;
+  if (threadIdx.x == 0) SR_TL_MARK(g_tl_tc, ROW ? 3 : 2, b, 0);
   // unit -> (line, first target t0) and the A / B / K origins of its strip
   auto unit = [&](int u, int& line, int& t0, int& a_row0, int& b_row0, int& k0) {
     line = p.first + u / p.strips;
@@ -407,6 +415,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
                               "r"(TC_TMEM_COLS));
+  if (threadIdx.x == 0) SR_TL_MARK(g_tl_tc, ROW ? 3 : 2, b, 1);
 }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -440,6 +449,18 @@ FormLayout form_layout(int n) {
 }
 
 }  // namespace
+
+#ifdef SR_TIMELINE
+extern "C" int sr_timeline_tc(void* host, int reset) {
+  if (reset) {
+    static unsigned long long init[8][1024][2];
+    for (int k = 0; k < 8; ++k)
+      for (int s = 0; s < 1024; ++s) init[k][s][0] = ~0ull, init[k][s][1] = 0;
+    return cudaMemcpyToSymbol(g_tl_tc, init, sizeof(init)) == cudaSuccess ? 0 : 4;
+  }
+  return cudaMemcpyFromSymbol(host, g_tl_tc, sizeof(g_tl_tc)) == cudaSuccess ? 0 : 4;
+}
+#endif
 
 size_t far_tc_forms_bytes(int n) { return n <= 0 ? 0 : form_layout(n).total; }
 

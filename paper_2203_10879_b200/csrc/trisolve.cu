@@ -60,10 +60,25 @@ namespace {
 SR_TL_DECLARE(g_tl_solve)  // kinds: 0 SOLVE, 1 NEAR (slot = level)
 
 constexpr int NB = 32;
-constexpr int NT = 128;   // SOLVE / NEAR CTAs: 16 x 8 threads, each a 2 x 4 block of the tile
+constexpr int NT = 128;   // NEAR CTAs: 16 x 8 threads, each a 2 x 4 block of the tile
+// SOLVE CTAs: 128 threads, 2 x 4 blocks.  (64 threads with 4 x 4 blocks — a
+// register footprint that co-resides with a far tensor-core CTA — measured
+// slower: 24.8 vs 24.0 ms per n = 8192 solve, 2.69 vs 2.34 ms at n = 2048;
+// kept selectable with -DSR_SOLVE_C64_THREADS=64 for the timeline tool.)
+template <typename C>
+struct SolveShape {
+#ifndef SR_SOLVE_C64_THREADS
+#define SR_SOLVE_C64_THREADS 128
+#endif
+  static constexpr int THREADS = sizeof(C) == 8 ? SR_SOLVE_C64_THREADS : 128;
+  static constexpr int RPT = NB * NB / (4 * THREADS);  // rows per thread (x 4 columns)
+};
 constexpr int LD = NB + 1;
 constexpr int BW = 4;     // levels per far batch = tiles per far strip = source tiles per far update
-constexpr int FAR_LA = 1; // batches of slack: the far updates of batch b target levels >= 4 (b + 1 + FAR_LA)
+#ifndef SR_FAR_LA
+#define SR_FAR_LA 1
+#endif
+constexpr int FAR_LA = SR_FAR_LA;  // batches of slack: the far updates of batch b target levels >= 4 (b + 1 + FAR_LA)
 constexpr int FT = 256;   // FAR CTAs
 
 template <typename C>
@@ -137,9 +152,9 @@ __device__ __forceinline__ void load_block_async(C* s, int pitch, const C* __res
   }
 }
 
-template <typename C>
+template <typename C, int THREADS = NT>
 __device__ __forceinline__ void load_tile_async(C* s, const C* __restrict__ g, long long ld, int r0, int c0, int n) {
-  load_block_async<C>(s, LD, g, ld, r0, c0, NB, NB, n, threadIdx.x, NT);
+  load_block_async<C>(s, LD, g, ld, r0, c0, NB, NB, n, threadIdx.x, THREADS);
 }
 
 struct SweepArgs {
@@ -147,21 +162,24 @@ struct SweepArgs {
   long long ld;
 };
 
-// acc (2 x 4 block of the tile per thread) -= A B (col term) / += A B (row term)
-template <typename C, bool ADD>
-__device__ __forceinline__ void tile_mac(C (&acc)[2][4], const C* sA, const C* sB, int ty, int tx) {
+// acc (RPT x 4 block of the tile per thread: rows RPT ty .., cols 4 tx ..)
+// -= A B (col term) / += A B (row term)
+template <typename C, bool ADD, int RPT = 2>
+__device__ __forceinline__ void tile_mac(C (&acc)[RPT][4], const C* sA, const C* sB, int ty, int tx) {
 #pragma unroll 8
   for (int k = 0; k < NB; ++k) {
-    const C a0 = sA[(2 * ty) * LD + k], a1 = sA[(2 * ty + 1) * LD + k];
+    C a[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) a[r] = sA[(RPT * ty + r) * LD + k];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const C b = sB[k * LD + 4 * tx + c];
-      if (ADD) {
-        cfma(acc[0][c], a0, b);
-        cfma(acc[1][c], a1, b);
-      } else {
-        cfms(acc[0][c], a0, b);
-        cfms(acc[1][c], a1, b);
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        if (ADD)
+          cfma(acc[r][c], a[r], b);
+        else
+          cfms(acc[r][c], a[r], b);
       }
     }
   }
@@ -244,7 +262,7 @@ __device__ __forceinline__ unsigned tile_solve_warp(const C* sT2, const C* sD, c
 // SOLVE launch of level `lev`: one CTA per tile (M + N - 1 - lev, M).  Folds in
 // the level lev-1 sources, adds the two right-hand-side buffers and solves.
 template <typename C>
-__global__ void __launch_bounds__(NT) solve_kernel(SweepArgs p, const C* __restrict__ T, const C* __restrict__ Rn,
+__global__ void __launch_bounds__(SolveShape<C>::THREADS) solve_kernel(SweepArgs p, const C* __restrict__ T, const C* __restrict__ Rn,
                                                    const C* __restrict__ Rf, C* __restrict__ L,
                                                    typename Real<C>::T clip,
                                                    unsigned long long* __restrict__ clipped) {
@@ -266,42 +284,43 @@ __global__ void __launch_bounds__(NT) solve_kernel(SweepArgs p, const C* __restr
   const bool has_row = lev >= 1 && I >= N - lev;
   const int tid = threadIdx.x;
   if (tid == 0) SR_TL_MARK(g_tl_solve, 0, lev, 0);
-  load_tile_async(sR, Rn, ld, I * NB, M * NB, n);
-  load_tile_async(sRf, Rf, ld, I * NB, M * NB, n);
+  load_tile_async<C, SolveShape<C>::THREADS>(sR, Rn, ld, I * NB, M * NB, n);
+  load_tile_async<C, SolveShape<C>::THREADS>(sRf, Rf, ld, I * NB, M * NB, n);
   if (has_col) {
     const int K = M + N - lev;
-    load_tile_async(s1, T, ld, I * NB, K * NB, n);  // T_IK
-    load_tile_async(s2, L, ld, K * NB, M * NB, n);  // L_KM
+    load_tile_async<C, SolveShape<C>::THREADS>(s1, T, ld, I * NB, K * NB, n);  // T_IK
+    load_tile_async<C, SolveShape<C>::THREADS>(s2, L, ld, K * NB, M * NB, n);  // L_KM
   }
   if (has_row) {
     const int J = I - N + lev;
-    load_tile_async(s3, L, ld, I * NB, J * NB, n);  // L_IJ
-    load_tile_async(s4, T, ld, J * NB, M * NB, n);  // T_JM
+    load_tile_async<C, SolveShape<C>::THREADS>(s3, L, ld, I * NB, J * NB, n);  // L_IJ
+    load_tile_async<C, SolveShape<C>::THREADS>(s4, T, ld, J * NB, M * NB, n);  // T_JM
   }
-  load_tile_async(sT2, T, ld, I * NB, I * NB, n);  // T_II
-  load_tile_async(sT1, T, ld, M * NB, M * NB, n);  // T_MM
+  load_tile_async<C, SolveShape<C>::THREADS>(sT2, T, ld, I * NB, I * NB, n);  // T_II
+  load_tile_async<C, SolveShape<C>::THREADS>(sT1, T, ld, M * NB, M * NB, n);  // T_MM
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
   {
-    const int ty = tid / 8, tx = tid % 8;  // rows 2ty..2ty+1, cols 4tx..4tx+3
-    C acc[2][4];
+    constexpr int RPT = SolveShape<C>::RPT;
+    const int ty = tid / 8, tx = tid % 8;  // rows RPT ty .., cols 4tx..4tx+3
+    C acc[RPT][4];
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+    for (int a = 0; a < RPT; ++a)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const int o = (2 * ty + a) * LD + 4 * tx + c;
+        const int o = (RPT * ty + a) * LD + 4 * tx + c;
         acc[a][c].x = sR[o].x + sRf[o].x;
         acc[a][c].y = sR[o].y + sRf[o].y;
       }
-    if (has_col) tile_mac<C, false>(acc, s1, s2, ty, tx);
-    if (has_row) tile_mac<C, true>(acc, s3, s4, ty, tx);
+    if (has_col) tile_mac<C, false, RPT>(acc, s1, s2, ty, tx);
+    if (has_row) tile_mac<C, true, RPT>(acc, s3, s4, ty, tx);
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+    for (int a = 0; a < RPT; ++a)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) sRf[(2 * ty + a) * LD + 4 * tx + c] = acc[a][c];  // sRf is not read again
+      for (int c = 0; c < 4; ++c) sRf[(RPT * ty + a) * LD + 4 * tx + c] = acc[a][c];  // sRf is not read again
     // reciprocal pivots and the diagonal-major copy of T_MM
-    for (int idx = tid; idx < NB * NB; idx += NT) {
+    for (int idx = tid; idx < NB * NB; idx += SolveShape<C>::THREADS) {
       const int i = idx / NB, j = idx % NB;
       C d;
       d.x = sT2[i * LD + i].x - sT1[j * LD + j].x;
@@ -644,7 +663,7 @@ int enqueue(SolveCtx& c, int n, const C* t, const C* e, long long ld, C* l, doub
     if (lev % BW == 0 && lev >= BW * (1 + FAR_LA))
       SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, c.ev_f[(lev / BW - 1 - FAR_LA) % NFAR_EV], 0));
     SweepArgs a{n, N, lev, 0, ld};
-    solve_kernel<C><<<lev + 1, NT, smem_solve, s_solve>>>(a, t, Rn, Rf, l, cl, d_clipped);
+    solve_kernel<C><<<lev + 1, SolveShape<C>::THREADS, smem_solve, s_solve>>>(a, t, Rn, Rf, l, cl, d_clipped);
     SR_LAUNCH_CHECK();
     // NEAR(lev): sources of level lev-1 into levels lev+1 .. 4 (b + 1 + FAR_LA) - 1, b = (lev-1)/4
     if (lev >= 1) {

@@ -26,6 +26,11 @@
 
 #include <stdlib.h>
 
+#include <algorithm>
+#include <map>
+#include <tuple>
+#include <vector>
+
 #include "sr_common.cuh"
 #include "tc_common.cuh"
 
@@ -46,6 +51,8 @@ struct OzParams {
   int lower_only;               // Hermitian product: only tiles with nt <= mt
   int group_m;                  // work units per rasterisation group (L2 reuse of the A panel)
   int real;                     // real x real product, 256-column tiles, one N = 256 MMA per k-step
+  const int* table;             // lower_only: the units of one modulus that hold a lower tile, in raster
+  int units_per_mod;            //   order (mp | nt << 16), so every cluster gets only real work
   int stages;                   // ring slots in use
   long long out_pitch;          // bytes between output rows
   long long out_plane;          // bytes between output planes (re / im)
@@ -149,12 +156,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int cid = blockIdx.x / CM, ncl = gridDim.x / CM;
   OzParams pu = p;
   pu.tiles_m = (p.tiles_m + CM - 1) / CM;
-  const int total_tiles = p.nmod * pu.tiles_m * p.tiles_n;
+  const int total_tiles = p.table ? p.nmod * p.units_per_mod : p.nmod * pu.tiles_m * p.tiles_n;
   const int kblocks = (p.K + TK - 1) / TK;
   // a Hermitian (lower_only) unit is skipped only when every tile of it is
   // strictly upper, so both CTAs of a cluster run identical pipelines
   auto unit = [&](int t, int& l, int& mt, int& nt) -> bool {
     int mp;
+    if (p.table) {
+      l = t / p.units_per_mod;
+      const int v = __ldg(p.table + (t - l * p.units_per_mod));
+      mp = v & 0xFFFF;
+      nt = v >> 16;
+      mt = mp * CM + crank;
+      return true;
+    }
     decode_tile(pu, t, l, mp, nt);
     mt = mp * CM + crank;
     return !(p.lower_only && nt > mp * CM + CM - 1);
@@ -316,6 +331,31 @@ int make_map(CUtensorMap* map, const void* base, int K, int rows, int planes, in
   return r == CUDA_SUCCESS ? SR_OK : SR_ECUDA;
 }
 
+// Unit table of a lower_only product (cached per shape): units (mp, nt) with
+// at least one tile on or below the diagonal, in decode_tile's raster order.
+const int* lower_table(int tiles_mp, int tiles_n, int cm, int group, int* count) {
+  static std::map<std::tuple<int, int, int, int>, std::pair<int*, int>> cache;
+  const auto key = std::make_tuple(tiles_mp, tiles_n, cm, group);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *count = it->second.second;
+    return it->second.first;
+  }
+  std::vector<int> v;
+  for (int first = 0; first < tiles_mp; first += group) {
+    const int gm = std::min(group, tiles_mp - first);
+    for (int nt = 0; nt < tiles_n; ++nt)
+      for (int mp = first; mp < first + gm; ++mp)
+        if (nt <= mp * cm + cm - 1) v.push_back(mp | (nt << 16));
+  }
+  int* d = nullptr;
+  if (cudaMalloc(&d, v.size() * sizeof(int)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  cache[key] = std::make_pair(d, (int)v.size());
+  *count = (int)v.size();
+  return d;
+}
+
 }  // namespace
 
 extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, const void* a, int a_planes,
@@ -366,6 +406,11 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
   // inside one die's half of the L2 while every N-tile streams past it
   p.group_m = (getenv("SR_OZ_GROUP_M") ? atoi(getenv("SR_OZ_GROUP_M")) : GROUP_M) / cm;
   if (p.group_m < 1) p.group_m = 1;
+  if (lower_only && !getenv("SR_OZ_NO_COMPACT")) {
+    const int tiles_mp = (p.tiles_m + cm - 1) / cm;
+    p.table = lower_table(tiles_mp, p.tiles_n, cm, p.group_m, &p.units_per_mod);
+    if (!p.table) return sr_set_cuda_error(cudaErrorMemoryAllocation, "oz_gemm lower-unit table");
+  }
   if (grid > tiles) grid = tiles;
   grid -= grid % cm;
   if (grid < cm) grid = cm;

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
       for (int l = 0; l < p.nmod; ++l) {
         const int pm = p.pi[l];
         const uint32_t bm = p.bm[l];
-        const int lo = -(pm >> 1), hi = ((pm + 1) >> 1) - 1;
+        const int lo = -(pm >> 1);
         const int w0 = p.wb[l][0], w1 = p.wb[l][1], o0 = p.off0[l], c64 = p.c64[l];
         int rr[4], ri[4];
 #pragma unroll
@@ -275,13 +275,10 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
         // pack the four low bytes per plane (two byte permutes each)
         const uint32_t wr = __byte_perm(__byte_perm(rr[0], rr[1], 0x0040), __byte_perm(rr[2], rr[3], 0x0040), 0x5410);
         const uint32_t wi = __byte_perm(__byte_perm(ri[0], ri[1], 0x0040), __byte_perm(ri[2], ri[3], 0x0040), 0x5410);
-        uint32_t wn = 0;
-        if (need_neg) {
-          int rn[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) rn[e] = -ri[e] > hi ? -ri[e] - pm : -ri[e];
-          wn = __byte_perm(__byte_perm(rn[0], rn[1], 0x0040), __byte_perm(rn[2], rn[3], 0x0040), 0x5410);
-        }
+        // -im: per-byte two's-complement negation is the symmetric residue of
+        // -x for every modulus (odd p: |r| <= 127; p = 256: -(-128) wraps to
+        // -128, the representative of 128)
+        const uint32_t wn = need_neg ? __vneg4(wi) : 0u;
         store_planes(p, dst, l, mod_stride, mod_stride2, plane_stride, i, k, wr, wi, wn);
       }
       continue;

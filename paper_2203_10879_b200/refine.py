@@ -135,6 +135,7 @@ class _Fp64Workspace:
         self.red = [torch.zeros(red, dtype=torch.uint8, device=device) for _ in range(4)]
         self.solver = SolverWorkspace(n, torch.complex64, device)
         self.staging = None
+        self.inputs = None
         self.device = device
 
     def host_staging(self):
@@ -144,6 +145,18 @@ class _Fp64Workspace:
             self.staging = tuple(torch.empty((self.n, self.n), dtype=torch.complex128, device=self.device)
                                  for _ in range(2))
         return self.staging
+
+    def host_inputs(self, real_a):
+        """Device landing buffers for host inputs (Q^ planar, A planar real or
+        complex), kept across calls so an end-to-end call allocates nothing."""
+        if self.inputs is None:
+            self.inputs = {}
+        key = "a_real" if real_a else "a_cplx"
+        if "qhat" not in self.inputs:
+            self.inputs["qhat"] = ZPlanar.empty(self.n, device=self.device)
+        if key not in self.inputs:
+            self.inputs[key] = ZPlanar.empty(self.n, device=self.device, real=real_a)
+        return self.inputs["qhat"], self.inputs[key]
 
     def ptr(self, i):
         return self.scal.data_ptr() + 8 * i
@@ -182,28 +195,84 @@ def _is_host_matrix(x):
     return isinstance(x, np.ndarray) or (isinstance(x, torch.Tensor) and x.device.type == "cpu")
 
 
+def _host_tensor(x):
+    if isinstance(x, np.ndarray):
+        if x.ndim != 2:
+            raise ValueError("expected a 2-d array")
+        x = torch.from_numpy(np.ascontiguousarray(x))
+    if x.dim() != 2:
+        raise ValueError("expected a 2-d array")
+    return x
+
+
+def _h2d_planar(x, dst, landing):
+    """Copy a host (n, n) matrix, real or complex, C or Fortran order, into
+    the planar device matrix dst: one contiguous H2D of its storage into
+    the interleaved complex128 landing buffer, then a de-interleave (and,
+    for Fortran order, a transpose) on the device."""
+    n = x.shape[0]
+    if x.is_contiguous():
+        src, transposed = x, False
+    elif x.t().is_contiguous():  # Fortran order (LAPACK outputs): copy the storage as is
+        src, transposed = x.t(), True
+    else:
+        src, transposed = x.contiguous(), False
+    if src.is_complex():
+        src = src.to(torch.complex128) if src.dtype != torch.complex128 else src
+        stage = landing
+    else:
+        src = src.to(torch.float64) if src.dtype != torch.float64 else src
+        stage = torch.view_as_real(landing).view(-1)[: n * n].view(n, n)
+    stage.copy_(src, non_blocking=True)
+    view = stage.t() if transposed else stage
+    if src.is_complex():
+        dst.re_buf[:, :n].copy_(view.real)
+        dst.im_buf[:, :n].copy_(view.imag)
+    else:
+        dst.re_buf[:, :n].copy_(view)
+        if dst.im_buf is not None:
+            dst.im_buf.zero_()
+    if dst.ld != n:
+        dst.re_buf[:, n:].zero_()
+        if dst.im_buf is not None:
+            dst.im_buf[:, n:].zero_()
+    return dst
+
+
+def _upload_qhat(x, dst, landing):
+    """_coerce_hp (refine.py:341-350) of a host Q^ into the workspace's planar
+    buffer (the landing buffer is the workspace's result staging, free until
+    the first measurement); the finiteness check runs on the device."""
+    x = _host_tensor(x)
+    if x.shape[0] != x.shape[1]:
+        raise ValueError("refinement needs a square matrix")
+    _h2d_planar(x, dst, landing)
+    fin = torch.isfinite(dst.re).all() & torch.isfinite(dst.im).all()
+    if not bool(fin):
+        raise ValueError("input matrix has non-finite entries")
+    return dst
+
+
 class _AsyncUpload:
     """A host matrix copied to the device on a side stream, so the copy
     overlaps the entry step (A is first needed by the first measurement);
     the finiteness check (_coerce_hp, refine.py:341-350) is evaluated on the
     device and raised as soon as A is needed."""
 
-    def __init__(self, x, device):
-        if isinstance(x, np.ndarray):
-            if x.ndim != 2:
-                raise ValueError("expected a 2-d array")
-            x = torch.from_numpy(np.ascontiguousarray(x))
-        if x.dim() != 2:
-            raise ValueError("expected a 2-d array")
+    def __init__(self, x, device, dst=None, landing=None):
+        x = _host_tensor(x)
         rows, cols = x.shape
         if rows != cols:
             raise ValueError("refinement needs a square matrix")
         main = torch.cuda.current_stream(device)
-        self.m = ZPlanar.empty(rows, cols, device=device, real=not x.is_complex())  # allocated on main
+        self.m = dst if dst is not None else ZPlanar.empty(rows, cols, device=device, real=not x.is_complex())
         self.stream = torch.cuda.Stream(device=device)
         self.stream.wait_stream(main)
         with torch.cuda.stream(self.stream):
-            ZPlanar.fill_from(self.m, x)
+            if landing is not None:
+                _h2d_planar(x, self.m, landing)
+            else:
+                ZPlanar.fill_from(self.m, x)
             fin = torch.isfinite(self.m.re).all()
             if self.m.im is not None:
                 fin = fin & torch.isfinite(self.m.im).all()
@@ -518,19 +587,35 @@ def refine_template(a, qhat, cfg=None, device=None, out=None):
         torch.cuda.current_stream().synchronize()
         report.wall_time = time.perf_counter() - t0
         return pair, report
-    qhat = _coerce(qhat, device)
-    a_upload = None
-    if _is_host_matrix(a):
-        a_upload = _AsyncUpload(a, device)
+    ws = None
+    if _is_host_matrix(qhat) and _is_host_matrix(a):
+        # end to end from host memory: every device buffer comes from the workspace
+        qh, ah = _host_tensor(qhat), _host_tensor(a)
+        if qh.shape[0] != qh.shape[1] or ah.shape[0] != ah.shape[1]:
+            raise ValueError("refinement needs a square matrix")
+        if ah.shape != qh.shape:
+            raise ValueError("matrix and candidate shapes differ")
+        ws = _workspace(qh.shape[0], device)
+        q_dst, a_dst = ws.host_inputs(real_a=not ah.is_complex())
+        qhat = _upload_qhat(qh, q_dst, ws.host_staging()[0])
+        # A's H2D lands in T's result staging buffer (dead once copied into a_dst;
+        # T is first staged after the main stream waited for the upload)
+        a_upload = _AsyncUpload(ah, device, dst=a_dst, landing=ws.host_staging()[1])
         a = a_upload.m
     else:
-        a = _coerce(a, device)
+        qhat = _coerce(qhat, device)
+        a_upload = None
+        if _is_host_matrix(a):
+            a_upload = _AsyncUpload(a, device)
+            a = a_upload.m
+        else:
+            a = _coerce(a, device)
     if a.shape != qhat.shape:
         raise ValueError("matrix and candidate shapes differ")
     if qhat.is_real:
         qhat = ZPlanar.from_any(qhat.re, device=device, force_complex=True)
     if True:
-        ws = _workspace(a.rows, device)
+        ws = _workspace(a.rows, device) if ws is None else ws
         host = _HostResult(a.rows, device, *out, bufs=ws.host_staging()) if out is not None else None
         pair, report = _run_fp64(a, qhat, cfg, ws, host=host, a_upload=a_upload)
     torch.cuda.current_stream().synchronize()

@@ -175,3 +175,45 @@ def test_host_result_matches_device_result():
     p3, _ = refine_template(a, q, cfg2)
     p4, _ = refine_template(a, q, cfg2, out=host())
     assert torch.equal(p3.q.cpu(), p4.q) and torch.equal(p3.t.cpu(), p4.t)
+
+
+def test_host_inputs_match_device_inputs():
+    """Host inputs land in the workspace's buffers (no per-call allocation):
+    numpy, pinned torch and device-resident inputs give identical results,
+    real A stays real, and a non-finite host Q^ still raises ValueError."""
+    from paper_2203_10879_b200 import ZPlanar, inputs
+    n = 256
+    cfg = RefineConfig(precision="fp64", tol_factor=10.0 / n, max_iters=10)
+    a = inputs.gaussian_real(n, 3)
+    q = inputs.schur_vectors(a).astype(np.complex128)
+    p_dev, r_dev = refine_template(ZPlanar.from_any(a), ZPlanar.from_any(q), cfg)
+    q_dev, t_dev = p_dev.q.cpu(), p_dev.t.cpu()
+    for aa, qq in ((a, q), (torch.from_numpy(a).pin_memory(), torch.from_numpy(q).pin_memory())):
+        for _ in range(2):  # second call reuses the landing buffers
+            p, r = refine_template(aa, qq, cfg)
+            assert torch.equal(p.q.cpu(), q_dev) and torch.equal(p.t.cpu(), t_dev)
+            assert r.residual_history == r_dev.residual_history
+    bad = q.copy()
+    bad[3, 7] = np.nan
+    with pytest.raises(ValueError):
+        refine_template(a, bad, cfg)
+    bad_a = a.copy()
+    bad_a[1, 1] = np.inf
+    with pytest.raises(ValueError):
+        refine_template(bad_a, q, cfg)
+
+
+def test_host_inputs_fortran_order():
+    """Fortran-ordered host inputs (LAPACK outputs) are transposed on the
+    device, with results identical to C-ordered ones."""
+    from paper_2203_10879_b200 import inputs
+    n = 200
+    cfg = RefineConfig(precision="fp64", tol_factor=10.0 / n, max_iters=10)
+    for a in (inputs.gaussian_real(n, 5), inputs.gaussian_complex(n, 5)):
+        q = inputs.schur_vectors(a).astype(np.complex128)
+        p_c, r_c = refine_template(np.ascontiguousarray(a), np.ascontiguousarray(q), cfg)
+        p_f, r_f = refine_template(np.asfortranarray(a), np.asfortranarray(q), cfg)
+        p_t, r_t = refine_template(torch.from_numpy(np.asfortranarray(a)), torch.from_numpy(np.asfortranarray(q)), cfg)
+        assert torch.equal(p_c.q.cpu(), p_f.q.cpu()) and torch.equal(p_c.t.cpu(), p_f.t.cpu())
+        assert torch.equal(p_c.q.cpu(), p_t.q.cpu())
+        assert r_c.residual_history == r_f.residual_history == r_t.residual_history

@@ -224,7 +224,7 @@ def main():
     q_out = torch.empty((n, n), dtype=torch.complex128).pin_memory()
     t_out = torch.empty((n, n), dtype=torch.complex128).pin_memory()
     e2e = []
-    for i in range(1 + max(1, min(args.steps, 3))):  # the first call is an untimed warm-up of the host path
+    for i in range(1 + max(1, min(args.steps, 5))):  # the first call is an untimed warm-up of the host path
         barrier()
         t0 = time.perf_counter()
         if world > 1:
@@ -275,10 +275,10 @@ def main():
         "roofline": {"bound": "tensor", "kernel": "oz_gemm_kernel (tcgen05 kind::i8)",
                      "achieved": achieved, "peak": int8_peak, "unit": "TOP/s (int8)",
                      "frac": (achieved / int8_peak) if achieved else None,
-                     "traffic": 34.02e9 if n == 8192 else None,
+                     "traffic": 20.03e9 if n == 8192 else None,
                      "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of one hp "
-                                       "complex launch at n=8192 (profiles/r1_oz_gemm_ncu.md); algorithmic operand "
-                                       "+ residue bytes of that launch: 8.4e9",
+                                       "complex launch at n=8192, 17 moduli (profiles/r1_oz_gemm_ncu.md, dynamic "
+                                       "unit queue); algorithmic operand + residue bytes of that launch: 7.7e9",
                      "launches": gemm_launches, "avg_launch_ms": gemm_ms / max(gemm_launches, 1),
                      "share_of_step": gemm_ms / total_ms if total_ms else None, "peak_source": peak_src,
                      "algorithmic_ops_per_launch": gemm_ops / max(gemm_launches, 1)},
@@ -289,7 +289,7 @@ def main():
                             "note": "algorithmic FP64 flops of the hp products over the whole time-to-refine"},
         "clocks": clocks,
         "gpu_launches": int(launches),
-        "e2e": {"value": e2e_v, "unit": "s", "h2d_bytes_per_step": int(a_host.numel() * 8 + q_host.numel() * 16),
+        "e2e": {"value": e2e_v, "unit": "s", "samples": e2e, "h2d_bytes_per_step": int(a_host.numel() * 8 + q_host.numel() * 16),
                 "d2h_bytes_per_step": int(q_out.numel() * 16 + t_out.numel() * 16)},
     }
     if not args.no_cpu_baseline:

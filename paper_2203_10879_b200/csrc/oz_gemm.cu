@@ -19,8 +19,9 @@
 //   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2-5  epilogue: tcgen05.ld -> mod p -> int8 residues -> global
 // with two 256-column TMEM accumulators so the epilogue of tile i overlaps
-// the MMAs of tile i+1.  Tiles are rasterised in groups of 16 M-tiles so
-// the operand panels of a wave stay resident in the 126 MB L2.
+// the MMAs of tile i+1.  Tiles are rasterised in groups of 16 M-tiles and
+// handed out from a global counter, so the units in flight are one contiguous
+// window of the raster and their shared operand panels hit in the 126 MB L2.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -41,8 +42,14 @@ constexpr int MAX_STAGES = 8;                 // ring slots (complex: 5 x 40 KB,
 constexpr int SMEM_RING = 200 * 1024;
 constexpr int PLANE_BYTES = TM * TK;        // 8 KB per 128-row, 64-byte plane
 constexpr int NUM_THREADS = 192;
-constexpr int GROUP_M = 8;  // M-tiles per rasterisation group (measured best with 2-CTA clusters)
+// M-tiles per rasterisation group (complex products; the stacked real ones use
+// twice as many — their M is 2n).  Measured with the dynamic unit queue at
+// n = 8192, 17 moduli: DRAM reads per hp launch 30 / 17.7 / 31.7 / 132 GB for
+// groups of 8 / 16 / 32 / 64 (operands 5.4 GB), 26.9 ms at 16.
+constexpr int GROUP_M = 16;
 constexpr int MAX_MODULI = 32;
+constexpr int QD = 16;        // work-unit queue depth (producer -> MMA / epilogue, rank 0 -> rank 1)
+constexpr int SMEM_TAIL = 1024;  // barriers, unit queues, TMEM slot
 
 struct OzParams {
   int M, N, K, nmod;
@@ -74,6 +81,36 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, int v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ int ld_volatile_shared(const int* p) {
+  int v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ void decode_tile(const OzParams& p, int t, int& l, int& mt, int& nt) {
@@ -110,7 +147,7 @@ __device__ __forceinline__ int sym_mod(int v, int p, float inv) {
 template <int CM>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                   const __grid_constant__ OzParams p, int8_t* __restrict__ out) {
+                   const __grid_constant__ OzParams p, int8_t* __restrict__ out, int* __restrict__ counter) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int a_bytes = p.a_planes * PLANE_BYTES;
@@ -119,14 +156,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int STAGES = p.stages;
   const int tn = p.real ? 2 * TN : TN;
   uint64_t* bars = (uint64_t*)(smem + SMEM_RING);
-  // bars: full[MAX_STAGES], empty[MAX_STAGES], tfull[2], tempty[2]; then tmem base slot
-  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * MAX_STAGES + 4);
+  // bars: full[MAX_STAGES], empty[MAX_STAGES], tfull[2], tempty[2], qfull[QD], qempty[QD],
+  // pfull[QD], pempty[QD]; then the unit queues unitq[QD], peerq[QD] and the tmem base slot
+  int* unitq = (int*)(bars + 2 * MAX_STAGES + 4 + 4 * QD);
+  int* peerq = unitq + QD;
+  uint32_t* tmem_slot = (uint32_t*)(peerq + QD);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (MAX_STAGES + s); };
   auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * MAX_STAGES + b); };
   auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * MAX_STAGES + 2 + b); };
+  // work-unit queue: the producer pushes every unit it fetched to the MMA and
+  // epilogue warps (qfull / qempty); in a pair, rank 0 fetches and hands the
+  // unit to rank 1's producer (pfull / pempty, arrived across the cluster)
+  auto qfull_bar = [&](int s) { return bar0 + 8u * (2 * MAX_STAGES + 4 + s); };
+  auto qempty_bar = [&](int s) { return bar0 + 8u * (2 * MAX_STAGES + 4 + QD + s); };
+  auto pfull_bar = [&](int s) { return bar0 + 8u * (2 * MAX_STAGES + 4 + 2 * QD + s); };
+  auto pempty_bar = [&](int s) { return bar0 + 8u * (2 * MAX_STAGES + 4 + 3 * QD + s); };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -136,6 +183,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull_bar(b), 1);
       mbar_init(tempty_bar(b), 128);
+    }
+    for (int q = 0; q < QD; ++q) {
+      mbar_init(qfull_bar(q), 1);
+      mbar_init(qempty_bar(q), 5);  // the MMA thread + one lane per epilogue warp
+      mbar_init(pfull_bar(q), 1);
+      mbar_init(pempty_bar(q), CM > 1 ? CM - 1 : 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&tmap_a) : "memory");
@@ -151,9 +204,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
 
-  // work units: tiles (CM = 1) or vertical tile pairs (CM = 2), one per cluster
+  // work units: tiles (CM = 1) or vertical tile pairs (CM = 2), in raster
+  // order, handed out dynamically (one global counter per launch) so the
+  // units in flight always form one contiguous window of the raster: the
+  // operand panels they share are read within microseconds of each other
+  // and hit in L2, however much the clusters drift apart
   const int crank = CM > 1 ? (int)cluster_ctarank() : 0;
-  const int cid = blockIdx.x / CM, ncl = gridDim.x / CM;
   OzParams pu = p;
   pu.tiles_m = (p.tiles_m + CM - 1) / CM;
   const int total_tiles = p.table ? p.nmod * p.units_per_mod : p.nmod * pu.tiles_m * p.tiles_n;
@@ -180,7 +236,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cid; t < total_tiles; t += ncl) {
+      for (int v = 0;; ++v) {
+        const int qs = v % QD;
+        const uint32_t qph = (uint32_t)(v / QD) & 1u;
+        int t;
+        if (CM == 1) {
+          t = atomicAdd(counter, 1);
+        } else if (crank == 0) {
+          t = atomicAdd(counter, 1);
+          if (v >= QD) mbar_wait_cluster(pempty_bar(qs), qph ^ 1);  // every peer has taken unit v - QD
+#pragma unroll
+          for (int r = 1; r < CM; ++r) {
+            st_cluster_u32(mapa_u32(smem_u32(peerq + qs), r), t);
+            mbar_arrive_cluster(mapa_u32(pfull_bar(qs), r));
+          }
+        } else {
+          mbar_wait_cluster(pfull_bar(qs), qph);
+          t = ld_volatile_shared(peerq + qs);
+          mbar_arrive_cluster(mapa_u32(pempty_bar(qs), 0));
+        }
+        if (v >= QD) mbar_wait(qempty_bar(qs), qph ^ 1);
+        unitq[qs] = t;
+        mbar_arrive(qfull_bar(qs));  // release: the unit is visible to the waiting warps
+        if (t >= total_tiles) break;
         int l, mt, nt;
         if (!unit(t, l, mt, nt)) continue;
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -215,7 +293,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = cid; t < total_tiles; t += ncl) {
+    for (int v = 0;; ++v) {
+      const int qs = v % QD;
+      mbar_wait(qfull_bar(qs), (uint32_t)(v / QD) & 1u);
+      const int t = ld_volatile_shared(unitq + qs);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qempty_bar(qs));
+      if (t >= total_tiles) break;
       {
         int l, mt, nt;
         if (!unit(t, l, mt, nt)) continue;
@@ -267,7 +351,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int ew = warp & 3;  // TMEM lane quadrant this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = cid; t < total_tiles; t += ncl) {
+    for (int v = 0;; ++v) {
+      const int qs = v % QD;
+      mbar_wait(qfull_bar(qs), (uint32_t)(v / QD) & 1u);
+      const int t = ld_volatile_shared(unitq + qs);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qempty_bar(qs));
+      if (t >= total_tiles) break;
       int l, mt, nt;
       if (!unit(t, l, mt, nt)) continue;
       const int pm = p.moduli[l];
@@ -402,9 +492,7 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
   if (getenv("SR_OZ_CM")) cm = atoi(getenv("SR_OZ_CM"));
   if (cm != 1 && cm != 2 && cm != 4) cm = 2;
   if (p.tiles_m < cm) cm = 1;
-  // 16 M-tiles (a 2 x 128 x K byte A panel each) per group keep the panel
-  // inside one die's half of the L2 while every N-tile streams past it
-  p.group_m = (getenv("SR_OZ_GROUP_M") ? atoi(getenv("SR_OZ_GROUP_M")) : GROUP_M) / cm;
+  p.group_m = (getenv("SR_OZ_GROUP_M") ? atoi(getenv("SR_OZ_GROUP_M")) : (real ? 2 : 1) * GROUP_M) / cm;
   if (p.group_m < 1) p.group_m = 1;
   if (lower_only && !getenv("SR_OZ_NO_COMPACT")) {
     const int tiles_mp = (p.tiles_m + cm - 1) / cm;
@@ -419,7 +507,16 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
     return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(A)");
   if (make_map(&mb, b, K, N, b_planes, nmod, b_kpitch, (real ? 2 * TN : TN) / cm, cm == 1 ? b_planes : 1) != SR_OK)
     return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(B)");
-  const size_t smem = 1024 + (size_t)SMEM_RING + 256;
+  const size_t smem = 1024 + (size_t)SMEM_RING + SMEM_TAIL;
+  // one zeroed unit counter per launch (a pool, so launches on different
+  // streams never share one)
+  static int* counters = nullptr;
+  static unsigned launch_seq = 0;
+  constexpr int NCOUNTERS = 256;
+  if (!counters && cudaMalloc(&counters, NCOUNTERS * 32 * sizeof(int)) != cudaSuccess)
+    return sr_set_cuda_error(cudaErrorMemoryAllocation, "oz_gemm unit counters");
+  int* counter = counters + 32 * (launch_seq++ % NCOUNTERS);  // 128-byte apart
+  SR_CUDA_CHECK(cudaMemsetAsync(counter, 0, sizeof(int), (cudaStream_t)stream));
   static bool configured = false;
   if (!configured) {
     SR_CUDA_CHECK(cudaFuncSetAttribute(oz_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -447,11 +544,11 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
     SR_CUDA_CHECK(cudaOccupancyMaxActiveClusters(&ncl, oz_gemm_kernel<4>, &cfg));
     if (ncl > 0 && ncl * cm < grid) grid = ncl * cm;
     cfg.gridDim = dim3(grid);
-    SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<4>, ma, mb, p, (int8_t*)out));
+    SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<4>, ma, mb, p, (int8_t*)out, counter));
   } else if (cm == 2)
-    SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<2>, ma, mb, p, (int8_t*)out));
+    SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<2>, ma, mb, p, (int8_t*)out, counter));
   else
-    SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<1>, ma, mb, p, (int8_t*)out));
+    SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<1>, ma, mb, p, (int8_t*)out, counter));
   SR_LAUNCH_CHECK();
   return SR_OK;
 }

@@ -113,6 +113,35 @@ __device__ __forceinline__ int ld_volatile_shared(const int* p) {
   return v;
 }
 
+// cta_group::2 variants: the TMA completes on the pair leader's mbarrier (a
+// shared::cluster address), the MMA spans both CTAs (M = 256), its commit
+// arrives on the barrier at the same offset in every CTA of the mask.
+__device__ __forceinline__ void tma_load_4d_2sm(uint32_t dst, const CUtensorMap* map, uint32_t cluster_bar, int c0,
+                                                int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(cluster_bar)
+      : "memory");
+}
+__device__ __forceinline__ void umma_i8_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_2sm(uint32_t bar, uint16_t cta_mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          bar),
+      "h"(cta_mask)
+      : "memory");
+}
+
 __device__ __forceinline__ void decode_tile(const OzParams& p, int t, int& l, int& mt, int& nt) {
   const int per_mod = p.tiles_m * p.tiles_n;
   const int G = p.group_m;
@@ -144,14 +173,20 @@ __device__ __forceinline__ int sym_mod(int v, int p, float inv) {
 // operand traffic (the L1TEX->XBAR request path is the measured limiter,
 // profiles/r1_oz_gemm_ncu.md).  A stage slot is refilled only after both
 // CTAs' MMAs released it (empty barriers count the two multicast commits).
-template <int CM>
+// TWO (CM = 2): one M = 256 MMA per pair (tcgen05 cta_group::2) issued by the
+// leader; each CTA holds its 128 A rows and HALF of the N = 256 B operand, so
+// an SM ingests 32 KB per complex k-block instead of 40 (B planes: leader
+// [B_re, -B_im], peer [B_im, B_re]: the pair's two MMAs read [B_re | B_im] and
+// [-B_im | B_re]) and 16 KB instead of 24 for the stacked real products.
+template <int CM, bool TWO = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                    const __grid_constant__ OzParams p, int8_t* __restrict__ out, int* __restrict__ counter) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int a_bytes = p.a_planes * PLANE_BYTES;
-  const int b_bytes = (p.real ? 2 : p.b_planes) * PLANE_BYTES;  // real: one 256-row B plane
+  // real: one 256-row B plane (TWO: this CTA's 128 rows); complex: 3 planes (TWO: 2)
+  const int b_bytes = TWO ? (p.real ? 1 : 2) * PLANE_BYTES : (p.real ? 2 : p.b_planes) * PLANE_BYTES;
   const int stage_bytes = a_bytes + b_bytes;
   const int STAGES = p.stages;
   const int tn = p.real ? 2 * TN : TN;
@@ -178,11 +213,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full_bar(s), 1);
-      mbar_init(empty_bar(s), CM);
+      mbar_init(empty_bar(s), TWO ? 1 : CM);  // TWO: the leader's commit arrives in both CTAs
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull_bar(b), 1);
-      mbar_init(tempty_bar(b), 128);
+      mbar_init(tempty_bar(b), TWO ? 8 : 128);  // TWO: one arrive per epilogue warp of both CTAs
     }
     for (int q = 0; q < QD; ++q) {
       mbar_init(qfull_bar(q), 1);
@@ -195,8 +230,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&tmap_b) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    if (TWO) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -264,6 +304,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           uint8_t* st = smem + stage * stage_bytes;
+          if (TWO) {
+            // both CTAs' bytes complete on the leader's full barrier
+            const uint32_t fb = mapa_u32(full_bar(stage), 0);
+            if (crank == 0) mbar_expect_tx(full_bar(stage), 2 * stage_bytes);
+            tma_load_4d_2sm(smem_u32(st), &tmap_a, fb, kb * TK, mt * TM, 0, l);
+            if (p.real) {
+              tma_load_4d_2sm(smem_u32(st + a_bytes), &tmap_b, fb, kb * TK, nt * tn + crank * TN, 0, l);
+            } else {
+              // encoded B planes: 0 = -im, 1 = re, 2 = im
+              tma_load_4d_2sm(smem_u32(st + a_bytes), &tmap_b, fb, kb * TK, nt * TN, crank == 0 ? 1 : 2, l);
+              tma_load_4d_2sm(smem_u32(st + a_bytes + PLANE_BYTES), &tmap_b, fb, kb * TK, nt * TN,
+                              crank == 0 ? 0 : 1, l);
+            }
+          } else {
           mbar_expect_tx(full_bar(stage), stage_bytes);
           tma_load_4d(smem_u32(st), &tmap_a, full_bar(stage), kb * TK, mt * TM, 0, l);
           if (CM == 1) {
@@ -277,6 +331,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int pl = 0; pl < p.b_planes; ++pl)
               tma_load_4d_mc(smem_u32(st + a_bytes + pl * PLANE_BYTES + crank * (PLANE_BYTES / CM)), &tmap_b,
                              full_bar(stage), kb * TK, nt * TN + crank * (TN / CM), pl, l, (uint16_t)((1 << CM) - 1));
+          }
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -304,7 +359,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int l, mt, nt;
         if (!unit(t, l, mt, nt)) continue;
       }
-      mbar_wait(tempty_bar(acc), acc_phase ^ 1);
+      if (TWO && crank != 0) continue;  // the pair's MMAs are issued by the leader
+      if (TWO)
+        mbar_wait_cluster(tempty_bar(acc), acc_phase ^ 1);
+      else
+        mbar_wait(tempty_bar(acc), acc_phase ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const uint32_t d = tmem_base + (uint32_t)(acc * 256);
       for (int kb = 0; kb < kblocks; ++kb) {
@@ -313,6 +372,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) {
           const uint32_t sa = smem_u32(smem + stage * stage_bytes);
           const uint32_t sb = sa + a_bytes;
+          if (TWO) {
+            const uint32_t id = idesc_i8(256, 256);
+#pragma unroll
+            for (int ks = 0; ks < TK / 32; ++ks) {
+              const uint32_t acc_flag = (kb | ks) != 0;
+              umma_i8_2sm(d, umma_desc_sw64(sa + ks * 32), umma_desc_sw64(sb + ks * 32), id, acc_flag);
+              if (!p.real)
+                umma_i8_2sm(d, umma_desc_sw64(sa + PLANE_BYTES + ks * 32), umma_desc_sw64(sb + PLANE_BYTES + ks * 32),
+                            id, 1u);
+            }
+            umma_commit_2sm(empty_bar(stage), 3);
+            if (kb == kblocks - 1) umma_commit_2sm(tfull_bar(acc), 3);
+          } else {
 #pragma unroll
           for (int ks = 0; ks < TK / 32; ++ks) {
             const uint32_t acc_flag = (kb | ks) != 0;
@@ -336,6 +408,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           else
             umma_commit_mc(empty_bar(stage), (uint16_t)((1 << CM) - 1));  // release the slot in every CTA
           if (kb == kblocks - 1) umma_commit(tfull_bar(acc));
+          }
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -394,7 +467,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      mbar_arrive(tempty_bar(acc));
+      if (TWO) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_u32(tempty_bar(acc), 0));  // the leader's barrier
+      } else {
+        mbar_arrive(tempty_bar(acc));
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -403,7 +481,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   if (CM > 1) cluster_sync();  // no CTA leaves while its peer may still multicast into it
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base));
+  if (warp == 1) {
+    if (TWO)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base));
+  }
 }
 
 // 4-d map over [nmod][planes][rows][kpitch] int8, box (64, 128, planes, 1).
@@ -475,10 +558,13 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
   p.out_pitch = out_pitch;
   p.out_plane = out_pitch * M;
   p.out_mod = out_pitch * M * 2;
+  // 2-SM MMAs (cta_group::2) for CTA pairs unless SR_OZ_2SM=0
+  const bool two_sm = !(getenv("SR_OZ_2SM") && atoi(getenv("SR_OZ_2SM")) == 0);
   {
     const int stage_bytes = (p.a_planes + (real ? 2 : b_planes)) * PLANE_BYTES;
     p.stages = SMEM_RING / stage_bytes;
     if (p.stages > MAX_STAGES) p.stages = MAX_STAGES;
+    if (getenv("SR_OZ_STAGES")) p.stages = std::max(2, std::min(p.stages, atoi(getenv("SR_OZ_STAGES"))));
   }
   for (int i = 0; i < nmod; ++i) {
     if (moduli[i] < 3 || moduli[i] > 256) return SR_EINVAL;
@@ -492,6 +578,11 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
   if (getenv("SR_OZ_CM")) cm = atoi(getenv("SR_OZ_CM"));
   if (cm != 1 && cm != 2 && cm != 4) cm = 2;
   if (p.tiles_m < cm) cm = 1;
+  const bool two = two_sm && cm == 2;
+  if (two) {  // per CTA: its A rows and half of the pair's B operand
+    p.stages = std::min(MAX_STAGES, SMEM_RING / ((p.a_planes + (real ? 1 : 2)) * PLANE_BYTES));
+    if (getenv("SR_OZ_STAGES")) p.stages = std::max(2, std::min(p.stages, atoi(getenv("SR_OZ_STAGES"))));
+  }
   p.group_m = (getenv("SR_OZ_GROUP_M") ? atoi(getenv("SR_OZ_GROUP_M")) : (real ? 2 : 1) * GROUP_M) / cm;
   if (p.group_m < 1) p.group_m = 1;
   if (lower_only && !getenv("SR_OZ_NO_COMPACT")) {
@@ -505,7 +596,8 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
   CUtensorMap ma, mb;
   if (make_map(&ma, a, K, p.M, p.a_planes, nmod, a_kpitch, TM, p.a_planes) != SR_OK)
     return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(A)");
-  if (make_map(&mb, b, K, N, b_planes, nmod, b_kpitch, (real ? 2 * TN : TN) / cm, cm == 1 ? b_planes : 1) != SR_OK)
+  if (make_map(&mb, b, K, N, b_planes, nmod, b_kpitch, two ? TN : (real ? 2 * TN : TN) / cm,
+               (cm == 1 && !two) ? b_planes : 1) != SR_OK)
     return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(B)");
   const size_t smem = 1024 + (size_t)SMEM_RING + SMEM_TAIL;
   // one zeroed unit counter per launch (a pool, so launches on different
@@ -521,6 +613,8 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
   if (!configured) {
     SR_CUDA_CHECK(cudaFuncSetAttribute(oz_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     SR_CUDA_CHECK(cudaFuncSetAttribute(oz_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    SR_CUDA_CHECK(
+        cudaFuncSetAttribute(oz_gemm_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     SR_CUDA_CHECK(cudaFuncSetAttribute(oz_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
@@ -545,7 +639,9 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
     if (ncl > 0 && ncl * cm < grid) grid = ncl * cm;
     cfg.gridDim = dim3(grid);
     SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<4>, ma, mb, p, (int8_t*)out, counter));
-  } else if (cm == 2)
+  } else if (two)
+    SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<2, true>, ma, mb, p, (int8_t*)out, counter));
+  else if (cm == 2)
     SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<2>, ma, mb, p, (int8_t*)out, counter));
   else
     SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<1>, ma, mb, p, (int8_t*)out, counter));

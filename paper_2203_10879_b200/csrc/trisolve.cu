@@ -59,6 +59,9 @@ namespace {
 
 SR_TL_DECLARE(g_tl_solve)  // kinds: 0 SOLVE, 1 NEAR (slot = level)
 
+#ifndef SR_SOLVE_ONE_WARP
+#define SR_SOLVE_ONE_WARP 0  // 1: the earlier single-warp tile solve (A/B builds)
+#endif
 constexpr int NB = 32;
 constexpr int NT = 128;   // NEAR CTAs: 16 x 8 threads, each a 2 x 4 block of the tile
 // SOLVE CTAs: 128 threads, 2 x 4 blocks.  (64 threads with 4 x 4 blocks — a
@@ -259,6 +262,80 @@ __device__ __forceinline__ unsigned tile_solve_warp(const C* sT2, const C* sD, c
   return nclip;
 }
 
+// In-tile solve by all four warps of the CTA (same equations and finalisation
+// order as tile_solve_warp): lane i owns row i in every warp, warp w owns the
+// window positions d = 8w .. 8w+7 (columns j+d of row i).  Per step warp 0
+// finalises position 0 and publishes the new values through shared memory;
+// after one named barrier every warp folds them into its 8 positions (column
+// terms read the new values of rows i+d straight from shared memory, no
+// shuffles; row terms as before) and slides its window — the value leaving a
+// warp's position 0 is handed to warp w-1's position 7 through a double-
+// buffered shared slot that is read after the next step's barrier.  A quarter
+// of the multiply-adds per warp and a quarter of the registers (the CTA can
+// share an SM with a far tensor-core CTA).
+template <typename C, bool DIAG>
+__device__ __forceinline__ unsigned tile_solve_cta(const C* sT2, const C* sD, const C* sP, const C* sR, C* sX,
+                                                   C (*xs)[NB], C (*hand)[4][NB], int valid_i, int valid_j,
+                                                   typename Real<C>::T clip) {
+  using R = typename Real<C>::T;
+  constexpr int W = 8;  // window positions per warp
+  const int i = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const R clip2 = clip * clip;
+  unsigned nclip = 0;
+  C pend[W], tr[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    const int d = W * w + k;
+    const int c = i - (NB - 1) + d;  // window at step 0 covers columns i-31 .. i
+    pend[k] = (c >= 0) ? sR[i * LD + c] : czero<C>();
+    tr[k] = (i + d < NB) ? sT2[i * LD + i + d] : czero<C>();
+  }
+#pragma unroll 2
+  for (int t = 0; t < 2 * NB - 1; ++t) {
+    const int j = t - (NB - 1) + i;  // this lane's column at step t
+    if (w == 0) {
+      const bool valid = (j >= 0) && (j < NB) && (i < valid_i) && (j < valid_j) && (!DIAG || i > j);
+      C x = czero<C>();
+      if (valid) {
+        x = cmul(pend[0], sP[i * LD + j]);
+        if (clip > 0 && x.x * x.x + x.y * x.y > clip2) {
+          x = czero<C>();
+          ++nclip;
+        }
+        sX[i * LD + j] = x;
+      }
+      xs[t & 1][i] = x;
+    }
+    asm volatile("bar.sync 1, 128;\n" ::: "memory");
+    // position 7: handed over by warp w+1 at the end of the previous step
+    // (warp 3: the column entering the window)
+    if (t > 0) {
+      if (w < 3) {
+        pend[W - 1] = hand[(t - 1) & 1][w + 1][i];
+      } else {
+        const int c = t + i;
+        pend[W - 1] = (c < NB) ? sR[i * LD + c] : czero<C>();
+      }
+    }
+    const C xi = xs[t & 1][i];
+    const int jc = min(max(j, 0), NB - 1);
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const int d = W * w + k;
+      if (d == 0) continue;
+      // column term: row i+d finalised (i+d, j+d) (tr = 0 past the tile edge)
+      const C xv = xs[t & 1][min(i + d, NB - 1)];
+      cfms(pend[k], tr[k], xv);
+      // row term: (i, j) feeds (i, j+d) through T1[j][j+d] (0 past the edge)
+      cfma(pend[k], xi, sD[d * NB + jc]);
+    }
+    if (w > 0) hand[t & 1][w][i] = pend[0];
+#pragma unroll
+    for (int k = 0; k < W - 1; ++k) pend[k] = pend[k + 1];
+  }
+  return nclip;
+}
+
 // SOLVE launch of level `lev`: one CTA per tile (M + N - 1 - lev, M).  Folds in
 // the level lev-1 sources, adds the two right-hand-side buffers and solves.
 template <typename C>
@@ -331,10 +408,11 @@ __global__ void __launch_bounds__(SolveShape<C>::THREADS) solve_kernel(SweepArgs
     }
   }
   __syncthreads();
-  if (tid >= 32) return;
   const int vi = min(NB, n - I * NB), vj = min(NB, n - M * NB);
   const auto cl = clip;
   unsigned nclip;
+#if SR_SOLVE_ONE_WARP
+  if (tid >= 32) return;
   if (I == M)
     nclip = tile_solve_warp<C, true>(sT2, sD, sP, sRf, s1, vi, vj, cl);
   else
@@ -345,6 +423,24 @@ __global__ void __launch_bounds__(SolveShape<C>::THREADS) solve_kernel(SweepArgs
     const int gi = I * NB + r;
     if (gi < n && gj < n) L[(size_t)gi * ld + gj] = (I == M && r <= tid) ? czero<C>() : s1[r * LD + tid];
   }
+#else
+  static_assert(SolveShape<C>::THREADS == 128, "the CTA tile solve needs four warps");
+  __shared__ C xs[2][NB];
+  __shared__ C hand[2][4][NB];
+  if (I == M)
+    nclip = tile_solve_cta<C, true>(sT2, sD, sP, sRf, s1, xs, hand, vi, vj, cl);
+  else
+    nclip = tile_solve_cta<C, false>(sT2, sD, sP, sRf, s1, xs, hand, vi, vj, cl);
+  __syncthreads();
+  {
+    const int gj = M * NB + (tid & 31);
+    for (int r = tid >> 5; r < NB; r += 4) {
+      const int gi = I * NB + r;
+      if (gi < n && gj < n) L[(size_t)gi * ld + gj] = (I == M && r <= (tid & 31)) ? czero<C>() : s1[r * LD + (tid & 31)];
+    }
+  }
+  if (tid >= 32) return;
+#endif
   nclip = __reduce_add_sync(0xffffffffu, nclip);
   if (tid == 0 && nclip) atomicAdd(clipped, (unsigned long long)nclip);
   if (tid == 0) SR_TL_MARK(g_tl_solve, 0, lev, 1);

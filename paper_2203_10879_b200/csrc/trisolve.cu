@@ -706,6 +706,12 @@ int ctx_init(SolveCtx& c) {
                                      (int)(sizeof(C) * (9 * NB * LD + NB * NB))));
   SR_CUDA_CHECK(cudaFuncSetAttribute(near_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(sizeof(C) * 5 * NB * LD)));
+  // one shared-memory carveout (all of it) for every sweep kernel, so SOLVE,
+  // NEAR and far CTAs can share an SM whichever launched first
+  SR_CUDA_CHECK(cudaFuncSetAttribute(solve_kernel<C>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared));
+  SR_CUDA_CHECK(cudaFuncSetAttribute(near_kernel<C>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared));
   SR_CUDA_CHECK(cudaFuncSetAttribute(far_kernel<C, false, FAR_STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)(sizeof(C) * FAR_STAGES * FarShape<C, false>::STAGE)));
   SR_CUDA_CHECK(cudaFuncSetAttribute(far_kernel<C, true, FAR_STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -225,7 +225,15 @@ struct FarTcArgs {
 };
 
 template <bool ROW>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+// At most 216 registers per thread: the two epilogue-heavy warp pairs then
+// leave 2304 registers free in every SM sub-partition, so a 4-warp SOLVE
+// CTA (72 registers) can be resident beside a far CTA (254 registers would
+// fill two sub-partitions completely and serialise the critical path behind
+// every far launch).
+#ifndef SR_FAR_TC_MAXNREG
+#define SR_FAR_TC_MAXNREG 216
+#endif
+__global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
     far_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                   const __grid_constant__ FarTcArgs p, float2* __restrict__ Rf) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -347,22 +355,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       __syncwarp();
       const int tgt = t0 + ew;  // target tile index along the line
       const bool live = tgt < p.h;
-      // prefetch this unit's Rf block into registers before waiting for the
+      // prefetch this unit's Rf block into the warp's shared staging block
+      // (cp.async, zero-filled outside the matrix) before waiting for the
       // accumulator: the loads overlap the unit's MMAs (targets of different
-      // units never overlap, so nothing in flight writes them)
-      float2 q[NB];
-      if (!ROW) {
-        const int c0 = line * NB, row0 = a_row0 + ew * 32;
-        const bool ok = live && c0 + lane < n;
-#pragma unroll
-        for (int r = 0; r < NB; ++r)
-          q[r] = (ok && row0 + r < n) ? Rf[(size_t)(row0 + r) * ld + c0 + lane] : make_float2(0.f, 0.f);
-      } else {
-        const int r0 = line * NB;
-        const bool ok = live && idx < n;
-#pragma unroll
-        for (int i = 0; i < NB; ++i)
-          q[i] = (ok && r0 + i < n) ? Rf[(size_t)(r0 + i) * ld + idx] : make_float2(0.f, 0.f);
+      // units never overlap, so nothing in flight writes them).  Shared
+      // memory instead of registers keeps the kernel at <= 216 registers.
+      // buf[r][c] = Rf[R0 + r][C0 + c]: COL (R0, C0) = (target rows, line
+      // column block); ROW = (line row block, target columns)
+      const int R0 = !ROW ? a_row0 + ew * 32 : line * NB;
+      const int C0 = !ROW ? line * NB : a_row0 + ew * 32;
+      {
+        const bool okc = live && C0 + lane < n;
+#pragma unroll 8
+        for (int r = 0; r < NB; ++r) {
+          const bool ok = okc && R0 + r < n;
+          const float2* src = Rf + (ok ? (size_t)(R0 + r) * ld + C0 + lane : 0);
+          const uint32_t dst = smem_u32(buf + r * 33 + lane);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0)
+                       : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
       }
       mbar_wait(tfull_bar(acc), (k >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -375,39 +387,38 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       mbar_arrive(tempty_bar(acc));  // the accumulator is in registers: release it to the MMA warp
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      __syncwarp();
       if (live) {
         if (!ROW) {
-          // stage the warp's 32 x 32 block, then update Rf row by row with
-          // coalesced 256-byte stores
+          // this lane's accumulator row (R0 + lane) folded into the staged
+          // block, then the block stored row by row (coalesced 256-byte rows)
 #pragma unroll
           for (int c = 0; c < NB; ++c) {
             const float sc = ldexpf(1.f, ea + eb_s[ew][c]);
-            buf[lane * 33 + c] = make_float2(__uint_as_float(v[2 * c]) * sc, __uint_as_float(v[2 * c + 1]) * sc);
+            float2& q = buf[lane * 33 + c];
+            q = make_float2(q.x - __uint_as_float(v[2 * c]) * sc, q.y - __uint_as_float(v[2 * c + 1]) * sc);
           }
           __syncwarp();
-          const int c0 = line * NB, row0 = a_row0 + ew * 32;
-          if (c0 + lane < n) {
-#pragma unroll
-            for (int r = 0; r < NB; ++r) {
-              if (row0 + r < n) {
-                const float2 a = buf[r * 33 + lane];
-                Rf[(size_t)(row0 + r) * ld + c0 + lane] = make_float2(q[r].x - a.x, q[r].y - a.y);
-              }
-            }
+          if (C0 + lane < n) {
+#pragma unroll 8
+            for (int r = 0; r < NB; ++r)
+              if (R0 + r < n) Rf[(size_t)(R0 + r) * ld + C0 + lane] = buf[r * 33 + lane];
           }
-          __syncwarp();
         } else if (idx < n) {
-          const int r0 = line * NB;
+          // this lane's accumulator column (C0 + lane = idx)
 #pragma unroll
           for (int i = 0; i < NB; ++i) {
-            if (r0 + i < n) {
+            if (R0 + i < n) {
               const float sc = ldexpf(1.f, ea + eb_s[ew][i]);
-              Rf[(size_t)(r0 + i) * ld + idx] = make_float2(q[i].x + __uint_as_float(v[2 * i]) * sc,
-                                                            q[i].y + __uint_as_float(v[2 * i + 1]) * sc);
+              const float2 q = buf[i * 33 + lane];
+              Rf[(size_t)(R0 + i) * ld + idx] = make_float2(q.x + __uint_as_float(v[2 * i]) * sc,
+                                                            q.y + __uint_as_float(v[2 * i + 1]) * sc);
             }
           }
         }
       }
+      __syncwarp();  // buf is refilled by the next unit's prefetch
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -494,6 +505,12 @@ int far_tc_prepare(FarTcPlan* plan, int n, const float2* T, long long ld, void* 
   if (!configured) {
     SR_CUDA_CHECK(cudaFuncSetAttribute(far_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
     SR_CUDA_CHECK(cudaFuncSetAttribute(far_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+    // the whole 228 KB as shared memory: a far CTA (131 KB) leaves room for a
+    // critical-path SOLVE CTA on the same SM (a 132 KB carveout would not)
+    SR_CUDA_CHECK(cudaFuncSetAttribute(far_tc_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       cudaSharedmemCarveoutMaxShared));
+    SR_CUDA_CHECK(cudaFuncSetAttribute(far_tc_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       cudaSharedmemCarveoutMaxShared));
     configured = true;
   }
   return SR_OK;

@@ -276,14 +276,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // the next unit is fetched one unit ahead, so the atomic's round trip
+      // overlaps the current unit's loads
+      int t_next = (CM == 1 || crank == 0) ? atomicAdd(counter, 1) : 0;
       for (int v = 0;; ++v) {
         const int qs = v % QD;
         const uint32_t qph = (uint32_t)(v / QD) & 1u;
         int t;
         if (CM == 1) {
-          t = atomicAdd(counter, 1);
+          t = t_next;
+          if (t < total_tiles) t_next = atomicAdd(counter, 1);
         } else if (crank == 0) {
-          t = atomicAdd(counter, 1);
+          t = t_next;
+          if (t < total_tiles) t_next = atomicAdd(counter, 1);
           if (v >= QD) mbar_wait_cluster(pempty_bar(qs), qph ^ 1);  // every peer has taken unit v - QD
 #pragma unroll
           for (int r = 1; r < CM; ++r) {

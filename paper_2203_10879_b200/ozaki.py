@@ -229,7 +229,9 @@ def timing_end():
     return ms, float(sum(o for _, _, o in recs)), len(recs)
 
 
-def gemm_residues(ea, eb, pl, res, lower_only=False):
+def gemm_residues(ea, eb, pl, res, lower_only=False, num_sms=0):
+    """Residue products on the tensor cores; num_sms > 0 caps the persistent
+    grid (the rest of the GPU stays free for concurrent work)."""
     if ea.K != eb.K:
         raise ValueError("inner dimensions disagree: %d vs %d" % (ea.K, eb.K))
     rec = _TIMING is not None
@@ -237,8 +239,8 @@ def gemm_residues(ea, eb, pl, res, lower_only=False):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
     _lib.call("sr_oz_gemm_i8", ea.rows, eb.rows, ea.K, pl.nmod, pl.moduli_ptr(), ea.buf.data_ptr(), ea.planes,
-              ea.kp, eb.buf.data_ptr(), eb.planes, eb.kp, res.buf.data_ptr(), res.pitch, 1 if lower_only else 0, 0,
-              _stream())
+              ea.kp, eb.buf.data_ptr(), eb.planes, eb.kp, res.buf.data_ptr(), res.pitch, 1 if lower_only else 0,
+              int(num_sms), _stream())
     if rec:
         e1.record()
         real_products = 4 if eb.planes == 3 else 2

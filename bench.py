@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=8192)
-    ap.add_argument("--gemm", default="ozaki", choices=["ozaki", "dmma"])
+    ap.add_argument("--gemm", default="ozaki", choices=["ozaki", "ozaki_std", "dmma"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 

@@ -186,7 +186,8 @@ int sr_oz_exponents(int rows, int cols, int kind, const void* re, const double* 
    round(op(X) * 2^(beta - exps[i])) modulo moduli[l] (3..256, pairwise
    coprime; host array).  op(X)[i][k] = X[i][k], or X[k][i] when transposed;
    conj negates the imaginary part.  layout 0: (re, im) A operand;
-   1: (-im, re, im) complex B operand; 2: (re) real B operand.
+   1: (-im, re, im) complex B operand; 2: (re) real B operand; 4: Gaussian
+   planes (re + iota im, re - iota im) mod p for either role (see below).
    beta <= 61 (<= 106 for SR_MAT_DD). */
 int sr_oz_encode(int rows_out, int K, int kind, const void* re, const double* im, const double* re_lo,
                  const double* im_lo, long long ld, int transposed, int conj, int layout, const int* exps, int beta,
@@ -227,6 +228,35 @@ int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* table, const 
                  const double* add_im_lo, long long ld_add, double add_scale, int out_kind, void* out_re,
                  double* out_im, double* out_re_lo, double* out_im_lo, long long ld_out, int hermitian,
                  int diag_col0, void* stream);
+
+/* ---- Gaussian-CRT complex products (FP64 mode).  Moduli p with a square
+   root iota of -1 (odd, every prime factor = 1 mod 4) split Z[i]/p into two
+   copies of Z/p: x + iy -> (x + iota y, x - iota y).  A complex product mod p
+   is then two independent REAL products, C+ = A+ B+^T and C- = A- B-^T, half
+   the tensor-core work of (re, im) planes.  Operands: sr_oz_encode layout 4
+   (planes phi+, phi-; the conjugate swaps them, so the B operand of X is the
+   A operand of X^H with a_swap = 1).  Replace the same matmul_hp / matmul_lp
+   call sites (matmul.py:52-110) as the entries above. */
+
+/* R[l][g] = A[l][g ^ a_swap] B[l][b_planes == 2 ? g : 0]^T mod p_l, g = 0, 1
+   (b_planes = 1: a real B operand, layout 2).  herm = +1 / -1 (M == N,
+   b_planes == 2, C Hermitian / skew-Hermitian): only plane 0 is multiplied and
+   plane 1 is written as +-(plane 0)^T, since C- = +-C+^T.  Valid when the
+   INTEGER product is (skew-)Hermitian: row i of A and column i of B scaled
+   alike (Q^H Q from one encoding of Q; W W for skew-Hermitian W). */
+int sr_oz_gemm_i8_gauss(int M, int N, int K, int nmod, const int* moduli, const void* a, int a_swap,
+                        long long a_kpitch, const void* b, int b_planes, long long b_kpitch, void* out,
+                        long long out_pitch, int herm, int num_sms, void* stream);
+
+/* sr_oz_decode for Gaussian residue planes: table = the sr_oz_decode table
+   with the weights of the real part (w_l (p_l+1)/2 mod P), followed by
+   [nmod][6] weights of the imaginary part (w_l (2 iota_l)^-1 mod P).
+   out_kind SR_MAT_F64 (add: none or SR_MAT_F64) or SR_MAT_C64 (no add). */
+int sr_oz_decode_gauss(int M, int N, int nmod, int nchunk, const double* table, const void* res,
+                       long long res_pitch, const int* exps_a, int beta_a, const int* exps_b, int beta_b,
+                       double alpha, double shift, int add_kind, const double* add_re, const double* add_im,
+                       long long ld_add, double add_scale, int out_kind, void* out_re, double* out_im,
+                       long long ld_out, int diag_col0, void* stream);
 
 #ifdef __cplusplus
 }

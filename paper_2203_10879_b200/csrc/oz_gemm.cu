@@ -38,7 +38,7 @@
 namespace {
 
 constexpr int TM = 128, TN = 128, TK = 64;  // tile: 128 rows x 128 cols, 64-byte k blocks
-constexpr int MAX_STAGES = 8;                 // ring slots (complex: 5 x 40 KB, real: 8 x 24 KB)
+constexpr int MAX_STAGES = 12;                // ring slots (2-SM: complex 6 x 32 KB, real 12 x 16 KB)
 constexpr int SMEM_RING = 200 * 1024;
 constexpr int PLANE_BYTES = TM * TK;        // 8 KB per 128-row, 64-byte plane
 constexpr int NUM_THREADS = 192;
@@ -61,6 +61,10 @@ struct OzParams {
   const int* table;             // lower_only: the units of one modulus that hold a lower tile, in raster
   int units_per_mod;            //   order (mp | nt << 16), so every cluster gets only real work
   int stages;                   // ring slots in use
+  int gauss;                    // Gaussian planes: tile plane g = mt / tpp (real product of A plane g ^ a_swap
+  int a_swap, b_gplane, tpp;    //   with B plane g, or B plane 0 when b_gplane = 0), output plane g
+  int herm;                     // gauss, Hermitian (+1) / skew (-1) C: only plane 0 is computed, and the
+                                //   epilogue also writes herm * its transpose as plane 1 (C- = +-C+^T)
   long long out_pitch;          // bytes between output rows
   long long out_plane;          // bytes between output planes (re / im)
   long long out_mod;            // bytes between moduli
@@ -306,6 +310,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (t >= total_tiles) break;
         int l, mt, nt;
         if (!unit(t, l, mt, nt)) continue;
+        int arow = mt * TM, apl = 0, bpl = 0;
+        if (p.gauss) {
+          const int g = mt / p.tpp;
+          arow = (mt - g * p.tpp) * TM;
+          apl = g ^ p.a_swap;
+          bpl = p.b_gplane ? g : 0;
+        }
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           uint8_t* st = smem + stage * stage_bytes;
@@ -313,9 +324,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // both CTAs' bytes complete on the leader's full barrier
             const uint32_t fb = mapa_u32(full_bar(stage), 0);
             if (crank == 0) mbar_expect_tx(full_bar(stage), 2 * stage_bytes);
-            tma_load_4d_2sm(smem_u32(st), &tmap_a, fb, kb * TK, mt * TM, 0, l);
+            tma_load_4d_2sm(smem_u32(st), &tmap_a, fb, kb * TK, arow, apl, l);
             if (p.real) {
-              tma_load_4d_2sm(smem_u32(st + a_bytes), &tmap_b, fb, kb * TK, nt * tn + crank * TN, 0, l);
+              tma_load_4d_2sm(smem_u32(st + a_bytes), &tmap_b, fb, kb * TK, nt * tn + crank * TN, bpl, l);
             } else {
               // encoded B planes: 0 = -im, 1 = re, 2 = im
               tma_load_4d_2sm(smem_u32(st + a_bytes), &tmap_b, fb, kb * TK, nt * TN, crank == 0 ? 1 : 2, l);
@@ -324,13 +335,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           } else {
           mbar_expect_tx(full_bar(stage), stage_bytes);
-          tma_load_4d(smem_u32(st), &tmap_a, full_bar(stage), kb * TK, mt * TM, 0, l);
+          tma_load_4d(smem_u32(st), &tmap_a, full_bar(stage), kb * TK, arow, apl, l);
           if (CM == 1) {
-            tma_load_4d(smem_u32(st + a_bytes), &tmap_b, full_bar(stage), kb * TK, nt * tn, 0, l);
+            tma_load_4d(smem_u32(st + a_bytes), &tmap_b, full_bar(stage), kb * TK, nt * tn, bpl, l);
           } else if (p.real) {
             // this CTA's 128 of the tile's 256 B rows, multicast to the pair
             tma_load_4d_mc(smem_u32(st + a_bytes + crank * (2 * PLANE_BYTES / CM)), &tmap_b, full_bar(stage),
-                           kb * TK, nt * tn + crank * (tn / CM), 0, l, (uint16_t)((1 << CM) - 1));
+                           kb * TK, nt * tn + crank * (tn / CM), bpl, l, (uint16_t)((1 << CM) - 1));
           } else {
             // this CTA's half of every B plane, multicast to the pair
             for (int pl = 0; pl < p.b_planes; ++pl)
@@ -442,8 +453,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const float inv = p.inv[l];
       mbar_wait(tfull_bar(acc), acc_phase);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const int row = mt * TM + ew * 32 + lane;
-      int8_t* base = out + (size_t)l * p.out_mod + (size_t)row * p.out_pitch;
+      int g = 0, row = mt * TM + ew * 32 + lane;
+      if (p.gauss) {
+        g = mt / p.tpp;
+        row = (mt - g * p.tpp) * TM + ew * 32 + lane;
+      }
+      int8_t* base = out + (size_t)l * p.out_mod + (size_t)g * p.out_plane + (size_t)row * p.out_pitch;
 #pragma unroll 1
       for (int chunk = 0; chunk < 16; ++chunk) {
         uint32_t v[16];
@@ -461,6 +476,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             w |= ((uint32_t)(r & 0xFF)) << (8 * e);
           }
           packed[q] = w;
+        }
+        if (p.herm && row < p.M) {
+          // C- = herm * C+^T: this row's 16 values down column `row` of plane 1
+          // (the warp's 32 rows are 32 consecutive bytes of each target row)
+          int8_t* tdst = out + (size_t)l * p.out_mod + p.out_plane + row;
+          const uint32_t nmask = p.herm < 0 ? 0xFFFFFFFFu : 0u;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int col = col0 + e;
+            if (col < p.N) {
+              uint32_t b = (packed[e >> 2] >> (8 * (e & 3))) & 0xFFu;
+              b = ((b ^ nmask) - nmask) & 0xFFu;  // two's-complement negation when skew
+              tdst[(size_t)col * p.out_pitch] = (int8_t)b;
+            }
+          }
         }
         if (row < p.M) {
           int8_t* dst = base + (size_t)plane * p.out_plane + col0;
@@ -534,14 +564,17 @@ const int* lower_table(int tiles_mp, int tiles_n, int cm, int group, int* count)
   return d;
 }
 
-}  // namespace
-
-extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, const void* a, int a_planes,
-                             long long a_kpitch, const void* b, int b_planes, long long b_kpitch, void* out,
-                             long long out_pitch, int lower_only, int num_sms, void* stream) {
+int gemm_launch(int M, int N, int K, int nmod, const int* moduli, const void* a, int a_planes, long long a_kpitch,
+                const void* b, int b_planes, long long b_kpitch, void* out, long long out_pitch, int lower_only,
+                int num_sms, void* stream, bool gauss, int a_swap, int herm) {
   if (M <= 0 || N <= 0 || K <= 0 || nmod <= 0 || nmod > MAX_MODULI) return SR_EINVAL;
   if (lower_only && M != N) return SR_EINVAL;
-  if (a_planes != 2 || (b_planes != 1 && b_planes != 3)) return SR_EINVAL;
+  if (gauss) {
+    if (a_planes != 2 || (b_planes != 1 && b_planes != 2) || lower_only) return SR_EINVAL;
+    if (herm != 0 && (M != N || b_planes != 2 || (herm != 1 && herm != -1))) return SR_EINVAL;
+  } else if (a_planes != 2 || (b_planes != 1 && b_planes != 3)) {
+    return SR_EINVAL;
+  }
   if ((a_kpitch | b_kpitch | out_pitch) & 15) return SR_EINVAL;
   if (K > (1 << 16)) return SR_EINVAL;  // 2K terms of |x| <= 2^14: int32 accumulation stays exact
   if (((uintptr_t)a | (uintptr_t)b | (uintptr_t)out) & 15) return SR_EINVAL;
@@ -549,8 +582,8 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
   memset(&p, 0, sizeof(p));
   // complex x real: [C_re; C_im] = [A_re; A_im] B^T is one real product with
   // 2M stacked rows (the A planes and the output planes are stacked row blocks)
-  const bool real = (b_planes == 1 && !lower_only && !getenv("SR_OZ_NO_REAL"));
-  p.M = real ? 2 * M : M;
+  const bool real = gauss || (b_planes == 1 && !lower_only && !getenv("SR_OZ_NO_REAL"));
+  p.M = (real && !gauss) ? 2 * M : M;
   p.N = N;
   p.K = K;
   p.nmod = nmod;
@@ -558,6 +591,15 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
   p.a_planes = real ? 1 : a_planes;
   p.b_planes = b_planes;
   p.tiles_m = (p.M + TM - 1) / TM;
+  const int planes_out = herm ? 1 : 2;
+  if (gauss) {
+    p.gauss = 1;
+    p.a_swap = a_swap ? 1 : 0;
+    p.b_gplane = b_planes == 2 ? 1 : 0;
+    p.herm = herm;
+    p.tpp = p.tiles_m;
+    p.tiles_m = planes_out * p.tpp;
+  }
   p.tiles_n = (N + (real ? 2 * TN : TN) - 1) / (real ? 2 * TN : TN);
   p.lower_only = lower_only;
   p.out_pitch = out_pitch;
@@ -576,13 +618,18 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
     p.moduli[i] = moduli[i];
     p.inv[i] = 1.0f / (float)moduli[i];
   }
-  const int tiles = nmod * p.tiles_m * p.tiles_n;
   int grid = num_sms > 0 ? num_sms : 148;
   // clusters of two CTAs sharing the B tile whenever there are M-tile pairs to share
   int cm = (p.tiles_m >= 2 && grid >= 2 && !getenv("SR_OZ_NO_CLUSTER")) ? 2 : 1;
   if (getenv("SR_OZ_CM")) cm = atoi(getenv("SR_OZ_CM"));
   if (cm != 1 && cm != 2 && cm != 4) cm = 2;
   if (p.tiles_m < cm) cm = 1;
+  if (gauss && cm == 4) cm = 2;
+  if (gauss && cm == 2 && (p.tpp & 1)) {  // a CTA pair never straddles two planes
+    p.tpp += 1;
+    p.tiles_m = planes_out * p.tpp;
+  }
+  const int tiles = nmod * p.tiles_m * p.tiles_n;
   const bool two = two_sm && cm == 2;
   if (two) {  // per CTA: its A rows and half of the pair's B operand
     p.stages = std::min(MAX_STAGES, SMEM_RING / ((p.a_planes + (real ? 1 : 2)) * PLANE_BYTES));
@@ -599,10 +646,11 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
   grid -= grid % cm;
   if (grid < cm) grid = cm;
   CUtensorMap ma, mb;
-  if (make_map(&ma, a, K, p.M, p.a_planes, nmod, a_kpitch, TM, p.a_planes) != SR_OK)
-    return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(A)");
+  const int rc_a = gauss ? make_map(&ma, a, K, M, 2, nmod, a_kpitch, TM, 1)
+                         : make_map(&ma, a, K, p.M, p.a_planes, nmod, a_kpitch, TM, p.a_planes);
+  if (rc_a != SR_OK) return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(A)");
   if (make_map(&mb, b, K, N, b_planes, nmod, b_kpitch, two ? TN : (real ? 2 * TN : TN) / cm,
-               (cm == 1 && !two) ? b_planes : 1) != SR_OK)
+               (cm == 1 && !two && !gauss) ? b_planes : 1) != SR_OK)
     return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(B)");
   const size_t smem = 1024 + (size_t)SMEM_RING + SMEM_TAIL;
   // one zeroed unit counter per launch (a pool, so launches on different
@@ -652,4 +700,19 @@ extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, c
     SR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, oz_gemm_kernel<1>, ma, mb, p, (int8_t*)out, counter));
   SR_LAUNCH_CHECK();
   return SR_OK;
+}
+}  // namespace
+
+extern "C" int sr_oz_gemm_i8(int M, int N, int K, int nmod, const int* moduli, const void* a, int a_planes,
+                             long long a_kpitch, const void* b, int b_planes, long long b_kpitch, void* out,
+                             long long out_pitch, int lower_only, int num_sms, void* stream) {
+  return gemm_launch(M, N, K, nmod, moduli, a, a_planes, a_kpitch, b, b_planes, b_kpitch, out, out_pitch, lower_only,
+                     num_sms, stream, false, 0, 0);
+}
+
+extern "C" int sr_oz_gemm_i8_gauss(int M, int N, int K, int nmod, const int* moduli, const void* a, int a_swap,
+                                   long long a_kpitch, const void* b, int b_planes, long long b_kpitch, void* out,
+                                   long long out_pitch, int herm, int num_sms, void* stream) {
+  return gemm_launch(M, N, K, nmod, moduli, a, 2, a_kpitch, b, b_planes, b_kpitch, out, out_pitch, 0, num_sms, stream,
+                     true, a_swap, herm);
 }

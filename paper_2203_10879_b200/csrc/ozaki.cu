@@ -129,7 +129,11 @@ __global__ void exps_transposed_kernel(int rows, int cols, Src s, long long ld, 
 // layout 0: A operand (re, im);  1: B operand (-im, re, im);  2: B operand (re);
 // 3: both roles of one matrix X read column-wise (transposed): the A operand
 //    of X^H (re, -im) into out and the B operand of X (-im, re, im) into out2,
-//    sharing the residue computation (Q^H and Q of every measurement)
+//    sharing the residue computation (Q^H and Q of every measurement);
+// 4: Gaussian planes (re + iota im, re - iota im) mod p, iota^2 = -1 mod p, for
+//    either role: a complex product mod p is then two independent real
+//    products (oz_gemm.cu, gauss mode).  The conjugate swaps the two planes, so
+//    the B operand of X is also the A operand of X^H (planes swapped).
 struct EncodeParams {
   int rows_out, K, transposed, conj, layout, beta, nmod, ndig;
   long long ld, kpitch;
@@ -141,6 +145,8 @@ struct EncodeParams {
   int c64[MAXMOD];             // 2^64 mod p, symmetric
   uint32_t bm[MAXMOD];         // Barrett multiplier floor(2^32 / p) + 1
   int off0[MAXMOD], off1[MAXMOD];  // positive shift (a multiple of p), and it minus 2^64 mod p
+  int iota[MAXMOD];                // layout 4: a square root of -1 mod p (symmetric)
+  int offg[MAXMOD];                // layout 4: a multiple of p above |re +- iota im|, minus lo
 };
 
 // balanced 11-bit digits of an integer-valued double (error-free, top-down)
@@ -173,6 +179,9 @@ __device__ __forceinline__ void store_planes(const EncodeParams& p, int8_t* dst,
     *reinterpret_cast<uint32_t*>(dm) = wn;
     *reinterpret_cast<uint32_t*>(dm + plane_stride) = wr;
     *reinterpret_cast<uint32_t*>(dm + 2 * plane_stride) = wi;
+  } else if (p.layout == 4) {
+    *reinterpret_cast<uint32_t*>(dm) = wr;  // (phi+, phi-) passed in wr, wi
+    *reinterpret_cast<uint32_t*>(dm + plane_stride) = wi;
   } else if (p.layout == 3) {
     *reinterpret_cast<uint32_t*>(dm) = wr;  // A operand of X^H: (re, -im)
     *reinterpret_cast<uint32_t*>(dm + plane_stride) = wn;
@@ -222,7 +231,7 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
     }
   }
   __syncthreads();
-  const int planes = p.layout == 0 || p.layout == 3 ? 2 : (p.layout == 1 ? 3 : 1);
+  const int planes = p.layout == 0 || p.layout == 3 || p.layout == 4 ? 2 : (p.layout == 1 ? 3 : 1);
   const long long plane_stride = (long long)p.rows_out * p.kpitch;
   const long long mod_stride = plane_stride * planes;
   const long long mod_stride2 = plane_stride * 3;  // layout 3: out2 holds the 3 B planes
@@ -271,6 +280,19 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
           b = b - (b >> 31) * pm + lo;
           rr[e] = a;
           ri[e] = b;
+        }
+        if (p.layout == 4) {
+          // phi+- = re +- iota im (|.| < 2^14), reduced like the byte sums above
+          const int io = p.iota[l], og = p.offg[l];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int t = ri[e] * io;
+            const int vp = rr[e] + t + og, vm = rr[e] - t + og;
+            int a = vp - (int)__umulhi((uint32_t)vp, bm) * pm;
+            int b = vm - (int)__umulhi((uint32_t)vm, bm) * pm;
+            rr[e] = a - (a >> 31) * pm + lo;
+            ri[e] = b - (b >> 31) * pm + lo;
+          }
         }
         // pack the four low bytes per plane (two byte permutes each)
         const uint32_t wr = __byte_perm(__byte_perm(rr[0], rr[1], 0x0040), __byte_perm(rr[2], rr[3], 0x0040), 0x5410);
@@ -346,6 +368,7 @@ struct DecodeParams {
   double offv[MAXCHUNK];       // 2^off[j]
   double cw[MAXCHUNK], icw[MAXCHUNK];  // 2^(off[j-1]-off[j]) and its inverse
   double inv_p;                // 1 / P
+  double w_im[MAXMOD][MAXCHUNK];  // gauss: weights of the imaginary part (w holds the real part's)
 };
 
 __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
@@ -405,8 +428,12 @@ struct Dst {
   double* im_lo;
 };
 
-// one thread: row i, columns j0..j0+3, both planes
-template <int NC, int OUT, int ADD>
+// one thread: row i, columns j0..j0+3, both planes.  G: the residue planes are
+// Gaussian (phi+, phi-) = (re + iota im, re - iota im) mod p; re = (phi+ + phi-)/2
+// and im = (phi+ - phi-)/(2 iota) mod p, the constant factors folded into the
+// CRT weights (w: real part, w_im: imaginary part), so the decode only forms
+// phi+ +- phi- (|.| <= 240: the chunk sums stay below 2^53 for <= 32 moduli).
+template <int NC, int OUT, int ADD, bool G = false>
 __global__ void __launch_bounds__(256) decode_kernel(const __grid_constant__ DecodeParams p,
                                                      const int8_t* __restrict__ res, const int* __restrict__ ea,
                                                      const int* __restrict__ eb, Src add, Dst out) {
@@ -424,14 +451,19 @@ __global__ void __launch_bounds__(256) decode_kernel(const __grid_constant__ Dec
       for (int e = 0; e < 4; ++e)
 #pragma unroll
         for (int j = 0; j < NC; ++j) S[e][j] = 0.0;
-      const int8_t* r = res + (size_t)plane * p.res_plane + (size_t)i * p.res_pitch + j0;
+      const int8_t* r = res + (size_t)(G ? 0 : plane) * p.res_plane + (size_t)i * p.res_pitch + j0;
+      const double(*W)[MAXCHUNK] = (G && plane == 1) ? p.w_im : p.w;
+      const double sgn = plane == 0 ? 1.0 : -1.0;  // G: phi+ + phi- (re) or phi+ - phi- (im)
       // residue words in groups of 8 moduli (8 loads in flight, bounded registers)
 #pragma unroll 1
       for (int l0 = 0; l0 < p.nmod; l0 += 8) {
-        uint32_t wv[8];
+        uint32_t wv[8], wm[8];
 #pragma unroll
         for (int g = 0; g < 8; ++g)
-          if (l0 + g < p.nmod) wv[g] = *reinterpret_cast<const uint32_t*>(r + (size_t)(l0 + g) * p.res_mod);
+          if (l0 + g < p.nmod) {
+            wv[g] = *reinterpret_cast<const uint32_t*>(r + (size_t)(l0 + g) * p.res_mod);
+            if (G) wm[g] = *reinterpret_cast<const uint32_t*>(r + p.res_plane + (size_t)(l0 + g) * p.res_mod);
+          }
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
           if (l0 + g >= p.nmod) break;
@@ -439,11 +471,13 @@ __global__ void __launch_bounds__(256) decode_kernel(const __grid_constant__ Dec
           // x + 128 in [0, 255]; as the low word of 0x4338000000000000 it reads
           // 1.5 * 2^52 + x + 128, so one DADD recovers x exactly.
           const uint32_t w4 = wv[g] ^ 0x80808080u;
+          const uint32_t m4 = G ? (wm[g] ^ 0x80808080u) : 0u;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const double x = __hiloint2double(0x43380000, (w4 >> (8 * e)) & 0xFF) - 6755399441055872.0;
+            double x = __hiloint2double(0x43380000, (w4 >> (8 * e)) & 0xFF) - 6755399441055872.0;
+            if (G) x = fma(sgn, __hiloint2double(0x43380000, (m4 >> (8 * e)) & 0xFF) - 6755399441055872.0, x);
 #pragma unroll
-            for (int j = 0; j < NC; ++j) S[e][j] = fma(x, p.w[l0 + g][j], S[e][j]);  // exact: < 2^52
+            for (int j = 0; j < NC; ++j) S[e][j] = fma(x, W[l0 + g][j], S[e][j]);  // exact: < 2^53
           }
         }
       }
@@ -533,6 +567,25 @@ void launch_decode(int grid, cudaStream_t st, const DecodeParams& p, const int8_
   decode_kernel<NC, OUT, ADD><<<grid, 256, 0, st>>>(p, res, ea, eb, add, out);
 }
 
+// Gaussian residues: FP64-mode outputs only (planar FP64 or complex64; + FP64 X)
+template <int NC>
+int dispatch_gauss(int out_kind, int add_kind, int grid, cudaStream_t st, const DecodeParams& p, const int8_t* res,
+                   const int* ea, const int* eb, Src add, Dst out) {
+  if (add_kind >= 0 && add_kind != SR_MAT_F64) return SR_EINVAL;
+  const bool with_add = add_kind == SR_MAT_F64;
+  if (out_kind == SR_MAT_F64) {
+    if (with_add)
+      decode_kernel<NC, SR_MAT_F64, SR_MAT_F64, true><<<grid, 256, 0, st>>>(p, res, ea, eb, add, out);
+    else
+      decode_kernel<NC, SR_MAT_F64, -1, true><<<grid, 256, 0, st>>>(p, res, ea, eb, add, out);
+  } else if (out_kind == SR_MAT_C64 && !with_add) {
+    decode_kernel<NC, SR_MAT_C64, -1, true><<<grid, 256, 0, st>>>(p, res, ea, eb, add, out);
+  } else {
+    return SR_EINVAL;
+  }
+  return SR_OK;
+}
+
 template <int NC, int OUT>
 int dispatch_add(int add_kind, int grid, cudaStream_t st, const DecodeParams& p, const int8_t* res, const int* ea,
                  const int* eb, Src add, Dst out) {
@@ -596,7 +649,8 @@ namespace {
 int encode_launch(int rows_out, int K, int kind, const void* re, const double* im, const double* re_lo,
                   const double* im_lo, long long ld, int transposed, int conj, int layout, const int* exps, int beta,
                   int nmod, const int* moduli, void* out, void* out2, long long kpitch, cudaStream_t st) {
-  if (rows_out <= 0 || K <= 0 || nmod <= 0 || nmod > MAXMOD || layout < 0 || layout > 3) return SR_EINVAL;
+  if (rows_out <= 0 || K <= 0 || nmod <= 0 || nmod > MAXMOD || layout < 0 || layout > 4) return SR_EINVAL;
+  if (layout == 4 && kind == SR_MAT_DD) return SR_EINVAL;
   if (kind < 0 || kind > SR_MAT_DD || (kind == SR_MAT_DD && (!re_lo || !im_lo || !im))) return SR_EINVAL;
   const int max_beta = kind == SR_MAT_DD ? 106 : 61;
   if (beta < 1 || beta > max_beta || (kpitch & 15) || kpitch < K) return SR_EINVAL;
@@ -643,9 +697,18 @@ int encode_launch(int rows_out, int K, int kind, const void* re, const double* i
     const int shift = (8 * 255 * 128 + 256 + m - 1) / m * m;  // > |byte dot products| + |2^64 mod m|
     p.off0[l] = shift + (m >> 1);  // + (-lo): the residue comes out in [0, m), then shifted by lo
     p.off1[l] = 0;
+    if (layout == 4) {
+      int io = 0;
+      for (int x = 1; x < m && !io; ++x)
+        if ((x * x + 1) % m == 0) io = x;
+      if (!io || !(m & 1)) return SR_EINVAL;  // needs an odd modulus with a square root of -1
+      p.iota[l] = (int)sym(io);
+      const int half = m >> 1;
+      p.offg[l] = (half + half * half + m - 1) / m * m + half;  // >= |re| + |iota im|, then -lo
+    }
   }
   // K padding columns of the residue planes must read as zero
-  const int planes = layout == 0 || layout == 3 ? 2 : (layout == 1 ? 3 : 1);
+  const int planes = layout == 0 || layout == 3 || layout == 4 ? 2 : (layout == 1 ? 3 : 1);
   if (kpitch > K) {
     SR_CUDA_CHECK(cudaMemsetAsync(out, 0, (size_t)nmod * planes * rows_out * kpitch, st));
     if (out2) SR_CUDA_CHECK(cudaMemsetAsync(out2, 0, (size_t)nmod * 3 * rows_out * kpitch, st));
@@ -675,7 +738,7 @@ extern "C" int sr_oz_encode(int rows_out, int K, int kind, const void* re, const
                             const double* im_lo, long long ld, int transposed, int conj, int layout,
                             const int* exps, int beta, int nmod, const int* moduli, void* out, long long kpitch,
                             void* stream) {
-  if (layout > 2) return SR_EINVAL;
+  if (layout == 3) return SR_EINVAL;  // the dual layout has its own entry (two outputs)
   return encode_launch(rows_out, K, kind, re, im, re_lo, im_lo, ld, transposed, conj, layout, exps, beta, nmod,
                        moduli, out, nullptr, kpitch, (cudaStream_t)stream);
 }
@@ -691,12 +754,14 @@ extern "C" int sr_oz_encode_dual(int rows_out, int K, int kind, const void* re, 
 
 // table (host): [nmod][6] CRT weights, [6] modulus-product chunks, [6] chunk
 // offsets (as doubles), 1/P
-extern "C" int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* table, const void* res,
-                            long long res_pitch, const int* exps_a, int beta_a, const int* exps_b, int beta_b,
-                            double alpha, double shift, int add_kind, const double* add_re, const double* add_im,
-                            const double* add_re_lo, const double* add_im_lo, long long ld_add, double add_scale,
-                            int out_kind, void* out_re, double* out_im, double* out_re_lo, double* out_im_lo,
-                            long long ld_out, int hermitian, int diag_col0, void* stream) {
+namespace {
+int decode_launch(int M, int N, int nmod, int nchunk, const double* table, const void* res, long long res_pitch,
+                  const int* exps_a, int beta_a, const int* exps_b, int beta_b, double alpha, double shift,
+                  int add_kind, const double* add_re, const double* add_im, const double* add_re_lo,
+                  const double* add_im_lo, long long ld_add, double add_scale, int out_kind, void* out_re,
+                  double* out_im, double* out_re_lo, double* out_im_lo, long long ld_out, int hermitian,
+                  int diag_col0, bool gauss, void* stream) {
+  if (gauss && hermitian != 0) return SR_EINVAL;
   if (M <= 0 || N <= 0 || nmod <= 0 || nmod > MAXMOD || nchunk < 1 || nchunk > MAXCHUNK) return SR_EINVAL;
   if (res_pitch & 3) return SR_EINVAL;
   if (out_kind < 0 || out_kind > SR_MAT_DD) return SR_EINVAL;
@@ -735,6 +800,9 @@ extern "C" int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* ta
     p.icw[j] = ldexp(1.0, -(off[j - 1] - off[j]));
   }
   p.inv_p = table[nmod * MAXCHUNK + 2 * MAXCHUNK];
+  if (gauss)
+    for (int l = 0; l < nmod; ++l)
+      for (int j = 0; j < MAXCHUNK; ++j) p.w_im[l][j] = table[nmod * MAXCHUNK + 2 * MAXCHUNK + 1 + l * MAXCHUNK + j];
   const long long total = (long long)M * ((N + 3) / 4);
   int grid = (int)((total + 255) / 256);
   if (grid > 148 * 16) grid = 148 * 16;
@@ -742,6 +810,15 @@ extern "C" int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* ta
   Src add{add_re, add_im, add_re_lo, add_im_lo, add_kind};
   Dst out{(double*)out_re, out_im, out_re_lo, out_im_lo};
   int rc;
+  if (gauss) {
+    const int8_t* r8 = (const int8_t*)res;
+    rc = nchunk <= 2   ? dispatch_gauss<2>(out_kind, add_kind, grid, st, p, r8, exps_a, exps_b, add, out)
+         : nchunk <= 4 ? dispatch_gauss<4>(out_kind, add_kind, grid, st, p, r8, exps_a, exps_b, add, out)
+                       : dispatch_gauss<6>(out_kind, add_kind, grid, st, p, r8, exps_a, exps_b, add, out);
+    if (rc != SR_OK) return rc;
+    SR_LAUNCH_CHECK();
+    return SR_OK;
+  }
   switch (nchunk) {
     case 1:
     case 2:
@@ -767,4 +844,26 @@ extern "C" int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* ta
     SR_LAUNCH_CHECK();
   }
   return SR_OK;
+}
+}  // namespace
+
+extern "C" int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* table, const void* res,
+                            long long res_pitch, const int* exps_a, int beta_a, const int* exps_b, int beta_b,
+                            double alpha, double shift, int add_kind, const double* add_re, const double* add_im,
+                            const double* add_re_lo, const double* add_im_lo, long long ld_add, double add_scale,
+                            int out_kind, void* out_re, double* out_im, double* out_re_lo, double* out_im_lo,
+                            long long ld_out, int hermitian, int diag_col0, void* stream) {
+  return decode_launch(M, N, nmod, nchunk, table, res, res_pitch, exps_a, beta_a, exps_b, beta_b, alpha, shift,
+                       add_kind, add_re, add_im, add_re_lo, add_im_lo, ld_add, add_scale, out_kind, out_re, out_im,
+                       out_re_lo, out_im_lo, ld_out, hermitian, diag_col0, false, stream);
+}
+
+extern "C" int sr_oz_decode_gauss(int M, int N, int nmod, int nchunk, const double* table, const void* res,
+                                  long long res_pitch, const int* exps_a, int beta_a, const int* exps_b, int beta_b,
+                                  double alpha, double shift, int add_kind, const double* add_re,
+                                  const double* add_im, long long ld_add, double add_scale, int out_kind,
+                                  void* out_re, double* out_im, long long ld_out, int diag_col0, void* stream) {
+  return decode_launch(M, N, nmod, nchunk, table, res, res_pitch, exps_a, beta_a, exps_b, beta_b, alpha, shift,
+                       add_kind, add_re, add_im, nullptr, nullptr, ld_add, add_scale, out_kind, out_re, out_im,
+                       nullptr, nullptr, ld_out, 0, diag_col0, true, stream);
 }

@@ -27,6 +27,10 @@ from .matrix import DDPlanar
 # pairwise-coprime moduli <= 256, largest first (greedy from 256 down)
 MODULI = [256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193, 191, 181, 179, 173,
           167, 163, 157, 151, 149, 139, 137, 131, 127, 113, 109, 107]
+# Gaussian moduli: odd, every prime factor = 1 mod 4, so -1 has a square root
+# iota mod p and a complex product mod p splits into two real ones (GaussPlan)
+GAUSS_MODULI = [241, 233, 229, 221, 205, 197, 193, 181, 173, 157, 149, 137, 113, 109, 101, 97, 89, 73, 61, 53, 37,
+                29]
 CHUNK_BITS = 40
 MAXCHUNK = 6
 
@@ -36,23 +40,39 @@ DD_BETA = 102    # dd-mode hp operands (double-double; the stop rule is 10 n 2^-
 DD_LP_BETA = 55  # dd-mode lp (binary64) operands
 
 
-class OzPlan:
-    """Moduli and CRT constants for products with inner dimension <= K."""
+def sqrt_minus_one(p):
+    """iota with iota^2 = -1 mod p (p odd, every prime factor = 1 mod 4)."""
+    for x in range(1, p):
+        if (x * x + 1) % p == 0:
+            return x
+    raise ValueError("%d has no square root of -1" % p)
 
-    def __init__(self, K, beta_a, beta_b):
+
+class OzPlan:
+    """Moduli and CRT constants for products with inner dimension <= K.
+
+    gauss: Gaussian moduli (GAUSS_MODULI); the residue planes of a complex
+    operand are (x + iota y, x - iota y) mod p and the table carries a second
+    set of weights that maps phi+ - phi- to the imaginary part."""
+
+    gauss = False
+
+    def __init__(self, K, beta_a, beta_b, gauss=False):
         self.K = K
         self.beta_a = beta_a
         self.beta_b = beta_b
+        self.gauss = gauss
+        mods = GAUSS_MODULI if gauss else MODULI
         need = beta_a + beta_b + math.ceil(math.log2(max(K, 2))) + 2
         P = 1
         r = 0
         while P.bit_length() - 1 < need:
-            if r == len(MODULI):
+            if r == len(mods):
                 raise ValueError("no Ozaki plan for K=%d beta=(%d,%d)" % (K, beta_a, beta_b))
-            P *= MODULI[r]
+            P *= mods[r]
             r += 1
         self.nmod = r
-        self.moduli = MODULI[:r]
+        self.moduli = mods[:r]
         self.P = P
         nbits = P.bit_length()
         nchunk = (nbits + CHUNK_BITS - 1) // CHUNK_BITS
@@ -67,13 +87,23 @@ class OzPlan:
                 out.append(float((x >> offs[j]) & ((1 << (hi - offs[j])) - 1)))
             return out + [0.0] * (MAXCHUNK - nchunk)
         table = []
+        weights = []
         for p in self.moduli:
             m = P // p
-            w = (m * pow(m % p, -1, p)) % P
+            weights.append((m * pow(m % p, -1, p)) % P)
+        if gauss:
+            # re = (phi+ + phi-) / 2, im = (phi+ - phi-) / (2 iota) mod p_l
+            w_re = [(w * pow(2, -1, p)) % P for w, p in zip(weights, self.moduli)]
+            w_im = [(w * pow(2 * sqrt_minus_one(p), -1, p)) % P for w, p in zip(weights, self.moduli)]
+        else:
+            w_re, w_im = weights, []
+        for w in w_re:
             table += chunks(w)
         table += chunks(P)
         table += [float(o) for o in offs] + [0.0] * (MAXCHUNK - nchunk)
         table += [1.0 / float(P)]
+        for w in w_im:
+            table += chunks(w)
         self.nchunk = nchunk
         self.table = np.array(table, dtype=np.float64)
         self._moduli_c = np.array(self.moduli, dtype=np.int32)
@@ -88,11 +118,15 @@ class OzPlan:
 _PLANS = {}
 
 
-def plan(K, beta_a, beta_b):
-    key = (K, beta_a, beta_b)
+def plan(K, beta_a, beta_b, gauss=False):
+    key = (K, beta_a, beta_b, bool(gauss))
     if key not in _PLANS:
-        _PLANS[key] = OzPlan(K, beta_a, beta_b)
+        _PLANS[key] = OzPlan(K, beta_a, beta_b, gauss)
     return _PLANS[key]
+
+
+def gauss_plan(K, beta_a, beta_b):
+    return plan(K, beta_a, beta_b, gauss=True)
 
 
 def kpitch(K):
@@ -102,14 +136,25 @@ def kpitch(K):
 class Encoded:
     """Residue planes of one operand (A role: op(X) rows; B role: columns)."""
 
-    __slots__ = ("buf", "exps", "rows", "K", "planes", "beta", "nmod", "kp", "cap")
+    __slots__ = ("buf", "exps", "rows", "K", "planes", "beta", "nmod", "kp", "cap", "swap")
 
     def __init__(self, rows, K, planes, beta, nmod, device):
         self.rows, self.K, self.planes, self.beta, self.nmod = rows, K, planes, beta, nmod
+        self.swap = False  # Gaussian planes read in swapped order (the A operand of X^H, see conj_view)
         self.cap = nmod  # residue planes allocated; re-encodes may use fewer moduli
         self.kp = kpitch(K)
         self.buf = torch.empty(nmod * planes * rows * self.kp, dtype=torch.int8, device=device)
         self.exps = torch.empty(rows, dtype=torch.int32, device=device)
+
+
+def conj_view(eb):
+    """The B operand of X (Gaussian planes) read as the A operand of X^H: the
+    conjugate swaps phi+ and phi-, the scaling (per column of X) is the same."""
+    v = Encoded.__new__(Encoded)
+    for k in Encoded.__slots__:
+        setattr(v, k, getattr(eb, k))
+    v.swap = not eb.swap
+    return v
 
 
 def _stream():
@@ -142,10 +187,13 @@ def encode(x, rows, cols, role, pl, conj_t=False, out=None):
         out_rows, K, transposed, beta = cols, rows, 1, pl.beta_b
         layout, planes = (2, 1) if real else (1, 3)
         conj = 0
+    if pl.gauss and layout != 2:
+        layout, planes = 4, 2  # (phi+, phi-) for either role
     enc = out if out is not None else Encoded(out_rows, K, planes, beta, pl.nmod, dev)
     if enc.cap < pl.nmod or enc.rows != out_rows or enc.K != K or enc.planes != planes:
         raise ValueError("encoding buffer does not fit this operand / plan")
     enc.beta, enc.nmod = beta, pl.nmod
+    enc.swap = False
     st = _stream()
     _lib.call("sr_oz_exponents", rows, cols, kind, re, im, ld, transposed, enc.exps.data_ptr(), st)
     _lib.call("sr_oz_encode", out_rows, K, kind, re, im, re_lo, im_lo, ld, transposed, conj, layout,
@@ -238,11 +286,26 @@ def gemm_residues(ea, eb, pl, res, lower_only=False, num_sms=0):
     if rec:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-    _lib.call("sr_oz_gemm_i8", ea.rows, eb.rows, ea.K, pl.nmod, pl.moduli_ptr(), ea.buf.data_ptr(), ea.planes,
-              ea.kp, eb.buf.data_ptr(), eb.planes, eb.kp, res.buf.data_ptr(), res.pitch, 1 if lower_only else 0,
-              int(num_sms), _stream())
+    if pl.gauss:
+        # Hermitian C (lower_only=True): only C+ is multiplied, C- = C+^T.  That
+        # needs the INTEGER product to be Hermitian, i.e. the same power-of-two
+        # scale for row i of op(A) and column i of B: true for Q^H Q (one
+        # encoding) and W W (W skew-Hermitian: row and column maxima agree),
+        # not for W^2 W, so "skew" products run in full.
+        herm = 1 if (lower_only and lower_only != "skew") else 0
+        _lib.call("sr_oz_gemm_i8_gauss", ea.rows, eb.rows, ea.K, pl.nmod, pl.moduli_ptr(), ea.buf.data_ptr(),
+                  1 if ea.swap else 0, ea.kp, eb.buf.data_ptr(), eb.planes, eb.kp, res.buf.data_ptr(), res.pitch,
+                  herm, int(num_sms), _stream())
+    else:
+        _lib.call("sr_oz_gemm_i8", ea.rows, eb.rows, ea.K, pl.nmod, pl.moduli_ptr(), ea.buf.data_ptr(), ea.planes,
+                  ea.kp, eb.buf.data_ptr(), eb.planes, eb.kp, res.buf.data_ptr(), res.pitch, 1 if lower_only else 0,
+                  int(num_sms), _stream())
     if rec:
         e1.record()
+        if pl.gauss:  # one real product per output plane
+            ops = 2.0 * ea.rows * eb.rows * ea.K * (1 if herm else 2) * pl.nmod
+            _TIMING.append((e0, e1, ops))
+            return
         real_products = 4 if eb.planes == 3 else 2
         ops = 2.0 * ea.rows * eb.rows * ea.K * real_products * pl.nmod
         if lower_only:  # executed tiles: the lower 128 x 128 tiles only
@@ -263,6 +326,12 @@ def decode(res, ea, eb, pl, out, alpha=1.0, shift=0.0, add=None, add_scale=1.0, 
         a_kind, a_re, a_im, a_rl, a_il, ld_add = -1, None, None, None, None, 0
     else:
         a_kind, a_re, a_im, a_rl, a_il, ld_add, _ = mat_args(add)
+    if pl.gauss:  # both planes are full (the GEMM wrote C- = +-C+^T for Hermitian C)
+        _lib.call("sr_oz_decode_gauss", res.M, res.N, pl.nmod, pl.nchunk, pl.table_ptr(), res.buf.data_ptr(),
+                  res.pitch, ea.exps.data_ptr(), ea.beta, eb.exps.data_ptr(), eb.beta, float(alpha), float(shift),
+                  a_kind, a_re, a_im, ld_add, float(add_scale), o_kind, o_re, o_im, ld_out, int(diag_col0),
+                  _stream())
+        return out
     _lib.call("sr_oz_decode", res.M, res.N, pl.nmod, pl.nchunk, pl.table_ptr(), res.buf.data_ptr(), res.pitch,
               ea.exps.data_ptr(), ea.beta, eb.exps.data_ptr(), eb.beta, float(alpha), float(shift), a_kind, a_re,
               a_im, a_rl, a_il, ld_add, float(add_scale), o_kind, o_re, o_im, o_rl, o_il, ld_out,

@@ -87,20 +87,26 @@ class OzakiProducts:
 
     name = "ozaki"
 
-    def __init__(self, ws, a):
+    def __init__(self, ws, a, gauss=True):
+        """gauss (default): Gaussian-CRT plans — every complex product is two
+        real products per modulus (one for the Hermitian Q^H Q and W^2), and
+        one encoding of Q serves as Q (B role) and Q^H (A role, planes
+        swapped); gauss=False: the (re, im) planes, four real products."""
         self.ws = ws
+        self.gauss = gauss
         n = ws.n
         dev = ws.q.re_buf.device
-        self.hp = ozaki.plan(n, ozaki.HP_BETA, ozaki.HP_BETA)
-        self.lp = ozaki.plan(n, ozaki.LP_BETA, ozaki.LP_BETA)
+        self.hp = ozaki.plan(n, ozaki.HP_BETA, ozaki.HP_BETA, gauss)
+        self.lp = ozaki.plan(n, ozaki.LP_BETA, ozaki.LP_BETA, gauss)
         hp, lp = self.hp, self.lp
-        self.ea_qh = ozaki.Encoded(n, n, 2, hp.beta_a, hp.nmod, dev)   # Q^H, A role
+        bpl = 2 if gauss else 3
+        self.ea_qh = None if gauss else ozaki.Encoded(n, n, 2, hp.beta_a, hp.nmod, dev)   # Q^H, A role
         self.ea_x = ozaki.Encoded(n, n, 2, hp.beta_a, hp.nmod, dev)    # P or Q, A role
-        self.eb_q = ozaki.Encoded(n, n, 3, hp.beta_b, hp.nmod, dev)    # Q, B role
-        self.eb_s = ozaki.Encoded(n, n, 3, hp.beta_b, hp.nmod, dev)    # Sigma' / Y', B role
+        self.eb_q = ozaki.Encoded(n, n, bpl, hp.beta_b, hp.nmod, dev)  # Q, B role
+        self.eb_s = ozaki.Encoded(n, n, bpl, hp.beta_b, hp.nmod, dev)  # Sigma' / Y', B role
         self.res = ozaki.ResidueBuffer(n, n, hp.nmod, dev)
         self.la = ozaki.Encoded(n, n, 2, lp.beta_a, lp.nmod, dev)      # Y_lp / W / W^2, A role
-        self.lb = ozaki.Encoded(n, n, 3, lp.beta_b, lp.nmod, dev)      # W, B role
+        self.lb = ozaki.Encoded(n, n, bpl, lp.beta_b, lp.nmod, dev)    # W, B role
         self.lres = ozaki.ResidueBuffer(n, n, lp.nmod, dev)
         # the constant matrix A, B role (real A keeps one plane), encoded at the
         # first measurement so an asynchronous upload of A overlaps the entry step
@@ -116,7 +122,7 @@ class OzakiProducts:
         self._lp_with(self.lp, ea, eb, out, hermitian)
 
     def _lp_with(self, pl, ea, eb, out, hermitian=False):
-        ozaki.gemm_residues(ea, eb, pl, self.lres, lower_only=bool(hermitian))
+        ozaki.gemm_residues(ea, eb, pl, self.lres, lower_only=hermitian if hermitian == "skew" else bool(hermitian))
         ozaki.decode(self.lres, ea, eb, pl, out, hermitian=hermitian)
         _counters["lp_calls"] += 1
 
@@ -124,7 +130,7 @@ class OzakiProducts:
         """Plan for X S with a small S (||S||_F <= bound) added to an O(1) X:
         fewer moduli as the correction shrinks (ozaki.correction_beta)."""
         beta = ozaki.correction_beta(bound, self.ws.n)
-        return ozaki.plan(self.ws.n, beta, beta)
+        return ozaki.plan(self.ws.n, beta, beta, self.gauss)
 
     def _hp_with(self, pl, ea, eb, out, **kw):
         ozaki.gemm_residues(ea, eb, pl, self.res)
@@ -134,22 +140,33 @@ class OzakiProducts:
     def entry(self, qhat):
         """Q = Q^ (3I - G) / 2 = Q^ - Q^ (G - I) / 2 (orthogonal.py:167-169)."""
         ws, hp, n = self.ws, self.hp, self.ws.n
-        ozaki.encode_dual(qhat, n, n, hp, self.ea_qh, self.eb_q)        # Q^H (A role), Q^ (B role)
-        self._hp(self.ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True)  # G - I
+        ea_qh = self._encode_q(qhat)                                     # Q^H (A role), Q^ (B role)
+        self._hp(ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True)   # G - I
         pc = self._correction_plan(ws.fro_norm(ws.y))
         ozaki.encode(qhat, n, n, "a", pc, out=self.ea_x)
         ozaki.encode(ws.y, n, n, "b", pc, out=self.eb_s)
         self._hp_with(pc, self.ea_x, self.eb_s, ws.q, alpha=-0.5, add=qhat)  # Q^ - Q^ (G - I) / 2
 
+    def _encode_q(self, q):
+        """Q as the B operand (self.eb_q) and Q^H as the A operand (returned):
+        Gaussian planes — the same residues with the planes swapped; else one
+        dual encode into self.ea_qh."""
+        n, hp = self.ws.n, self.hp
+        if self.gauss:
+            ozaki.encode(q, n, n, "b", hp, out=self.eb_q)
+            return ozaki.conj_view(self.eb_q)
+        ozaki.encode_dual(q, n, n, hp, self.ea_qh, self.eb_q)
+        return self.ea_qh
+
     def measure(self, a):
         ws, hp, n = self.ws, self.hp, self.ws.n
-        ozaki.encode_dual(ws.q, n, n, hp, self.ea_qh, self.eb_q)          # Q^H (A role), Q (B role)
+        ea_qh = self._encode_q(ws.q)                                    # Q^H (A role), Q (B role)
         if self.eb_a is None:
             self.eb_a = ozaki.encode(self.a, n, n, "b", hp)
-        self._hp(self.ea_qh, self.eb_a, ws.p)                            # P = Q^H A
+        self._hp(ea_qh, self.eb_a, ws.p)                                # P = Q^H A
         ozaki.encode(ws.p, n, n, "a", hp, out=self.ea_x)
-        self._hp(self.ea_x, self.eb_q, ws.that)                          # T^ = P Q
-        self._hp(self.ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True)  # Y = Q^H Q - I
+        self._hp(self.ea_x, self.eb_q, ws.that)                         # T^ = P Q
+        self._hp(ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True)   # Y = Q^H Q - I
 
     def _lp_plans(self, norm_y, norm_w):
         """Plans for the fused update's W^2 and X W (X = Y - W - W^2) from
@@ -162,7 +179,7 @@ class OzakiProducts:
         nx = norm_y + norm_w + norm_w * norm_w
         b_w2 = ozaki.lp_product_beta(norm_w * norm_w, n)      # W^2 error x ||W|| vs u ||W||
         b_xw = ozaki.lp_product_beta(nx, n)                   # (X W) error vs u ||W||
-        return ozaki.plan(n, b_w2, b_w2), ozaki.plan(n, b_xw, b_xw)
+        return ozaki.plan(n, b_w2, b_w2, self.gauss), ozaki.plan(n, b_xw, b_xw, self.gauss)
 
     def update(self, restore_full_sigma, sigma_bound=None, norm_y=None, norm_w=None):
         ws, hp, lp, n = self.ws, self.hp, self.lp, self.ws.n
@@ -213,6 +230,8 @@ def sigma_prime_bound(norm_y, norm_w, restore_full_sigma):
 
 
 def make(kind, ws, a):
+    if kind == "ozaki_std":
+        return OzakiProducts(ws, a, gauss=False)
     if kind == "ozaki":
         return OzakiProducts(ws, a)
     if kind == "dmma":

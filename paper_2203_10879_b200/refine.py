@@ -54,8 +54,9 @@ class RefineStatus(enum.Enum):
 @dataclasses.dataclass
 class RefineConfig:
     """refine.py:53-82, plus `precision` ("fp64" | "dd") and `gemm`
-    ("ozaki": int8 tensor-core Ozaki-II products, default; "dmma": FP64
-    DMMA / FP32 SIMT products)."""
+    ("ozaki": int8 tensor-core Ozaki-II products on Gaussian-CRT planes,
+    default; "ozaki_std": the same with (re, im) planes, four real products
+    per complex one; "dmma": FP64 DMMA / FP32 SIMT products)."""
 
     tol_factor: float = 10.0
     max_iters: int = 20
@@ -81,8 +82,8 @@ class RefineConfig:
             raise ValueError("ortho must be an OrthoStrategy")
         if self.precision not in ("fp64", "dd"):
             raise ValueError("precision must be 'fp64' or 'dd'")
-        if self.gemm not in ("ozaki", "dmma"):
-            raise ValueError("gemm must be 'ozaki' or 'dmma'")
+        if self.gemm not in ("ozaki", "ozaki_std", "dmma"):
+            raise ValueError("gemm must be 'ozaki', 'ozaki_std' or 'dmma'")
 
 
 @dataclasses.dataclass

@@ -191,7 +191,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int a_bytes = p.a_planes * PLANE_BYTES;
   // real: one 256-row B plane (TWO: this CTA's 128 rows); complex: 3 planes (TWO: 2)
   const int b_bytes = TWO ? (p.real ? 1 : 2) * PLANE_BYTES : (p.real ? 2 : p.b_planes) * PLANE_BYTES;
-  const int stage_bytes = a_bytes + b_bytes;
+  // 2-SM real products carry two 64-byte k-blocks per ring slot (four MMAs per
+  // barrier round trip, like the complex products): with one k-block per slot
+  // the issuer's per-slot overhead left the tensor pipe ~45 % idle
+  const int kstep = (TWO && p.real) ? 2 : 1;
+  const int stage_bytes = kstep * (a_bytes + b_bytes);
   const int STAGES = p.stages;
   const int tn = p.real ? 2 * TN : TN;
   uint64_t* bars = (uint64_t*)(smem + SMEM_RING);
@@ -317,17 +321,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           apl = g ^ p.a_swap;
           bpl = p.b_gplane ? g : 0;
         }
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = 0; kb < kblocks; kb += kstep) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           uint8_t* st = smem + stage * stage_bytes;
           if (TWO) {
             // both CTAs' bytes complete on the leader's full barrier
             const uint32_t fb = mapa_u32(full_bar(stage), 0);
             if (crank == 0) mbar_expect_tx(full_bar(stage), 2 * stage_bytes);
-            tma_load_4d_2sm(smem_u32(st), &tmap_a, fb, kb * TK, arow, apl, l);
             if (p.real) {
-              tma_load_4d_2sm(smem_u32(st + a_bytes), &tmap_b, fb, kb * TK, nt * tn + crank * TN, bpl, l);
+              // [A kb, A kb+1 | B kb, B kb+1]; a k-block past K is zero-filled by the TMA
+              for (int h = 0; h < kstep; ++h) {
+                tma_load_4d_2sm(smem_u32(st + h * a_bytes), &tmap_a, fb, (kb + h) * TK, arow, apl, l);
+                tma_load_4d_2sm(smem_u32(st + kstep * a_bytes + h * b_bytes), &tmap_b, fb, (kb + h) * TK,
+                                nt * tn + crank * TN, bpl, l);
+              }
             } else {
+              tma_load_4d_2sm(smem_u32(st), &tmap_a, fb, kb * TK, arow, apl, l);
               // encoded B planes: 0 = -im, 1 = re, 2 = im
               tma_load_4d_2sm(smem_u32(st + a_bytes), &tmap_b, fb, kb * TK, nt * TN, crank == 0 ? 1 : 2, l);
               tma_load_4d_2sm(smem_u32(st + a_bytes + PLANE_BYTES), &tmap_b, fb, kb * TK, nt * TN,
@@ -382,7 +391,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(tempty_bar(acc), acc_phase ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const uint32_t d = tmem_base + (uint32_t)(acc * 256);
-      for (int kb = 0; kb < kblocks; ++kb) {
+      for (int kb = 0; kb < kblocks; kb += kstep) {
         mbar_wait(full_bar(stage), phase);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         if (lane == 0) {
@@ -390,16 +399,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t sb = sa + a_bytes;
           if (TWO) {
             const uint32_t id = idesc_i8(256, 256);
+            if (p.real) {
 #pragma unroll
-            for (int ks = 0; ks < TK / 32; ++ks) {
-              const uint32_t acc_flag = (kb | ks) != 0;
-              umma_i8_2sm(d, umma_desc_sw64(sa + ks * 32), umma_desc_sw64(sb + ks * 32), id, acc_flag);
-              if (!p.real)
+              for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int ks = 0; ks < TK / 32; ++ks)
+                  umma_i8_2sm(d, umma_desc_sw64(sa + h * a_bytes + ks * 32),
+                              umma_desc_sw64(sa + 2 * a_bytes + h * b_bytes + ks * 32), id, (kb | h | ks) != 0);
+            } else {
+#pragma unroll
+              for (int ks = 0; ks < TK / 32; ++ks) {
+                const uint32_t acc_flag = (kb | ks) != 0;
+                umma_i8_2sm(d, umma_desc_sw64(sa + ks * 32), umma_desc_sw64(sb + ks * 32), id, acc_flag);
                 umma_i8_2sm(d, umma_desc_sw64(sa + PLANE_BYTES + ks * 32), umma_desc_sw64(sb + PLANE_BYTES + ks * 32),
                             id, 1u);
+              }
             }
             umma_commit_2sm(empty_bar(stage), 3);
-            if (kb == kblocks - 1) umma_commit_2sm(tfull_bar(acc), 3);
+            if (kb + kstep >= kblocks) umma_commit_2sm(tfull_bar(acc), 3);
           } else {
 #pragma unroll
           for (int ks = 0; ks < TK / 32; ++ks) {
@@ -631,8 +648,8 @@ int gemm_launch(int M, int N, int K, int nmod, const int* moduli, const void* a,
   }
   const int tiles = nmod * p.tiles_m * p.tiles_n;
   const bool two = two_sm && cm == 2;
-  if (two) {  // per CTA: its A rows and half of the pair's B operand
-    p.stages = std::min(MAX_STAGES, SMEM_RING / ((p.a_planes + (real ? 1 : 2)) * PLANE_BYTES));
+  if (two) {  // per CTA: its A rows and half of the pair's B operand (real: two k-blocks per slot)
+    p.stages = std::min(MAX_STAGES, SMEM_RING / ((real ? 2 : 1) * (p.a_planes + (real ? 1 : 2)) * PLANE_BYTES));
     if (getenv("SR_OZ_STAGES")) p.stages = std::max(2, std::min(p.stages, atoi(getenv("SR_OZ_STAGES"))));
   }
   p.group_m = (getenv("SR_OZ_GROUP_M") ? atoi(getenv("SR_OZ_GROUP_M")) : (real ? 2 : 1) * GROUP_M) / cm;

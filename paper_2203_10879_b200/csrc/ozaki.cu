@@ -145,8 +145,9 @@ struct EncodeParams {
   int c64[MAXMOD];             // 2^64 mod p, symmetric
   uint32_t bm[MAXMOD];         // Barrett multiplier floor(2^32 / p) + 1
   int off0[MAXMOD], off1[MAXMOD];  // positive shift (a multiple of p), and it minus 2^64 mod p
-  int iota[MAXMOD];                // layout 4: a square root of -1 mod p (symmetric)
-  int offg[MAXMOD];                // layout 4: a multiple of p above |re +- iota im|, minus lo
+  int wgp[MAXMOD][2], wgm[MAXMOD][2];  // layout 4: +-iota 2^(8 c) mod p, symmetric int8, packed 4 per word
+  int cgp[MAXMOD];                 // layout 4: iota 2^64 mod p, symmetric
+  int offg[MAXMOD];                // layout 4: a multiple of p above four byte dot products, minus lo
 };
 
 // balanced 11-bit digits of an integer-valued double (error-free, top-down)
@@ -262,6 +263,35 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
         ng_i[e] = b < 0;
       }
       const bool need_neg = p.layout == 1 || p.layout == 3;  // planes with -im
+      if (p.layout == 4) {
+        // Gaussian planes straight from the bytes: phi+- = re +- iota im mod p is
+        // sum_c u_c(re) (2^(8c) mod p) + u_c(im) (+-iota 2^(8c) mod p) - the
+        // 2^64 corrections of negative values: four byte dot products, one
+        // Barrett reduction per plane (0 <= v < 2^21)
+        for (int l = 0; l < p.nmod; ++l) {
+          const int pm = p.pi[l];
+          const uint32_t bm = p.bm[l];
+          const int lo = -(pm >> 1);
+          const int w0 = p.wb[l][0], w1 = p.wb[l][1], c64 = p.c64[l];
+          const int gp0 = p.wgp[l][0], gp1 = p.wgp[l][1], gm0 = p.wgm[l][0], gm1 = p.wgm[l][1];
+          const int cg = p.cgp[l], og = p.offg[l];
+          int rp[4], rm[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int base = dp4a_us(hi_r[e], w1, dp4a_us(lo_r[e], w0, og - (int)ng_r[e] * c64));
+            const int vp = dp4a_us(hi_i[e], gp1, dp4a_us(lo_i[e], gp0, base - (int)ng_i[e] * cg));
+            const int vm = dp4a_us(hi_i[e], gm1, dp4a_us(lo_i[e], gm0, base + (int)ng_i[e] * cg));
+            int a = vp - (int)__umulhi((uint32_t)vp, bm) * pm;  // in [-p, p)
+            int b = vm - (int)__umulhi((uint32_t)vm, bm) * pm;
+            rp[e] = a - (a >> 31) * pm + lo;
+            rm[e] = b - (b >> 31) * pm + lo;
+          }
+          const uint32_t wp = __byte_perm(__byte_perm(rp[0], rp[1], 0x0040), __byte_perm(rp[2], rp[3], 0x0040), 0x5410);
+          const uint32_t wm = __byte_perm(__byte_perm(rm[0], rm[1], 0x0040), __byte_perm(rm[2], rm[3], 0x0040), 0x5410);
+          store_planes(p, dst, l, mod_stride, mod_stride2, plane_stride, i, k, wp, wm, 0u);
+        }
+        continue;
+      }
       for (int l = 0; l < p.nmod; ++l) {
         const int pm = p.pi[l];
         const uint32_t bm = p.bm[l];
@@ -280,19 +310,6 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
           b = b - (b >> 31) * pm + lo;
           rr[e] = a;
           ri[e] = b;
-        }
-        if (p.layout == 4) {
-          // phi+- = re +- iota im (|.| < 2^14), reduced like the byte sums above
-          const int io = p.iota[l], og = p.offg[l];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int t = ri[e] * io;
-            const int vp = rr[e] + t + og, vm = rr[e] - t + og;
-            int a = vp - (int)__umulhi((uint32_t)vp, bm) * pm;
-            int b = vm - (int)__umulhi((uint32_t)vm, bm) * pm;
-            rr[e] = a - (a >> 31) * pm + lo;
-            ri[e] = b - (b >> 31) * pm + lo;
-          }
         }
         // pack the four low bytes per plane (two byte permutes each)
         const uint32_t wr = __byte_perm(__byte_perm(rr[0], rr[1], 0x0040), __byte_perm(rr[2], rr[3], 0x0040), 0x5410);
@@ -453,7 +470,6 @@ __global__ void __launch_bounds__(256) decode_kernel(const __grid_constant__ Dec
         for (int j = 0; j < NC; ++j) S[e][j] = 0.0;
       const int8_t* r = res + (size_t)(G ? 0 : plane) * p.res_plane + (size_t)i * p.res_pitch + j0;
       const double(*W)[MAXCHUNK] = (G && plane == 1) ? p.w_im : p.w;
-      const double sgn = plane == 0 ? 1.0 : -1.0;  // G: phi+ + phi- (re) or phi+ - phi- (im)
       // residue words in groups of 8 moduli (8 loads in flight, bounded registers)
 #pragma unroll 1
       for (int l0 = 0; l0 < p.nmod; l0 += 8) {
@@ -471,11 +487,18 @@ __global__ void __launch_bounds__(256) decode_kernel(const __grid_constant__ Dec
           // x + 128 in [0, 255]; as the low word of 0x4338000000000000 it reads
           // 1.5 * 2^52 + x + 128, so one DADD recovers x exactly.
           const uint32_t w4 = wv[g] ^ 0x80808080u;
-          const uint32_t m4 = G ? (wm[g] ^ 0x80808080u) : 0u;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            double x = __hiloint2double(0x43380000, (w4 >> (8 * e)) & 0xFF) - 6755399441055872.0;
-            if (G) x = fma(sgn, __hiloint2double(0x43380000, (m4 >> (8 * e)) & 0xFF) - 6755399441055872.0, x);
+            double x;
+            if (G) {
+              // phi+ +- phi- in integers (|.| <= 240), one conversion (the low word
+              // of 1.5 * 2^52 carries x + 2^31)
+              const int bp = (int)(int8_t)(wv[g] >> (8 * e)), bn = (int)(int8_t)(wm[g] >> (8 * e));
+              const int xi = plane == 0 ? bp + bn : bp - bn;
+              x = __hiloint2double(0x43380000, xi ^ 0x80000000) - 6755401588539392.0;
+            } else {
+              x = __hiloint2double(0x43380000, (w4 >> (8 * e)) & 0xFF) - 6755399441055872.0;
+            }
 #pragma unroll
             for (int j = 0; j < NC; ++j) S[e][j] = fma(x, W[l0 + g][j], S[e][j]);  // exact: < 2^53
           }
@@ -702,9 +725,20 @@ int encode_launch(int rows_out, int K, int kind, const void* re, const double* i
       for (int x = 1; x < m && !io; ++x)
         if ((x * x + 1) % m == 0) io = x;
       if (!io || !(m & 1)) return SR_EINVAL;  // needs an odd modulus with a square root of -1
-      p.iota[l] = (int)sym(io);
-      const int half = m >> 1;
-      p.offg[l] = (half + half * half + m - 1) / m * m + half;  // >= |re| + |iota im|, then -lo
+      long long pg = 1;  // 2^(8c) mod m
+      uint32_t wp[2] = {0, 0}, wm[2] = {0, 0};
+      for (int c = 0; c < 8; ++c) {
+        wp[c / 4] |= ((uint32_t)(sym(io * pg) & 0xFF)) << (8 * (c % 4));
+        wm[c / 4] |= ((uint32_t)(sym(m - io * pg % m) & 0xFF)) << (8 * (c % 4));
+        pg = (pg << 8) % m;
+      }
+      p.wgp[l][0] = (int)wp[0];
+      p.wgp[l][1] = (int)wp[1];
+      p.wgm[l][0] = (int)wm[0];
+      p.wgm[l][1] = (int)wm[1];
+      p.cgp[l] = (int)sym(io * pg);  // pg = 2^64 mod m here
+      const int bound = 16 * 255 * (m >> 1) + 2 * (m >> 1);  // |16 byte products| + |corrections|
+      p.offg[l] = (bound + m - 1) / m * m + (m >> 1);        // a multiple of m above it, then -lo
     }
   }
   // K padding columns of the residue planes must read as zero

@@ -275,10 +275,11 @@ def main():
         "roofline": {"bound": "tensor", "kernel": "oz_gemm_kernel (tcgen05 kind::i8)",
                      "achieved": achieved, "peak": int8_peak, "unit": "TOP/s (int8)",
                      "frac": (achieved / int8_peak) if achieved else None,
-                     "traffic": 19.94e9 if n == 8192 else None,
+                     "traffic": 10.39e9 if n == 8192 else None,
                      "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of one hp "
-                                       "complex launch at n=8192, 17 moduli (profiles/r1_oz_gemm_ncu.md, 2-SM "
-                                       "MMAs + dynamic unit queue); algorithmic operand + residue bytes of that launch: 7.7e9",
+                                       "complex launch (T^ = P Q) at n=8192 on Gaussian planes, 19 moduli "
+                                       "(profiles/r1_oz_gemm_gauss_ncu.md); algorithmic operand + residue bytes "
+                                       "of that launch: 7.65e9",
                      "launches": gemm_launches, "avg_launch_ms": gemm_ms / max(gemm_launches, 1),
                      "share_of_step": gemm_ms / total_ms if total_ms else None, "peak_source": peak_src,
                      "algorithmic_ops_per_launch": gemm_ops / max(gemm_launches, 1)},

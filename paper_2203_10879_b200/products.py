@@ -98,6 +98,12 @@ class OzakiProducts:
         dev = ws.q.re_buf.device
         self.hp = ozaki.plan(n, ozaki.HP_BETA, ozaki.HP_BETA, gauss)
         self.lp = ozaki.plan(n, ozaki.LP_BETA, ozaki.LP_BETA, gauss)
+        # the measurement's plans: Q^H Q (hq), P = Q^H A (hp_p), T^ = P Q (hp_t);
+        # with Gaussian planes Q is encoded once, at beta HP_BETA_Q
+        bq = ozaki.HP_BETA_Q if gauss else ozaki.HP_BETA
+        self.hq = ozaki.plan(n, bq, bq, gauss)
+        self.hp_p = ozaki.plan(n, bq, ozaki.HP_BETA, gauss)
+        self.hp_t = ozaki.plan(n, ozaki.HP_BETA, bq, gauss)
         hp, lp = self.hp, self.lp
         bpl = 2 if gauss else 3
         self.ea_qh = None if gauss else ozaki.Encoded(n, n, 2, hp.beta_a, hp.nmod, dev)   # Q^H, A role
@@ -113,9 +119,10 @@ class OzakiProducts:
         self.a = a
         self.eb_a = None
 
-    def _hp(self, ea, eb, out, hermitian=False, **kw):
-        ozaki.gemm_residues(ea, eb, self.hp, self.res, lower_only=hermitian)
-        ozaki.decode(self.res, ea, eb, self.hp, out, hermitian=hermitian, **kw)
+    def _hp(self, ea, eb, out, hermitian=False, pl=None, **kw):
+        pl = pl or self.hp
+        ozaki.gemm_residues(ea, eb, pl, self.res, lower_only=hermitian)
+        ozaki.decode(self.res, ea, eb, pl, out, hermitian=hermitian, **kw)
         _counters["hp_calls"] += 1
 
     def _lp(self, ea, eb, out, hermitian=False):
@@ -141,7 +148,7 @@ class OzakiProducts:
         """Q = Q^ (3I - G) / 2 = Q^ - Q^ (G - I) / 2 (orthogonal.py:167-169)."""
         ws, hp, n = self.ws, self.hp, self.ws.n
         ea_qh = self._encode_q(qhat)                                     # Q^H (A role), Q^ (B role)
-        self._hp(ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True)   # G - I
+        self._hp(ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True, pl=self.hq)  # G - I
         pc = self._correction_plan(ws.fro_norm(ws.y))
         ozaki.encode(qhat, n, n, "a", pc, out=self.ea_x)
         ozaki.encode(ws.y, n, n, "b", pc, out=self.eb_s)
@@ -151,22 +158,22 @@ class OzakiProducts:
         """Q as the B operand (self.eb_q) and Q^H as the A operand (returned):
         Gaussian planes — the same residues with the planes swapped; else one
         dual encode into self.ea_qh."""
-        n, hp = self.ws.n, self.hp
+        n = self.ws.n
         if self.gauss:
-            ozaki.encode(q, n, n, "b", hp, out=self.eb_q)
+            ozaki.encode(q, n, n, "b", self.hq, out=self.eb_q)
             return ozaki.conj_view(self.eb_q)
-        ozaki.encode_dual(q, n, n, hp, self.ea_qh, self.eb_q)
+        ozaki.encode_dual(q, n, n, self.hq, self.ea_qh, self.eb_q)
         return self.ea_qh
 
     def measure(self, a):
         ws, hp, n = self.ws, self.hp, self.ws.n
         ea_qh = self._encode_q(ws.q)                                    # Q^H (A role), Q (B role)
         if self.eb_a is None:
-            self.eb_a = ozaki.encode(self.a, n, n, "b", hp)
-        self._hp(ea_qh, self.eb_a, ws.p)                                # P = Q^H A
-        ozaki.encode(ws.p, n, n, "a", hp, out=self.ea_x)
-        self._hp(self.ea_x, self.eb_q, ws.that)                         # T^ = P Q
-        self._hp(ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True)   # Y = Q^H Q - I
+            self.eb_a = ozaki.encode(self.a, n, n, "b", self.hp_p)
+        self._hp(ea_qh, self.eb_a, ws.p, pl=self.hp_p)                 # P = Q^H A
+        ozaki.encode(ws.p, n, n, "a", self.hp_t, out=self.ea_x)
+        self._hp(self.ea_x, self.eb_q, ws.that, pl=self.hp_t)          # T^ = P Q
+        self._hp(ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True, pl=self.hq)  # Y = Q^H Q - I
 
     def _lp_plans(self, norm_y, norm_w):
         """Plans for the fused update's W^2 and X W (X = Y - W - W^2) from

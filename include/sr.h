@@ -251,12 +251,14 @@ int sr_oz_gemm_i8_gauss(int M, int N, int K, int nmod, const int* moduli, const 
 /* sr_oz_decode for Gaussian residue planes: table = the sr_oz_decode table
    with the weights of the real part (w_l (p_l+1)/2 mod P), followed by
    [nmod][6] weights of the imaginary part (w_l (2 iota_l)^-1 mod P).
-   out_kind SR_MAT_F64 (add: none or SR_MAT_F64) or SR_MAT_C64 (no add). */
+   out_kind SR_MAT_F64 (add: none or SR_MAT_F64) or SR_MAT_C64 (no add).
+   hermitian = 1 (C Hermitian, no add): only the lower 128-tiles are decoded,
+   the strictly upper ones written as their conjugate transpose. */
 int sr_oz_decode_gauss(int M, int N, int nmod, int nchunk, const double* table, const void* res,
                        long long res_pitch, const int* exps_a, int beta_a, const int* exps_b, int beta_b,
                        double alpha, double shift, int add_kind, const double* add_re, const double* add_im,
                        long long ld_add, double add_scale, int out_kind, void* out_re, double* out_im,
-                       long long ld_out, int diag_col0, void* stream);
+                       long long ld_out, int hermitian, int diag_col0, void* stream);
 
 #ifdef __cplusplus
 }

@@ -57,7 +57,7 @@ SIGNATURES = {
                           _p, _p, _p, _p, _ll, _i, _i, _p]),
     "sr_oz_gemm_i8_gauss": (_i, [_i, _i, _i, _i, _p, _p, _i, _ll, _p, _i, _ll, _p, _ll, _i, _i, _p]),
     "sr_oz_decode_gauss": (_i, [_i, _i, _i, _i, _p, _p, _ll, _p, _i, _p, _i, _d, _d, _i, _p, _p, _ll, _d, _i,
-                                _p, _p, _ll, _i, _p]),
+                                _p, _p, _ll, _i, _i, _p]),
 }
 
 _lib = None

@@ -795,7 +795,7 @@ int decode_launch(int M, int N, int nmod, int nchunk, const double* table, const
                   const double* add_im_lo, long long ld_add, double add_scale, int out_kind, void* out_re,
                   double* out_im, double* out_re_lo, double* out_im_lo, long long ld_out, int hermitian,
                   int diag_col0, bool gauss, void* stream) {
-  if (gauss && hermitian != 0) return SR_EINVAL;
+  if (gauss && hermitian < 0) return SR_EINVAL;  // Hermitian only (the GEMM's transpose shortcut)
   if (M <= 0 || N <= 0 || nmod <= 0 || nmod > MAXMOD || nchunk < 1 || nchunk > MAXCHUNK) return SR_EINVAL;
   if (res_pitch & 3) return SR_EINVAL;
   if (out_kind < 0 || out_kind > SR_MAT_DD) return SR_EINVAL;
@@ -849,10 +849,7 @@ int decode_launch(int M, int N, int nmod, int nchunk, const double* table, const
     rc = nchunk <= 2   ? dispatch_gauss<2>(out_kind, add_kind, grid, st, p, r8, exps_a, exps_b, add, out)
          : nchunk <= 4 ? dispatch_gauss<4>(out_kind, add_kind, grid, st, p, r8, exps_a, exps_b, add, out)
                        : dispatch_gauss<6>(out_kind, add_kind, grid, st, p, r8, exps_a, exps_b, add, out);
-    if (rc != SR_OK) return rc;
-    SR_LAUNCH_CHECK();
-    return SR_OK;
-  }
+  } else {
   switch (nchunk) {
     case 1:
     case 2:
@@ -864,6 +861,7 @@ int decode_launch(int M, int N, int nmod, int nchunk, const double* table, const
       break;
     default:
       rc = dispatch_out<6>(out_kind, add_kind, grid, st, p, (const int8_t*)res, exps_a, exps_b, add, out);
+  }
   }
   if (rc != SR_OK) return rc;
   SR_LAUNCH_CHECK();
@@ -896,8 +894,9 @@ extern "C" int sr_oz_decode_gauss(int M, int N, int nmod, int nchunk, const doub
                                   long long res_pitch, const int* exps_a, int beta_a, const int* exps_b, int beta_b,
                                   double alpha, double shift, int add_kind, const double* add_re,
                                   const double* add_im, long long ld_add, double add_scale, int out_kind,
-                                  void* out_re, double* out_im, long long ld_out, int diag_col0, void* stream) {
+                                  void* out_re, double* out_im, long long ld_out, int hermitian, int diag_col0,
+                                  void* stream) {
   return decode_launch(M, N, nmod, nchunk, table, res, res_pitch, exps_a, beta_a, exps_b, beta_b, alpha, shift,
                        add_kind, add_re, add_im, nullptr, nullptr, ld_add, add_scale, out_kind, out_re, out_im,
-                       nullptr, nullptr, ld_out, 0, diag_col0, true, stream);
+                       nullptr, nullptr, ld_out, hermitian, diag_col0, true, stream);
 }

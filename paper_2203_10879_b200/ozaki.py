@@ -327,11 +327,14 @@ def decode(res, ea, eb, pl, out, alpha=1.0, shift=0.0, add=None, add_scale=1.0, 
         a_kind, a_re, a_im, a_rl, a_il, ld_add = -1, None, None, None, None, 0
     else:
         a_kind, a_re, a_im, a_rl, a_il, ld_add, _ = mat_args(add)
-    if pl.gauss:  # both planes are full (the GEMM wrote C- = +-C+^T for Hermitian C)
+    if pl.gauss:
+        # both residue planes are full (the GEMM wrote C- = C+^T for Hermitian C);
+        # Hermitian C: decode the lower 128-tiles, mirror the rest ("skew"
+        # products ran in full and are decoded in full)
         _lib.call("sr_oz_decode_gauss", res.M, res.N, pl.nmod, pl.nchunk, pl.table_ptr(), res.buf.data_ptr(),
                   res.pitch, ea.exps.data_ptr(), ea.beta, eb.exps.data_ptr(), eb.beta, float(alpha), float(shift),
-                  a_kind, a_re, a_im, ld_add, float(add_scale), o_kind, o_re, o_im, ld_out, int(diag_col0),
-                  _stream())
+                  a_kind, a_re, a_im, ld_add, float(add_scale), o_kind, o_re, o_im, ld_out,
+                  1 if herm == 1 else 0, int(diag_col0), _stream())
         return out
     _lib.call("sr_oz_decode", res.M, res.N, pl.nmod, pl.nchunk, pl.table_ptr(), res.buf.data_ptr(), res.pitch,
               ea.exps.data_ptr(), ea.beta, eb.exps.data_ptr(), eb.beta, float(alpha), float(shift), a_kind, a_re,

@@ -94,7 +94,8 @@ def refine_sharded(backend, cfg, group=None, align=128):
 
 
 class OzakiShardBackend:
-    """Column-sharded FP64-mode products on the int8 tensor cores (libsr)."""
+    """Column-sharded FP64-mode products on the int8 tensor cores (libsr),
+    Gaussian-CRT planes (two real products per modulus, ozaki.py)."""
 
     def __init__(self, a, qhat, device):
         self.dev = device
@@ -110,8 +111,8 @@ class OzakiShardBackend:
         red = _lib.load().sr_reduce_workspace_bytes()
         self.red = [torch.zeros(red, dtype=torch.uint8, device=device) for _ in range(4)]
         self.solver = SolverWorkspace(n, torch.complex64, device)
-        self.hp = ozaki.plan(n, ozaki.HP_BETA, ozaki.HP_BETA)
-        self.lp = ozaki.plan(n, ozaki.LP_BETA, ozaki.LP_BETA)
+        self.hp = ozaki.gauss_plan(n, ozaki.HP_BETA, ozaki.HP_BETA)
+        self.lp = ozaki.gauss_plan(n, ozaki.LP_BETA, ozaki.LP_BETA)
         self.ea_a = ozaki.encode(self.a, n, n, "a", self.hp)  # A, A role (Z_J = A Q_J)
 
     # ---- sharding
@@ -122,10 +123,10 @@ class OzakiShardBackend:
         self.zj, self.tj, self.yj, self.sj, self.qj = (ZPlanar.empty(n, w, device=dev) for _ in range(5))
         self.ywj, self.w2j, self.w3j, self.wj = (lp_empty(n, w, device=dev) for _ in range(4))
         self.ea_full = ozaki.Encoded(n, n, 2, hp.beta_a, hp.nmod, dev)
-        self.eb_cols = ozaki.Encoded(w, n, 3, hp.beta_b, hp.nmod, dev)
+        self.eb_cols = ozaki.Encoded(w, n, 2, hp.beta_b, hp.nmod, dev)
         self.res = ozaki.ResidueBuffer(n, w, hp.nmod, dev)
         self.la = ozaki.Encoded(n, n, 2, lp.beta_a, lp.nmod, dev)
-        self.lb = ozaki.Encoded(w, n, 3, lp.beta_b, lp.nmod, dev)
+        self.lb = ozaki.Encoded(w, n, 2, lp.beta_b, lp.nmod, dev)
         self.lres = ozaki.ResidueBuffer(n, w, lp.nmod, dev)
 
     def _cols(self, z):

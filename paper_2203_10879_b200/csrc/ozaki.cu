@@ -281,14 +281,17 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
             const int base = dp4a_us(hi_r[e], w1, dp4a_us(lo_r[e], w0, og - (int)ng_r[e] * c64));
             const int vp = dp4a_us(hi_i[e], gp1, dp4a_us(lo_i[e], gp0, base - (int)ng_i[e] * cg));
             const int vm = dp4a_us(hi_i[e], gm1, dp4a_us(lo_i[e], gm0, base + (int)ng_i[e] * cg));
-            int a = vp - (int)__umulhi((uint32_t)vp, bm) * pm;  // in [-p, p)
-            int b = vm - (int)__umulhi((uint32_t)vm, bm) * pm;
-            rp[e] = a - (a >> 31) * pm + lo;
-            rm[e] = b - (b >> 31) * pm + lo;
+            // v < 2^21: umulhi(v, floor(2^32 / p) + 1) is exactly floor(v / p)
+            // (the multiplier's excess times v stays below 2^32), so v - q p is
+            // already in [0, p)
+            rp[e] = vp - (int)__umulhi((uint32_t)vp, bm) * pm + lo;
+            rm[e] = vm - (int)__umulhi((uint32_t)vm, bm) * pm + lo;
           }
           const uint32_t wp = __byte_perm(__byte_perm(rp[0], rp[1], 0x0040), __byte_perm(rp[2], rp[3], 0x0040), 0x5410);
           const uint32_t wm = __byte_perm(__byte_perm(rm[0], rm[1], 0x0040), __byte_perm(rm[2], rm[3], 0x0040), 0x5410);
-          store_planes(p, dst, l, mod_stride, mod_stride2, plane_stride, i, k, wp, wm, 0u);
+          int8_t* dm = dst + (size_t)l * mod_stride;
+          *reinterpret_cast<uint32_t*>(dm) = wp;
+          *reinterpret_cast<uint32_t*>(dm + plane_stride) = wm;
         }
         continue;
       }
@@ -304,12 +307,9 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
           // negative): 0 <= v < 2^20; u = v mod p by Barrett, r = u + lo symmetric
           const int vr = dp4a_us(hi_r[e], w1, dp4a_us(lo_r[e], w0, o0 - (int)ng_r[e] * c64));
           const int vi = dp4a_us(hi_i[e], w1, dp4a_us(lo_i[e], w0, o0 - (int)ng_i[e] * c64));
-          int a = vr - (int)__umulhi((uint32_t)vr, bm) * pm;  // in [-p, p)
-          int b = vi - (int)__umulhi((uint32_t)vi, bm) * pm;
-          a = a - (a >> 31) * pm + lo;  // [0, p) + lo
-          b = b - (b >> 31) * pm + lo;
-          rr[e] = a;
-          ri[e] = b;
+          // v < 2^20: the Barrett quotient is exact, v - q p is in [0, p)
+          rr[e] = vr - (int)__umulhi((uint32_t)vr, bm) * pm + lo;
+          ri[e] = vi - (int)__umulhi((uint32_t)vi, bm) * pm + lo;
         }
         // pack the four low bytes per plane (two byte permutes each)
         const uint32_t wr = __byte_perm(__byte_perm(rr[0], rr[1], 0x0040), __byte_perm(rr[2], rr[3], 0x0040), 0x5410);

@@ -48,13 +48,16 @@ constexpr int KB_H = 32;                           // fp16 per 64-byte K block
 constexpr int NKB = BW * NB * 2 / KB_H;            // 8 K blocks per strip
 // persistent CTAs, one per SM; 4 stages keep 130 KB of shared memory so a
 // critical-path SOLVE CTA (84 KB) still fits beside it on the same SM
-constexpr int TC_STAGES = 4;
+#ifndef SR_FAR_STAGES
+#define SR_FAR_STAGES 3
+#endif
+constexpr int TC_STAGES = SR_FAR_STAGES;
 constexpr int A_PLANE = 128 * 64;                  // bytes: 128 rows x 64 B
 constexpr int B_PLANE = 64 * 64;                   // bytes: 64 rows x 64 B
 constexpr int TC_STAGE = 2 * A_PLANE + 2 * B_PLANE;
 constexpr int TC_THREADS = 192;
 constexpr uint32_t TC_TMEM_COLS = 128;             // two 64-column accumulators
-constexpr int EPI_BYTES = 4 * 32 * 33 * 8;          // COL epilogue staging (4 warps x 32 x 33 float2)
+constexpr int EPI_BYTES = 2 * 4 * 32 * 33 * 8;      // epilogue staging, double-buffered (2 x 4 warps x 32 x 33 float2)
 constexpr int TC_SMEM = 1024 + TC_STAGES * TC_STAGE + EPI_BYTES + 256;
 
 // exponent e with max < 2^e (0 for an all-zero line): the line is scaled by 2^-e
@@ -340,7 +343,27 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
     const int ew = warp & 3;
     const int n = p.n;
     const long long ld = p.ld;
-    float2* buf = stage_buf + ew * 32 * 33;
+    // two staging blocks per warp: the Rf block of unit k+1 is loaded while
+    // unit k is folded (the RMW was latency-bound on one 32 KB block in flight
+    // per SM)
+    float2* bufs[2] = {stage_buf + ew * 32 * 33, stage_buf + (4 + ew) * 32 * 33};
+    auto issue_rf = [&](int uu, float2* dstb) {
+      int line_, t0_, a_row0_, b_row0_, k0_;
+      unit(uu, line_, t0_, a_row0_, b_row0_, k0_);
+      const int R0_ = !ROW ? a_row0_ + ew * 32 : line_ * NB;
+      const int C0_ = !ROW ? line_ * NB : a_row0_ + ew * 32;
+      const bool okc = (t0_ + ew < p.h) && C0_ + lane < n;
+#pragma unroll 8
+      for (int r = 0; r < NB; ++r) {
+        const bool ok = okc && R0_ + r < n;
+        const float2* src = Rf + (ok ? (size_t)(R0_ + r) * ld + C0_ + lane : 0);
+        const uint32_t dst = smem_u32(dstb + r * 33 + lane);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0)
+                     : "memory");
+      }
+    };
+    if ((int)blockIdx.x < units) issue_rf(blockIdx.x, bufs[0]);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
     int k = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++k) {
       const int acc = k & 1;
@@ -355,27 +378,18 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
       __syncwarp();
       const int tgt = t0 + ew;  // target tile index along the line
       const bool live = tgt < p.h;
-      // prefetch this unit's Rf block into the warp's shared staging block
-      // (cp.async, zero-filled outside the matrix) before waiting for the
-      // accumulator: the loads overlap the unit's MMAs (targets of different
-      // units never overlap, so nothing in flight writes them).  Shared
-      // memory instead of registers keeps the kernel at <= 216 registers.
-      // buf[r][c] = Rf[R0 + r][C0 + c]: COL (R0, C0) = (target rows, line
-      // column block); ROW = (line row block, target columns)
+      // this unit's Rf block was prefetched into bufs[k & 1] (cp.async,
+      // zero-filled outside the matrix) one unit ahead; start the next unit's
+      // now, so two blocks are in flight while the MMAs run (targets of
+      // different units never overlap, so nothing in flight writes them).
+      // Shared memory instead of registers keeps the kernel at <= 216
+      // registers.  buf[r][c] = Rf[R0 + r][C0 + c]: COL (R0, C0) = (target
+      // rows, line column block); ROW = (line row block, target columns)
+      float2* buf = bufs[k & 1];
       const int R0 = !ROW ? a_row0 + ew * 32 : line * NB;
       const int C0 = !ROW ? line * NB : a_row0 + ew * 32;
-      {
-        const bool okc = live && C0 + lane < n;
-#pragma unroll 8
-        for (int r = 0; r < NB; ++r) {
-          const bool ok = okc && R0 + r < n;
-          const float2* src = Rf + (ok ? (size_t)(R0 + r) * ld + C0 + lane : 0);
-          const uint32_t dst = smem_u32(buf + r * 33 + lane);
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0)
-                       : "memory");
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-      }
+      if (u + (int)gridDim.x < units) issue_rf(u + (int)gridDim.x, bufs[(k + 1) & 1]);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
       mbar_wait(tfull_bar(acc), (k >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       uint32_t v[64];
@@ -387,7 +401,7 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
       asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       mbar_arrive(tempty_bar(acc));  // the accumulator is in registers: release it to the MMA warp
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // all but the next unit's block
       __syncwarp();
       if (live) {
         if (!ROW) {
@@ -418,7 +432,7 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
           }
         }
       }
-      __syncwarp();  // buf is refilled by the next unit's prefetch
+      __syncwarp();  // buf is refilled by the prefetch two units on
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");

@@ -240,7 +240,7 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
     far_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                   const __grid_constant__ FarTcArgs p, float2* __restrict__ Rf) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ int eb_s[4][32];
+  __shared__ float eb_s[4][32];  // 2^(e_b) of the tile's B lines
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   float2* stage_buf = reinterpret_cast<float2*>(smem + TC_STAGES * TC_STAGE);  // COL epilogue staging, 4 x 32 x 33
   uint64_t* bars = (uint64_t*)(smem + TC_STAGES * TC_STAGE + EPI_BYTES);
@@ -374,7 +374,12 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
       const int ea = idx < n ? line_exp(p.a_max[idx]) : 0;
       const int jl = line * NB + lane;
       __syncwarp();
-      eb_s[ew][lane] = jl < n ? line_exp(max4(p.b_max, (size_t)n, jl)) : 0;
+      // the epilogue scale 2^(e_a + e_b) as a product of two powers of two, one
+      // multiply per entry instead of an ldexpf (2^e is exact for line maxima
+      // in [2^-127, 2^127), i.e. every complex64 line that is neither
+      // subnormal nor within a factor 2 of overflow)
+      eb_s[ew][lane] = ldexpf(1.f, jl < n ? line_exp(max4(p.b_max, (size_t)n, jl)) : 0);
+      const float fa = ldexpf(1.f, ea);
       __syncwarp();
       const int tgt = t0 + ew;  // target tile index along the line
       const bool live = tgt < p.h;
@@ -409,7 +414,7 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
           // block, then the block stored row by row (coalesced 256-byte rows)
 #pragma unroll
           for (int c = 0; c < NB; ++c) {
-            const float sc = ldexpf(1.f, ea + eb_s[ew][c]);
+            const float sc = fa * eb_s[ew][c];
             float2& q = buf[lane * 33 + c];
             q = make_float2(q.x - __uint_as_float(v[2 * c]) * sc, q.y - __uint_as_float(v[2 * c + 1]) * sc);
           }
@@ -424,7 +429,7 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
 #pragma unroll
           for (int i = 0; i < NB; ++i) {
             if (R0 + i < n) {
-              const float sc = ldexpf(1.f, ea + eb_s[ew][i]);
+              const float sc = fa * eb_s[ew][i];
               const float2 q = buf[i * 33 + lane];
               Rf[(size_t)(R0 + i) * ld + idx] = make_float2(q.x + __uint_as_float(v[2 * i]) * sc,
                                                             q.y + __uint_as_float(v[2 * i + 1]) * sc);

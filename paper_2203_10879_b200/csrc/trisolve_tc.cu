@@ -63,6 +63,12 @@ constexpr int TC_SMEM = 1024 + TC_STAGES * TC_STAGE + EPI_BYTES + 256;
 // exponent e with max < 2^e (0 for an all-zero line): the line is scaled by 2^-e
 __device__ __forceinline__ int line_exp(float mx) { return mx > 0.f ? ilogbf(mx) + 1 : 0; }
 
+// x * 2^k: one multiply by an exact power of two for |k| <= 126 (every line
+// scale of non-extreme data), ldexpf beyond (no overflow of the factor)
+__device__ __forceinline__ float scale_pow2(float x, int k) {
+  return (k >= -126 && k <= 126) ? x * __int_as_float((k + 127) << 23) : ldexpf(x, k);
+}
+
 __device__ __forceinline__ void put_h2(__half* base, size_t plane, size_t off, float x, float y) {
   const __half2 h = __floats2half2_rn(x, y);
   const float2 hf = __half22float2(h);
@@ -113,7 +119,7 @@ __global__ void __launch_bounds__(256) tforms_kernel(int n, const float2* __rest
     if (gr < n && gc < n) {
       v = T[(size_t)gr * ld + gc];
       const int e = line_exp(rmax[gr]);
-      put_h2(tf, plane, (size_t)gr * P + 2 * gc, ldexpf(v.x, -e), ldexpf(v.y, -e));
+      put_h2(tf, plane, (size_t)gr * P + 2 * gc, scale_pow2(v.x, -e), scale_pow2(v.y, -e));
     }
     s[r][tx] = v;
   }
@@ -123,7 +129,7 @@ __global__ void __launch_bounds__(256) tforms_kernel(int n, const float2* __rest
     if (gr < n && gc < n) {
       const float2 v = s[tx][r];
       const int e = line_exp(cmax[gr]);
-      put_h2(ttf, plane, (size_t)gr * P + 2 * gc, ldexpf(v.x, -e), ldexpf(v.y, -e));
+      put_h2(ttf, plane, (size_t)gr * P + 2 * gc, scale_pow2(v.x, -e), scale_pow2(v.y, -e));
     }
   }
 }
@@ -186,7 +192,7 @@ __global__ void __launch_bounds__(256) lforms_kernel(int n, int N, int b, const 
     const int C = M * NB + c, K = I * NB + tx;
     if (C < n && K < n) {
       const float2 v = s[tx][c];
-      const float x = ldexpf(v.x, -ec[c]), y = ldexpf(v.y, -ec[c]);
+      const float x = scale_pow2(v.x, -ec[c]), y = scale_pow2(v.y, -ec[c]);
       put_h2(lb, plane, (size_t)(2 * C) * P + 2 * K, x, -y);
       put_h2(lb, plane, (size_t)(2 * C + 1) * P + 2 * K, y, x);
     }
@@ -195,7 +201,7 @@ __global__ void __launch_bounds__(256) lforms_kernel(int n, int N, int b, const 
     const int R = I * NB + i, K = M * NB + tx;
     if (R < n && K < n) {
       const float2 v = s[i][tx];
-      const float x = ldexpf(v.x, -er[i]), y = ldexpf(v.y, -er[i]);
+      const float x = scale_pow2(v.x, -er[i]), y = scale_pow2(v.y, -er[i]);
       put_h2(lc, plane, (size_t)(2 * R) * P + 2 * K, x, -y);
       put_h2(lc, plane, (size_t)(2 * R + 1) * P + 2 * K, y, x);
     }

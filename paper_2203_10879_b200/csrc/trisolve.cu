@@ -866,7 +866,10 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
       return rc;
     }
     if (ce != cudaSuccess) return sr_set_cuda_error(ce, "cudaStreamEndCapture(trisolve)");
-    const cudaError_t ie = cudaGraphInstantiate(&c.exec, g, 0);
+    // node priorities as captured (SOLVE > NEAR > far), so the block scheduler
+    // keeps preferring the critical path inside the graph too (SR_SOLVE_GRAPH_FLAT=1: off)
+    const cudaError_t ie = cudaGraphInstantiateWithFlags(
+        &c.exec, g, getenv("SR_SOLVE_GRAPH_FLAT") ? 0 : cudaGraphInstantiateFlagUseNodePriority);
     cudaGraphDestroy(g);
     if (ie != cudaSuccess) {
       c.exec = nullptr;

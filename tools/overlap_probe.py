@@ -20,9 +20,8 @@ e[:, :n] = torch.tril(torch.randn(n, n, device="cuda", generator=g, dtype=torch.
 work = SolverWorkspace(n)
 q = ZPlanar.from_any(torch.linalg.qr(torch.randn(n, n, dtype=torch.complex128, device="cuda", generator=g))[0])
 y = ZPlanar.empty(n)
-hp = ozaki.plan(n, ozaki.HP_BETA, ozaki.HP_BETA)
-ea = ozaki.Encoded(n, n, 2, hp.beta_a, hp.nmod, "cuda")
-eb = ozaki.Encoded(n, n, 3, hp.beta_b, hp.nmod, "cuda")
+hp = ozaki.gauss_plan(n, ozaki.HP_BETA, ozaki.HP_BETA)
+eb = ozaki.Encoded(n, n, 2, hp.beta_b, hp.nmod, "cuda")
 res = ozaki.ResidueBuffer(n, n, hp.nmod, "cuda")
 s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
 
@@ -32,7 +31,8 @@ def solve():
 
 
 def gram(sms):
-    ozaki.encode_dual(q, n, n, hp, ea, eb)
+    ozaki.encode(q, n, n, "b", hp, out=eb)  # Gaussian planes: one encoding for Q and Q^H
+    ea = ozaki.conj_view(eb)
     ozaki.gemm_residues(ea, eb, hp, res, lower_only=True, num_sms=sms)
     ozaki.decode(res, ea, eb, hp, y, shift=-1.0, hermitian=True)
 
@@ -64,7 +64,7 @@ def both(sms):
 
 ts = timed(solve)
 print("n=%d solve alone %.2f ms" % (n, ts), flush=True)
-for sms in (148, 120, 96, 72, 48):
+for sms in (148, 128, 112, 96, 72):
     tg = timed(lambda: gram(sms))
     tb = timed(lambda: both(sms))
     print("gram on %3d SMs alone %.2f ms; solve + gram concurrently %.2f ms (sequential %.2f)" % (

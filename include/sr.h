@@ -238,8 +238,9 @@ int sr_oz_decode(int M, int N, int nmod, int nchunk, const double* table, const 
    A operand of X^H with a_swap = 1).  Replace the same matmul_hp / matmul_lp
    call sites (matmul.py:52-110) as the entries above. */
 
-/* R[l][g] = A[l][g ^ a_swap] B[l][b_planes == 2 ? g : 0]^T mod p_l, g = 0, 1
-   (b_planes = 1: a real B operand, layout 2).  herm = +1 / -1 (M == N,
+/* R[l][g] = A[l][g ^ sa] B[l][b_planes == 2 ? g ^ sb : 0]^T mod p_l, g = 0, 1,
+   with sa = a_swap & 1, sb = (a_swap >> 1) & 1 (swapped planes read the
+   operand as its conjugate; b_planes = 1: a real B operand, layout 2).  herm = +1 / -1 (M == N,
    b_planes == 2, C Hermitian / skew-Hermitian): only plane 0 is multiplied and
    plane 1 is written as +-(plane 0)^T, since C- = +-C+^T.  Valid when the
    INTEGER product is (skew-)Hermitian: row i of A and column i of B scaled

@@ -62,7 +62,8 @@ struct OzParams {
   int units_per_mod;            //   order (mp | nt << 16), so every cluster gets only real work
   int stages;                   // ring slots in use
   int gauss;                    // Gaussian planes: tile plane g = mt / tpp (real product of A plane g ^ a_swap
-  int a_swap, b_gplane, tpp;    //   with B plane g, or B plane 0 when b_gplane = 0), output plane g
+  int a_swap, b_gplane, tpp;    //   with B plane g ^ b_swap, or B plane 0 when b_gplane = 0), output plane g
+  int b_swap;
   int herm;                     // gauss, Hermitian (+1) / skew (-1) C: only plane 0 is computed, and the
                                 //   epilogue also writes herm * its transpose as plane 1 (C- = +-C+^T)
   long long out_pitch;          // bytes between output rows
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int g = mt / p.tpp;
           arow = (mt - g * p.tpp) * TM;
           apl = g ^ p.a_swap;
-          bpl = p.b_gplane ? g : 0;
+          bpl = p.b_gplane ? (g ^ p.b_swap) : 0;
         }
         for (int kb = 0; kb < kblocks; kb += kstep) {
           mbar_wait(empty_bar(stage), phase ^ 1);
@@ -611,7 +612,8 @@ int gemm_launch(int M, int N, int K, int nmod, const int* moduli, const void* a,
   const int planes_out = herm ? 1 : 2;
   if (gauss) {
     p.gauss = 1;
-    p.a_swap = a_swap ? 1 : 0;
+    p.a_swap = a_swap & 1;        // bit 0: A planes swapped (X^H from X's B operand)
+    p.b_swap = (a_swap >> 1) & 1;  // bit 1: B planes swapped
     p.b_gplane = b_planes == 2 ? 1 : 0;
     p.herm = herm;
     p.tpp = p.tiles_m;

@@ -294,8 +294,11 @@ def gemm_residues(ea, eb, pl, res, lower_only=False, num_sms=0):
         # encoding) and W W (W skew-Hermitian: row and column maxima agree),
         # not for W^2 W, so "skew" products run in full.
         herm = 1 if (lower_only and lower_only != "skew") else 0
+        if eb.swap and eb.planes != 2:
+            raise ValueError("a swapped B operand needs Gaussian planes")
+        swaps = (1 if ea.swap else 0) | (2 if eb.swap else 0)
         _lib.call("sr_oz_gemm_i8_gauss", ea.rows, eb.rows, ea.K, pl.nmod, pl.moduli_ptr(), ea.buf.data_ptr(),
-                  1 if ea.swap else 0, ea.kp, eb.buf.data_ptr(), eb.planes, eb.kp, res.buf.data_ptr(), res.pitch,
+                  swaps, ea.kp, eb.buf.data_ptr(), eb.planes, eb.kp, res.buf.data_ptr(), res.pitch,
                   herm, int(num_sms), _stream())
     else:
         _lib.call("sr_oz_gemm_i8", ea.rows, eb.rows, ea.K, pl.nmod, pl.moduli_ptr(), ea.buf.data_ptr(), ea.planes,

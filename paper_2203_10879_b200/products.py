@@ -128,9 +128,9 @@ class OzakiProducts:
     def _lp(self, ea, eb, out, hermitian=False):
         self._lp_with(self.lp, ea, eb, out, hermitian)
 
-    def _lp_with(self, pl, ea, eb, out, hermitian=False):
+    def _lp_with(self, pl, ea, eb, out, hermitian=False, alpha=1.0):
         ozaki.gemm_residues(ea, eb, pl, self.lres, lower_only=hermitian if hermitian == "skew" else bool(hermitian))
-        ozaki.decode(self.lres, ea, eb, pl, out, hermitian=hermitian)
+        ozaki.decode(self.lres, ea, eb, pl, out, alpha=alpha, hermitian=hermitian)
         _counters["lp_calls"] += 1
 
     def _correction_plan(self, bound):
@@ -193,15 +193,26 @@ class OzakiProducts:
         if not restore_full_sigma:
             p_w2, p_xw = self._lp_plans(norm_y, norm_w)
             # two lp products instead of three: X W = YW - W^2 - W^3 with X = Y - W - W^2
-            ozaki.encode(ws.w_lp, n, n, "b", p_w2, out=self.lb)           # W, B role
-            ozaki.encode(ws.w_lp, n, n, "a", p_w2, out=self.la)
-            self._lp_with(p_w2, self.la, self.lb, ws.w2, hermitian=True)  # W^2 (W skew-Hermitian)
+            if self.gauss:
+                # W is exactly skew-Hermitian (sr_skew_c64): column j of W is -conj(row j),
+                # with the same scale, so W's B operand is its A operand with the
+                # Gaussian planes swapped and negated — one encoding of W, the
+                # sign folded into the decode (alpha = -1)
+                ozaki.encode(ws.w_lp, n, n, "a", p_w2, out=self.lb)       # W, A role
+                self._lp_with(p_w2, self.lb, ozaki.conj_view(self.lb), ws.w2, hermitian=True, alpha=-1.0)  # W^2
+            else:
+                ozaki.encode(ws.w_lp, n, n, "b", p_w2, out=self.lb)       # W, B role
+                ozaki.encode(ws.w_lp, n, n, "a", p_w2, out=self.la)
+                self._lp_with(p_w2, self.la, self.lb, ws.w2, hermitian=True)  # W^2 (W skew-Hermitian)
             _lib.call("sr_fused_lp_operand_c64", n, ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld, ws.w_lp.data_ptr(),
                       ws.w2.data_ptr(), ws.w_lp.shape[1], ws.y_lp.data_ptr(), _stream())
             if p_xw is not p_w2:
-                ozaki.encode(ws.w_lp, n, n, "b", p_xw, out=self.lb)
+                ozaki.encode(ws.w_lp, n, n, "a" if self.gauss else "b", p_xw, out=self.lb)
             ozaki.encode(ws.y_lp, n, n, "a", p_xw, out=self.la)
-            self._lp_with(p_xw, self.la, self.lb, ws.yw)                 # X W
+            if self.gauss:
+                self._lp_with(p_xw, self.la, ozaki.conj_view(self.lb), ws.yw, alpha=-1.0)  # X W
+            else:
+                self._lp_with(p_xw, self.la, self.lb, ws.yw)             # X W
             _sigma(ws, False, False, fused=True)                         # S' = S - 2I
         else:
             ozaki.encode(ws.w_lp, n, n, "b", lp, out=self.lb)            # W, B role (all lp products)

@@ -203,7 +203,8 @@ GMODS = [241, 233, 229, 221]
 
 @pytest.mark.parametrize("M,N,K,b_planes,a_swap,herm", [
     (128, 128, 64, 2, 0, 0), (200, 130, 100, 2, 1, 0), (256, 384, 512, 1, 0, 0), (77, 300, 1000, 1, 1, 0),
-    (300, 300, 129, 2, 1, 1), (129, 129, 70, 2, 0, -1), (384, 384, 256, 2, 0, 1)])
+    (300, 300, 129, 2, 1, 1), (129, 129, 70, 2, 0, -1), (384, 384, 256, 2, 0, 1), (200, 300, 96, 2, 2, 0),
+    (256, 256, 128, 2, 3, 0), (300, 300, 64, 2, 2, 1)])
 def test_oz_gemm_gauss_bit_exact(M, N, K, b_planes, a_swap, herm):
     rng = np.random.default_rng(M * 3 + N + K + herm)
     kp = ozaki.kpitch(K)
@@ -221,7 +222,9 @@ def test_oz_gemm_gauss_bit_exact(M, N, K, b_planes, a_swap, herm):
     assert rc is None or rc == 0
     got = out.cpu().numpy()[:, :, :, :N].astype(np.int64)
     for l, p in enumerate(GMODS):
-        c = [a[l, g ^ a_swap].astype(np.int64) @ b[l, g if b_planes == 2 else 0].astype(np.int64).T for g in (0, 1)]
+        sa, sb = a_swap & 1, (a_swap >> 1) & 1  # bit 1: B planes swapped
+        c = [a[l, g ^ sa].astype(np.int64) @ b[l, (g ^ sb) if b_planes == 2 else 0].astype(np.int64).T
+             for g in (0, 1)]
         assert np.array_equal(got[l, 0], sym_mod(c[0], p)), (l, p)
         if herm:
             assert np.array_equal(got[l, 1], sym_mod(herm * c[0].T, p)), (l, p)

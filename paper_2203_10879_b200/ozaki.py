@@ -9,12 +9,18 @@ picks the smallest r with  prod(p_l) >= 2 * 2K * 2^(beta_a + beta_b): the
 complex entries of C' are sums of 2K products below 2^(beta_a + beta_b), so
 |C'| < prod / 2 and the symmetric CRT representative is C' itself.
 
+Gaussian plans (OzPlan(gauss=True), the FP64-mode default): moduli with a
+square root iota of -1, complex operands stored as (x + iota y, x - iota y)
+mod p, so a complex product is two real products per modulus (one for a
+Hermitian result) and the conjugate of an operand is the same residues with
+the planes swapped (conj_view).  DESIGN.md §3.0.
+
 Where it sits in the reference: it replaces matmul_hp / matmul_lp
 (/root/reference/pkg/src/ddschur/matmul.py:52-110) — in FP64 mode (hp = FP64,
-beta 60; lp = complex64, beta 26) and in dd mode (hp = double-double, beta
-104; lp = binary64, beta 55) — and generalises the reference's own Ozaki-I
-dd path (_ozaki_gemm_hp, matmul.py:151-212), which splits into FP64 slices
-multiplied by BLAS.
+beta 58; lp = complex64, beta 24, fewer bits for the correction products) and
+in dd mode (hp = double-double, beta 102; lp = binary64, beta 55) — and
+generalises the reference's own Ozaki-I dd path (_ozaki_gemm_hp,
+matmul.py:151-212), which splits into FP64 slices multiplied by BLAS.
 """
 import math
 

@@ -290,7 +290,7 @@ __device__ __forceinline__ unsigned tile_solve_cta(const C* sT2, const C* sD, co
     pend[k] = (c >= 0) ? sR[i * LD + c] : czero<C>();
     tr[k] = (i + d < NB) ? sT2[i * LD + i + d] : czero<C>();
   }
-#pragma unroll 2
+#pragma unroll 4
   for (int t = 0; t < 2 * NB - 1; ++t) {
     const int j = t - (NB - 1) + i;  // this lane's column at step t
     if (w == 0) {

@@ -486,7 +486,9 @@ __device__ __forceinline__ void finish_store(const DecodeParams& p, const double
 // accumulator sets of four columns: 150 registers, 3.4 vs 3.1 ms for an
 // n = 8192 hp decode).
 template <int NC, int OUT, int ADD, bool G = false>
-__global__ void __launch_bounds__(256) decode_kernel(const __grid_constant__ DecodeParams p,
+// (Gaussian: at most 80 registers, three CTAs per SM — 2.68 -> 2.48 ms for an
+// n = 8192 hp decode despite a few spilled words)
+__global__ void __launch_bounds__(256, G ? 3 : 1) decode_kernel(const __grid_constant__ DecodeParams p,
                                                      const int8_t* __restrict__ res, const int* __restrict__ ea,
                                                      const int* __restrict__ eb, Src add, Dst out) {
   constexpr bool ONE = G;                    // both Gaussian planes in one pass

@@ -16,9 +16,13 @@ copies of A, Q̂ and the device->host copies of Q, T inside the timed region.
 N > 1 (torchrun, one rank per GPU): one refinement of the same matrix,
 every product sharded by output columns over the ranks with NCCL all-gathers
 (paper_2203_10879_b200/sharded.py) — strong scaling; the time
-is the max over ranks.  --impl reference times the CPU oracle port of the reference loop
-(oracle/refine_fp64.py: numpy BLAS + the C restatement of the reference
-solver) on a bounded sample of the same workload, on rank 0 only.
+is the max over ranks.  --impl reference times the CPU port of the reference
+loop (oracle/refine_fp64.py: numpy/OpenBLAS products + oracle/trisolve_blas.py,
+the BLAS-backed port of the reference solver) on ONE real refinement of this
+same n = 8192 workload, on rank 0 only (minutes of CPU time, so one step).
+The GPU arm's line also carries `cpu_baseline` (the port's phases measured on
+one n = 4096 refinement, composed for this run) and `config2`, a same-process
+head-to-head of both arms on BASELINE config 2 (n = 2048).
 """
 import argparse
 import json
@@ -35,52 +39,79 @@ sys.path.insert(0, REPO)
 
 METRIC = "time-to-refine (s), n=8192 complex FP32->FP64 (config 3)"
 U64 = 2.0 ** -53
-SAMPLE_N = 1024  # CPU sample size (same workload family, O(n^3) extrapolated)
+SAMPLE_N = 4096  # cpu_baseline sample: one full CPU refinement at this size, phases scaled to n
 
 
-def parse():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=8192)
-    ap.add_argument("--gemm", default="ozaki", choices=["ozaki", "ozaki_std", "dmma"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+def blas_threads():
+    try:
+        import threadpoolctl
+        return max((d.get("num_threads") or 0) for d in threadpoolctl.threadpool_info() if d.get("user_api") == "blas")
+    except Exception:  # noqa: BLE001
+        return None
 
 
-def dist_env():
-    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
-
-
-def log(*a):
-    print(*a, file=sys.stderr, flush=True)
-
-
-def workload(n, seed):
-    from paper_2203_10879_b200 import inputs
-    a = inputs.gaussian_real(n, seed)
-    t0 = time.time()
-    q = inputs.cached_qhat("c3_n%d_s%d" % (n, seed), a)
-    log("[bench] Q^ (complex64 Schur of A, n=%d) ready in %.1f s" % (n, time.time() - t0))
-    return a, q
-
-
-def cpu_oracle_sample(steps, n_full):
-    """Time the oracle port on SAMPLE_N real-Gaussian config-3-type inputs;
-    returns list of extrapolated seconds (x (n_full / SAMPLE_N)^3)."""
+def cpu_refine(a, q, n, solver="blas"):
+    """One refinement by the CPU port of the reference loop (oracle/refine_fp64.py;
+    BLAS hp / lp products, the BLAS-backed port of the reference solver)."""
     from oracle.refine_fp64 import refine_template_fp64
+    t0 = time.perf_counter()
+    out = refine_template_fp64(a, q, tol_factor=10.0 / n, max_iters=10, solver=solver)
+    return time.perf_counter() - t0, out
+
+
+def cpu_composed(n_full, iterations, skip_fired):
+    """cpu_baseline of the GPU arm: ONE full CPU refinement of the config-3
+    workload family at SAMPLE_N (real, measured), its per-phase times
+    (entry, one measurement, one solve, one update) scaled by (n/SAMPLE_N)^3
+    and composed with the GPU run's own phase counts at n."""
     from paper_2203_10879_b200 import inputs
     a = inputs.gaussian_real(SAMPLE_N, 0)
     q = inputs.cached_qhat("c3_n%d_s0" % SAMPLE_N, a).astype(np.complex128)
+    wall, out = cpu_refine(a, q, SAMPLE_N)
+    ph, k = out["phases"], out["iterations"]
+    n_upd = k - (1 if out["skip_fired"] else 0)
+    per = dict(entry=ph["entry"], measure=ph["measure"] / k, solve=ph["solve"] / k,
+               update=ph["update"] / max(n_upd, 1))
     scale = (n_full / SAMPLE_N) ** 3
-    vals, out = [], None
-    for _ in range(steps):
+    upd_full = iterations - (1 if skip_fired else 0)
+    v = scale * (per["entry"] + iterations * (per["measure"] + per["solve"]) + upd_full * per["update"])
+    sample = ("CPU port of the reference loop (oracle/refine_fp64.py, BLAS products, BLAS-backed port of "
+              "trisolve.py) on one full config-3-family refinement at n=%d (%.1f s, %d iterations, %s): its "
+              "per-phase times x (n/%d)^3, composed with this run's phase counts at n=%d (%d iterations, skip=%s); "
+              "the --impl reference arm times a real n=%d refinement"
+              % (SAMPLE_N, wall, k, out["status"], SAMPLE_N, n_full, iterations, skip_fired, n_full))
+    return v, sample
+
+
+def config2_head_to_head(cfg, dev):
+    """BASELINE config 2 (n = 2048 complex Gaussian, complex64-Schur start),
+    both arms on the same inputs in the same process: GPU time-to-refine
+    (inputs resident, median of 5 after a warm-up) and one full CPU
+    refinement by the port (all host threads)."""
+    import dataclasses
+
+    import torch
+
+    from paper_2203_10879_b200 import ZPlanar, inputs, refine_template
+    a, q = inputs.config_inputs(2)
+    n = a.shape[0]
+    c2 = dataclasses.replace(cfg, tol_factor=10.0 / n)
+    A, Q = ZPlanar.from_any(a, device=dev), ZPlanar.from_any(q, device=dev)
+    ts = []
+    for i in range(6):
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        out = refine_template_fp64(a, q, tol_factor=10.0 / SAMPLE_N, max_iters=10)
-        vals.append((time.perf_counter() - t0) * scale)
-    return vals, out
+        pair, rep = refine_template(A, Q, c2, device=dev)
+        torch.cuda.synchronize()
+        if i:
+            ts.append(time.perf_counter() - t0)
+    cpu_s, out = cpu_refine(a, q, n)
+    g = float(np.median(ts))
+    return {"n": n, "gpu_s": g, "cpu_s": cpu_s, "cpu_over_gpu": cpu_s / g, "cpu_cores": cores(),
+            "gpu": {"status": rep.status.value, "iterations": rep.iterations,
+                    "final_relE": rep.residual_history[-1][0] / float(np.linalg.norm(a))},
+            "cpu": {"status": out["status"], "iterations": out["iterations"],
+                    "final_relE": out["residual_history"][-1][0] / out["norm_a"]}}
 
 
 def cores():
@@ -91,23 +122,40 @@ def cores():
 
 
 def run_reference(args):
+    """The reference arm: the CPU port of the reference loop timed on ONE real
+    refinement of the bench workload itself (n = 8192, the same A and Q̂ as the
+    GPU arm) with all host threads.  A refinement takes minutes on the CPU, so
+    the arm times exactly one (steps = 1) whatever --steps asks for; the
+    warm-up is one small refinement (BLAS thread pools, code paths)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     n = args.n
+    from paper_2203_10879_b200 import inputs
+    a, q = workload(n, seed=0)
+    q = q.astype(np.complex128)
     if args.warmup > 0:
-        cpu_oracle_sample(args.warmup, n)
-    vals, out = cpu_oracle_sample(max(args.steps, 1), n)
-    v = float(np.median(vals))
-    sample = ("oracle port (oracle/refine_fp64.py: numpy/OpenBLAS hp, C restatement of trisolve.py lp) "
-              "full refine at n=%d on the config-3 workload family, %d iterations, scaled by (n/%d)^3"
-              % (SAMPLE_N, out["iterations"], SAMPLE_N))
+        aw = inputs.gaussian_real(256, 0)
+        cpu_refine(aw, inputs.cached_qhat("c3_n256_s0", aw).astype(np.complex128), 256)
+    v, out = cpu_refine(a, q, n)
+    hist = out["residual_history"]
+    sample = ("one full refinement of the bench workload (n=%d, the GPU arm's A and Q^) by the CPU port of the "
+              "reference loop: oracle/refine_fp64.py, numpy/OpenBLAS hp and lp products, the BLAS-backed port "
+              "of the reference solver (oracle/trisolve_blas.py); %d iterations, %s; %d BLAS threads, numba "
+              "unused" % (n, out["iterations"], out["status"], blas_threads() or -1, ))
     line = {"metric": METRIC, "value": v, "unit": "s", "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1000.0, "higher_is_better": False,
+            "steps": 1, "warmup": 1 if args.warmup > 0 else 0, "steps_requested": args.steps,
+            "ms_per_step": v * 1000.0, "higher_is_better": False,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "config3: n=%d real Gaussian A, complex64-Schur start, FP32->FP64, "
                                    "stop relE<10u64 or 10 iters" % n, "n": n},
-            "cpu_baseline": {"value": v, "unit": "s", "cores": cores(), "kind": "port", "sample": sample},
+            "result": {"status": out["status"], "iterations": out["iterations"], "skip_fired": out["skip_fired"],
+                       "final_relE": hist[-1][0] / out["norm_a"], "final_ortho": hist[-1][1],
+                       "hp_matmul_count": out["hp_matmul_count"],
+                       "phases_s": {k2: round(x, 3) for k2, x in out["phases"].items()}},
+            "same_config": True,
+            "cpu_baseline": {"value": v, "unit": "s", "cores": cores(), "blas_threads": blas_threads(),
+                             "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -294,10 +342,10 @@ def main():
                 "d2h_bytes_per_step": int(q_out.numel() * 16 + t_out.numel() * 16)},
     }
     if not args.no_cpu_baseline:
-        vals, out = cpu_oracle_sample(2, n)
-        line["cpu_baseline"] = {"value": float(np.median(vals)), "unit": "s", "cores": cores(), "kind": "port",
-                                "sample": "oracle port full refine at n=%d (config-3 workload family, %d "
-                                          "iterations), O(n^3)-scaled to n=%d" % (SAMPLE_N, out["iterations"], n)}
+        v, sample = cpu_composed(n, k_it, rep.skip_fired)
+        line["cpu_baseline"] = {"value": v, "unit": "s", "cores": cores(), "blas_threads": blas_threads(),
+                                "kind": "port", "sample": sample}
+        line["config2"] = config2_head_to_head(cfg, dev)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

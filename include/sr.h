@@ -261,6 +261,33 @@ int sr_oz_decode_gauss(int M, int N, int nmod, int nchunk, const double* table, 
                        long long ld_add, double add_scale, int out_kind, void* out_re, double* out_im,
                        long long ld_out, int hermitian, int diag_col0, void* stream);
 
+
+/* ---- double-double container operations (csrc/dd_ops.cu), bit-identical to
+   the reference's numpy / numba kernels for finite operands.  One real plane
+   (hi, lo) per call; row-major with leading dimensions. */
+
+/* z = x + y (negate_y = 0) or x - y (negate_y = 1) in dd: DDMatrix.__add__ /
+   __sub__ (ddmatrix.py:114-126 -> dd.add / dd.sub, dd.py:96-114). */
+int sr_dd_add(int m, int n, const double* xh, const double* xl, long long ldx, const double* yh,
+              const double* yl, long long ldy, int negate_y, double* zh, double* zl, long long ldz, void* stream);
+
+/* z = s x (s a binary64 scalar): DDMatrix.scale(float) (ddmatrix.py:138-147 -> dd.mul_d, dd.py:127-132). */
+int sr_dd_scale(int m, int n, const double* xh, const double* xl, long long ldx, double s, double* zh,
+                double* zl, long long ldz, void* stream);
+
+/* e = strictly lower part of src, t = the rest (either may be NULL):
+   stril_extract (ddmatrix.py:190-209), pure masking. */
+int sr_stril_split_f64(int m, int n, const double* src, long long lds, double* e, long long lde, double* t,
+                       long long ldt, void* stream);
+
+/* d_out[0..1] = (hi, lo) of the dd Frobenius norm of a complex dd matrix
+   (rl, ih, il may be NULL = zero planes): frobenius_norm (ddmatrix.py:216-251) —
+   dd squares, the reference's fixed pairwise tree over COLUMN-MAJOR order,
+   dd sqrt.  ws: sr_fro_norm_dd_workspace_bytes(rows * cols) bytes. */
+size_t sr_fro_norm_dd_workspace_bytes(long long entries);
+int sr_fro_norm_dd(int rows, int cols, const double* rh, const double* rl, const double* ih, const double* il,
+                   long long ld, double* d_out, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

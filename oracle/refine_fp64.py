@@ -91,8 +91,16 @@ def merged_update(q, w, y, restore_full_sigma=False):
 
 def refine_template_fp64(a, qhat, tol_factor=10.0, max_iters=20, n_min=4,
                          clip_threshold=None, skip_final_ortho=True,
-                         restore_full_sigma=False):
-    """refine.py:357-380 + _run (223-329) in FP64 mode.  Returns a dict."""
+                         restore_full_sigma=False, solver="c"):
+    """refine.py:357-380 + _run (223-329) in FP64 mode.  Returns a dict.
+
+    solver "c": the plain-C restatement of trisolve.py (the parity checker);
+    "blas": oracle/trisolve_blas.py, the same recursion on BLAS / LAPACK
+    kernels (the timed CPU baseline at large n; no clipping)."""
+    if solver not in ("c", "blas"):
+        raise ValueError("solver must be 'c' or 'blas'")
+    if solver == "blas" and clip_threshold is not None:
+        raise ValueError("the BLAS solver port does not clip")
     t0 = time.perf_counter()
     a = np.asarray(a)
     a = a.astype(np.complex128) if np.iscomplexobj(a) else a.astype(np.float64)
@@ -103,8 +111,11 @@ def refine_template_fp64(a, qhat, tol_factor=10.0, max_iters=20, n_min=4,
     if not (np.isfinite(a).all() and np.isfinite(qhat).all()):
         raise ValueError("input matrix has non-finite entries")
     hp = 0
+    phases = dict(entry=0.0, measure=0.0, solve=0.0, update=0.0)
+    tp = time.perf_counter()
     q = newton_schulz_step(qhat)
     hp += 2
+    phases["entry"] += time.perf_counter() - tp
     norm_a = float(np.linalg.norm(a))
     tol = tol_factor * n * U_FP64 * norm_a
     history = []
@@ -116,8 +127,15 @@ def refine_template_fp64(a, qhat, tol_factor=10.0, max_iters=20, n_min=4,
     that = None
     streak = 0
     eye = np.eye(n)
+    real_a = not np.iscomplexobj(a)
     for it in range(1, max_iters + 1):
-        that = (q.conj().T @ a) @ q
+        tp = time.perf_counter()
+        if real_a:  # Q^H A with real A: two real products (the same values up to rounding)
+            qha = (q.real.T @ a) - 1j * (q.imag.T @ a)
+        else:
+            qha = q.conj().T @ a
+        that = qha @ q
+        del qha
         hp += 2
         e = np.tril(that, -1)
         t = np.triu(that)
@@ -125,6 +143,7 @@ def refine_template_fp64(a, qhat, tol_factor=10.0, max_iters=20, n_min=4,
         y = q.conj().T @ q - eye
         hp += 1
         norm_y = float(np.linalg.norm(y))
+        phases["measure"] += time.perf_counter() - tp
         if it == 1:
             history.append((norm_e, norm_y))  # row 0: FP64 entry measurement
         history.append((norm_e, norm_y))
@@ -133,10 +152,15 @@ def refine_template_fp64(a, qhat, tol_factor=10.0, max_iters=20, n_min=4,
             detail = "iteration %d: residuals became non-finite" % it
             break
         converged = norm_e <= tol
+        tp = time.perf_counter()
         try:
-            l, nclip = clib.solve_block(t.astype(np.complex64), e.astype(np.complex64),
-                                        n_min=n_min, clip_threshold=clip_threshold,
-                                        dtype=np.complex64)
+            if solver == "c":
+                l, nclip = clib.solve_block(t.astype(np.complex64), e.astype(np.complex64),
+                                            n_min=n_min, clip_threshold=clip_threshold,
+                                            dtype=np.complex64)
+            else:
+                from . import trisolve_blas
+                l, nclip = trisolve_blas.solve_block(t, e, n_min=n_min, dtype=np.complex64), 0
         except clib.NonFiniteError as exc:
             status, iterations = "NonFinite", it
             detail = "iteration %d: %s" % (it, exc)
@@ -144,11 +168,14 @@ def refine_template_fp64(a, qhat, tol_factor=10.0, max_iters=20, n_min=4,
         clipped_total += nclip
         w = l - l.conj().T
         norm_w = float(np.linalg.norm(w))
+        phases["solve"] += time.perf_counter() - tp
         skip = (converged and skip_final_ortho and norm_y <= 10.0 * n * U_FP64
                 and norm_w <= math.sqrt(U_FP64))
         if not skip:
+            tp = time.perf_counter()
             q = merged_update(q, w, y, restore_full_sigma)
             hp += 1
+            phases["update"] += time.perf_counter() - tp
         if converged:
             status, iterations, skip_fired = "Converged", it, skip
             break
@@ -163,7 +190,7 @@ def refine_template_fp64(a, qhat, tol_factor=10.0, max_iters=20, n_min=4,
     return dict(q=q, t=np.triu(that), ortho_residual=last_y, tri_residual=last_e,
                 iterations=iterations, residual_history=history, hp_matmul_count=hp,
                 clipped_total=clipped_total, status=status, skip_fired=skip_fired,
-                detail=detail, wall_time=time.perf_counter() - t0, norm_a=norm_a)
+                detail=detail, wall_time=time.perf_counter() - t0, norm_a=norm_a, phases=phases)
 
 
 def residuals_fp64(a, q):

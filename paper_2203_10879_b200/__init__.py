@@ -16,7 +16,9 @@ from .refine import (
     VerifyResiduals,
     verify_pair,
 )
-from .trisolve import TriEqProblem, TriEqSolution, solve_block
+from .trisolve import TriEqProblem, TriEqSolution, reset_stats, solve_block, solve_scalar, stats
+from .ddmatrix import DDMatrix, DDScalar, frobenius_norm, precision_convert, stril_extract
+from .orthogonal import merged_update, newton_schulz_step
 from .continuation import refine_continuation
 from .symmetric import order_by_random_line, refine_symmetric
 from .mixed import refine_mixed
@@ -28,5 +30,6 @@ __all__ = [
     "matmul_lp", "reset_counters", "ZPlanar", "U_FP64", "U_HP", "OrthoStrategy", "RefineConfig",
     "RefineReport", "RefineStatus", "SchurPair", "refine_template", "verify_pair", "VerifyResiduals", "TriEqProblem",
     "TriEqSolution", "solve_block", "refine_continuation", "DDPlanar", "refine_symmetric",
-    "order_by_random_line", "refine_mixed",
+    "order_by_random_line", "refine_mixed", "solve_scalar", "stats", "reset_stats", "DDMatrix", "DDScalar",
+    "frobenius_norm", "precision_convert", "stril_extract", "merged_update", "newton_schulz_step",
 ]

@@ -58,6 +58,11 @@ SIGNATURES = {
     "sr_oz_gemm_i8_gauss": (_i, [_i, _i, _i, _i, _p, _p, _i, _ll, _p, _i, _ll, _p, _ll, _i, _i, _p]),
     "sr_oz_decode_gauss": (_i, [_i, _i, _i, _i, _p, _p, _ll, _p, _i, _p, _i, _d, _d, _i, _p, _p, _ll, _d, _i,
                                 _p, _p, _ll, _i, _i, _p]),
+    "sr_dd_add": (_i, [_i, _i, _p, _p, _ll, _p, _p, _ll, _i, _p, _p, _ll, _p]),
+    "sr_dd_scale": (_i, [_i, _i, _p, _p, _ll, _d, _p, _p, _ll, _p]),
+    "sr_stril_split_f64": (_i, [_i, _i, _p, _ll, _p, _ll, _p, _ll, _p]),
+    "sr_fro_norm_dd_workspace_bytes": (_sz, [_ll]),
+    "sr_fro_norm_dd": (_i, [_i, _i, _p, _p, _p, _p, _ll, _p, _p, _sz, _p]),
 }
 
 _lib = None

@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <map>
+#include <mutex>
 #include <tuple>
 #include <vector>
 
@@ -559,8 +560,19 @@ int make_map(CUtensorMap* map, const void* base, int K, int rows, int planes, in
 
 // Unit table of a lower_only product (cached per shape): units (mp, nt) with
 // at least one tile on or below the diagonal, in decode_tile's raster order.
-const int* lower_table(int tiles_mp, int tiles_n, int cm, int group, int* count) {
-  static std::map<std::tuple<int, int, int, int>, std::pair<int*, int>> cache;
+// Per-device launch state (sr_device_slot): the unit-table cache, the pool of
+// zeroed unit counters and the one-time shared-memory attributes.
+struct OzDevState {
+  std::mutex mu;
+  std::map<std::tuple<int, int, int, int>, std::pair<int*, int>> tables;
+  int* counters = nullptr;
+  unsigned launch_seq = 0;
+  bool configured = false;
+};
+OzDevState g_oz_dev[SR_MAX_DEVICES];
+
+const int* lower_table(OzDevState& ds, int tiles_mp, int tiles_n, int cm, int group, int* count) {
+  auto& cache = ds.tables;
   const auto key = std::make_tuple(tiles_mp, tiles_n, cm, group);
   auto it = cache.find(key);
   if (it != cache.end()) {
@@ -596,6 +608,10 @@ int gemm_launch(int M, int N, int K, int nmod, const int* moduli, const void* a,
   if ((a_kpitch | b_kpitch | out_pitch) & 15) return SR_EINVAL;
   if (K > (1 << 16)) return SR_EINVAL;  // 2K terms of |x| <= 2^14: int32 accumulation stays exact
   if (((uintptr_t)a | (uintptr_t)b | (uintptr_t)out) & 15) return SR_EINVAL;
+  int slot = 0;
+  if (sr_device_slot(&slot) != SR_OK) return SR_EINVAL;
+  OzDevState& ds = g_oz_dev[slot];
+  std::lock_guard<std::mutex> lock(ds.mu);
   OzParams p;
   memset(&p, 0, sizeof(p));
   // complex x real: [C_re; C_im] = [A_re; A_im] B^T is one real product with
@@ -658,7 +674,7 @@ int gemm_launch(int M, int N, int K, int nmod, const int* moduli, const void* a,
   if (p.group_m < 1) p.group_m = 1;
   if (lower_only && !getenv("SR_OZ_NO_COMPACT")) {
     const int tiles_mp = (p.tiles_m + cm - 1) / cm;
-    p.table = lower_table(tiles_mp, p.tiles_n, cm, p.group_m, &p.units_per_mod);
+    p.table = lower_table(ds, tiles_mp, p.tiles_n, cm, p.group_m, &p.units_per_mod);
     if (!p.table) return sr_set_cuda_error(cudaErrorMemoryAllocation, "oz_gemm lower-unit table");
   }
   if (grid > tiles) grid = tiles;
@@ -674,21 +690,18 @@ int gemm_launch(int M, int N, int K, int nmod, const int* moduli, const void* a,
   const size_t smem = 1024 + (size_t)SMEM_RING + SMEM_TAIL;
   // one zeroed unit counter per launch (a pool, so launches on different
   // streams never share one)
-  static int* counters = nullptr;
-  static unsigned launch_seq = 0;
   constexpr int NCOUNTERS = 256;
-  if (!counters && cudaMalloc(&counters, NCOUNTERS * 32 * sizeof(int)) != cudaSuccess)
+  if (!ds.counters && cudaMalloc(&ds.counters, NCOUNTERS * 32 * sizeof(int)) != cudaSuccess)
     return sr_set_cuda_error(cudaErrorMemoryAllocation, "oz_gemm unit counters");
-  int* counter = counters + 32 * (launch_seq++ % NCOUNTERS);  // 128-byte apart
+  int* counter = ds.counters + 32 * (ds.launch_seq++ % NCOUNTERS);  // 128-byte apart
   SR_CUDA_CHECK(cudaMemsetAsync(counter, 0, sizeof(int), (cudaStream_t)stream));
-  static bool configured = false;
-  if (!configured) {
+  if (!ds.configured) {
     SR_CUDA_CHECK(cudaFuncSetAttribute(oz_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     SR_CUDA_CHECK(cudaFuncSetAttribute(oz_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     SR_CUDA_CHECK(
         cudaFuncSetAttribute(oz_gemm_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     SR_CUDA_CHECK(cudaFuncSetAttribute(oz_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured = true;
+    ds.configured = true;
   }
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));

@@ -25,6 +25,18 @@ extern "C" unsigned long long sr_kernel_launches(void);
 
 static inline int sr_ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// Library state that belongs to a device (unit-counter pools, cached unit
+// tables, solver streams / graphs, one-time kernel attributes) lives in
+// per-device slots: a process may drive several GPUs (or switch devices)
+// and each device gets its own.  The slot index is the CURRENT device.
+constexpr int SR_MAX_DEVICES = 16;
+static inline int sr_device_slot(int* slot) {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= SR_MAX_DEVICES) return SR_EINVAL;
+  *slot = d;
+  return SR_OK;
+}
+
 struct cf32 {
   float x, y;
 };

@@ -52,6 +52,8 @@
 
 #include <type_traits>
 
+#include <mutex>
+
 #include "sr_common.cuh"
 #include "trisolve_tc.cuh"
 
@@ -836,7 +838,13 @@ int solve(int n, const C* t, const C* e, long long ld, C* l, double clip, unsign
   const size_t need = sr_trisolve_workspace_bytes(n, sizeof(C) == 8 ? 1 : 0);
   const size_t rb = r_bytes(n, ld, sizeof(C));
   if (ws_bytes < need || !ws || 2 * rb + (sizeof(C) == 8 ? far_tc_forms_bytes(n) : 0) > need) return SR_EINVAL;
-  static SolveCtx c;  // one per lp type
+  // one context per (device, lp type); a context serialises its callers
+  static SolveCtx ctxs[SR_MAX_DEVICES];
+  static std::mutex mus[SR_MAX_DEVICES];
+  int slot = 0;
+  if (sr_device_slot(&slot) != SR_OK) return SR_EINVAL;
+  std::lock_guard<std::mutex> lock(mus[slot]);
+  SolveCtx& c = ctxs[slot];
   if (ctx_init<C>(c) != SR_OK) return SR_ECUDA;
   const bool same = c.n == n && c.t == t && c.e == e && c.l == l && c.ld == ld && c.clip == clip &&
                     c.clipped == d_clipped && c.flags == d_flags && c.ws == ws && c.ws_bytes == ws_bytes;

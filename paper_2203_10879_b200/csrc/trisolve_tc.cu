@@ -247,6 +247,7 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
                   const __grid_constant__ FarTcArgs p, float2* __restrict__ Rf) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ float eb_s[4][32];  // 2^(e_b) of the tile's B lines
+  __shared__ int eb_x[4][32];    // e_b itself (the out-of-range path)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   float2* stage_buf = reinterpret_cast<float2*>(smem + TC_STAGES * TC_STAGE);  // COL epilogue staging, 4 x 32 x 33
   uint64_t* bars = (uint64_t*)(smem + TC_STAGES * TC_STAGE + EPI_BYTES);
@@ -384,8 +385,14 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
       // multiply per entry instead of an ldexpf (2^e is exact for line maxima
       // in [2^-127, 2^127), i.e. every complex64 line that is neither
       // subnormal nor within a factor 2 of overflow)
-      eb_s[ew][lane] = ldexpf(1.f, jl < n ? line_exp(max4(p.b_max, (size_t)n, jl)) : 0);
+      const int eb = jl < n ? line_exp(max4(p.b_max, (size_t)n, jl)) : 0;
+      eb_s[ew][lane] = ldexpf(1.f, eb);
+      eb_x[ew][lane] = eb;
       const float fa = ldexpf(1.f, ea);
+      // a line maximum outside [2^-127, 2^126] makes one factor 0 or inf: then
+      // the whole warp scales by the combined 2^(e_a + e_b) instead (one
+      // ldexpf per entry), so inf * 0 never turns a finite entry into NaN
+      const bool wide = __any_sync(0xffffffffu, ea > 126 || ea < -126 || eb > 126 || eb < -126);
       __syncwarp();
       const int tgt = t0 + ew;  // target tile index along the line
       const bool live = tgt < p.h;
@@ -420,7 +427,7 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
           // block, then the block stored row by row (coalesced 256-byte rows)
 #pragma unroll
           for (int c = 0; c < NB; ++c) {
-            const float sc = fa * eb_s[ew][c];
+            const float sc = wide ? ldexpf(1.f, ea + eb_x[ew][c]) : fa * eb_s[ew][c];
             float2& q = buf[lane * 33 + c];
             q = make_float2(q.x - __uint_as_float(v[2 * c]) * sc, q.y - __uint_as_float(v[2 * c + 1]) * sc);
           }
@@ -435,7 +442,7 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
 #pragma unroll
           for (int i = 0; i < NB; ++i) {
             if (R0 + i < n) {
-              const float sc = fa * eb_s[ew][i];
+              const float sc = wide ? ldexpf(1.f, ea + eb_x[ew][i]) : fa * eb_s[ew][i];
               const float2 q = buf[i * 33 + lane];
               Rf[(size_t)(R0 + i) * ld + idx] = make_float2(q.x + __uint_as_float(v[2 * i]) * sc,
                                                             q.y + __uint_as_float(v[2 * i + 1]) * sc);
@@ -526,8 +533,10 @@ int far_tc_prepare(FarTcPlan* plan, int n, const float2* T, long long ld, void* 
   SR_LAUNCH_CHECK();
   tforms_kernel<<<g, 256, 0, st>>>(n, T, ld, plan->tmax_r, plan->tmax_c, plan->tform, plan->ttform, P);
   SR_LAUNCH_CHECK();
-  static bool configured = false;
-  if (!configured) {
+  static bool configured[SR_MAX_DEVICES] = {};  // function attributes are per device
+  int slot = 0;
+  if (sr_device_slot(&slot) != SR_OK) return SR_EINVAL;
+  if (!configured[slot]) {
     SR_CUDA_CHECK(cudaFuncSetAttribute(far_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
     SR_CUDA_CHECK(cudaFuncSetAttribute(far_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
     // the whole 228 KB as shared memory: a far CTA (131 KB) leaves room for a
@@ -536,7 +545,7 @@ int far_tc_prepare(FarTcPlan* plan, int n, const float2* T, long long ld, void* 
                                        cudaSharedmemCarveoutMaxShared));
     SR_CUDA_CHECK(cudaFuncSetAttribute(far_tc_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                        cudaSharedmemCarveoutMaxShared));
-    configured = true;
+    configured[slot] = true;
   }
   return SR_OK;
 }

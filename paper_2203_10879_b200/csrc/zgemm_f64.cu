@@ -223,10 +223,12 @@ int launch(int m, int n, int k, double alpha, double shift, const double* ar, co
            const double* br, const double* bi, long long ldb, double* cr, double* ci, long long ldc,
            cudaStream_t st) {
   auto kern = zgemm_f64_kernel<OPA, BREAL>;
-  static bool configured = false;
-  if (!configured) {
+  static bool configured[SR_MAX_DEVICES] = {};  // function attributes are per device
+  int slot = 0;
+  if (sr_device_slot(&slot) != SR_OK) return SR_EINVAL;
+  if (!configured[slot]) {
     SR_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
-    configured = true;
+    configured[slot] = true;
   }
   dim3 grid(sr_ceil_div(n, BN), sr_ceil_div(m, BM));
   kern<<<grid, NTHREADS, SMEM_BYTES, st>>>(m, n, k, alpha, shift, ar, ai, lda, br, bi, ldb, cr, ci, ldc);

@@ -71,8 +71,11 @@ class DDProducts:
         self.la = ozaki.Encoded(n, n, 2, lp.beta_a, lp.nmod, dev)
         self.lb = ozaki.Encoded(n, n, 3, lp.beta_b, lp.nmod, dev)
         self.lres = ozaki.ResidueBuffer(n, n, lp.nmod, dev)
-        self.eb_a = ozaki.encode(a, n, n, "b", hp)
-        self.a_hi = a.hi
+        # a = None: products without A (the standalone newton_schulz_step /
+        # merged_update of orthogonal.py)
+        self.eb_a = ozaki.encode(a, n, n, "b", hp) if a is not None else None
+        self.w_skew = True  # W exactly skew-Hermitian (W = L - L^H): W^2 / W^3 on the lower tiles
+        self.a_hi = a.hi if a is not None else None
 
     def _hp(self, ea, eb, out, hermitian=False, **kw):
         ozaki.gemm_residues(ea, eb, self.hp, self.res, lower_only=hermitian)
@@ -136,9 +139,9 @@ class DDProducts:
         ozaki.encode(ws.y_lp, n, n, "a", lp, out=self.la)
         self._lp(self.la, self.lb, ws.yw)
         ozaki.encode(ws.w_lp, n, n, "a", lp, out=self.la)
-        self._lp(self.la, self.lb, ws.w2, hermitian=True)      # W skew-Hermitian: W^2 Hermitian
+        self._lp(self.la, self.lb, ws.w2, hermitian=self.w_skew)      # W skew-Hermitian: W^2 Hermitian
         ozaki.encode(ws.w2, n, n, "a", lp, out=self.la)
-        self._lp(self.la, self.lb, ws.w3, hermitian="skew")    # W^3 skew-Hermitian
+        self._lp(self.la, self.lb, ws.w3, hermitian="skew" if self.w_skew else False)  # W^3 skew-Hermitian
         w2y = w2yw = None
         if restore_full_sigma:
             if ws.w2y is None:
@@ -196,7 +199,8 @@ def coerce_dd(x, device):
 def run_dd(a, qhat, cfg, device, symmetric=False):
     """_run in dd mode on DDPlanar inputs (symmetric: the Hermitian variant of
     refine_symmetric — full off-diagonal defect, diagonal-correction solve)."""
-    from .refine import RefineReport, RefineStatus, SchurPair, _phase_permutation, _structural_triangle
+    from .refine import (RefineReport, RefineStatus, SchurPair, _exact_measure, _phase_permutation,
+                         _quarter_phases, _structural_triangle)
     n = a.rows
     ws = _workspace(n, device)
     st = _stream()
@@ -232,8 +236,12 @@ def run_dd(a, qhat, cfg, device, symmetric=False):
     skip_fired = False
     detail = ""
     streak = 0
+    ph = _quarter_phases(ws.q.hi, perm) if perm is not None else None
     for it in range(1, cfg.max_iters + 1):
-        prod.measure()
+        if ph is not None:  # Q a signed permutation: exact data movement (refine._exact_measure)
+            _exact_measure(a, ph, perm, ws.that, ws.y)
+        else:
+            prod.measure()
         that = ws.that
         _lib.call("sr_split_lp_c128", n, that.hi.re_ptr(), that.hi.im_ptr(), that.ld, ws.t_lp.data_ptr(),
                   ws.e_lp.data_ptr(), ws.t_lp.shape[1], ws.ptr(1), ws.red[1].data_ptr(), ws.red[1].numel(), st)
@@ -283,6 +291,10 @@ def run_dd(a, qhat, cfg, device, symmetric=False):
                 and norm_w <= math.sqrt(U_HP))
         if not skip:
             prod.update(cfg.restore_full_sigma)
+            if ph is not None:  # still a signed permutation (W = 0: every correction clipped)?
+                lo_zero = not (bool(ws.q.lo.re.any()) or bool(ws.q.lo.im.any()))
+                perm = _phase_permutation(ws.q.hi) if lo_zero else None
+                ph = _quarter_phases(ws.q.hi, perm)
         if converged:
             status, iterations, skip_fired = RefineStatus.CONVERGED, it, skip
             break

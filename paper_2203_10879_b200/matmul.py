@@ -35,12 +35,58 @@ def ctypes_stream(s):
     return s.cuda_stream
 
 
-def matmul_hp(a, b, trans_a=False, alpha=1.0, diag_shift=0.0, out=None):
+DD_PRODUCT_BETA = 106  # standalone dd products: every entry within 2^0 of its row max keeps 106 bits
+
+
+def _matmul_dd(a, b, trans_a, trans_b):
+    """C = op(A) op(B) in double-double (the reference's matmul_hp on
+    DDMatrix operands, matmul.py:52-81): an Ozaki-II product with dd in and
+    out (csrc/ozaki.cu, SR_MAT_DD); op(B) = B^H materialised on the device
+    first, like the reference (matmul.py:64-65).  Host DDMatrix operands give
+    a host DDMatrix, device DDPlanar ones a DDPlanar."""
+    from . import ozaki
+    from .ddmatrix import as_ddplanar
+    from .matrix import DDPlanar
+    host = not (isinstance(a, DDPlanar) and isinstance(b, DDPlanar))
+    A = as_ddplanar(a)
+    B = as_ddplanar(b, device=A.hi.re_buf.device)
+    if trans_b:
+        dev = B.hi.re_buf.device
+        Bt = DDPlanar.empty(B.cols, B.rows, device=dev)
+        for src, dst, sgn in ((B.hi.re, Bt.hi.re_buf, 1.0), (B.lo.re, Bt.lo.re_buf, 1.0),
+                              (B.hi.im, Bt.hi.im_buf, -1.0), (B.lo.im, Bt.lo.im_buf, -1.0)):
+            dst[:, : B.rows].copy_(src.t() * sgn if sgn < 0 else src.t())
+            dst[:, B.rows:].zero_()
+        B = Bt
+    m, k = (A.cols, A.rows) if trans_a else (A.rows, A.cols)
+    if B.rows != k:
+        raise ValueError("inner dimensions disagree: %d vs %d" % (k, B.rows))
+    n = B.cols
+    pl = ozaki.plan(max(k, 1), DD_PRODUCT_BETA, DD_PRODUCT_BETA)
+    ea = ozaki.encode(A, A.rows, A.cols, "a", pl, conj_t=trans_a)
+    eb = ozaki.encode(B, B.rows, B.cols, "b", pl)
+    res = ozaki.ResidueBuffer(m, n, pl.nmod, A.hi.re_buf.device)
+    out = DDPlanar.empty(m, n, device=A.hi.re_buf.device)
+    ozaki.gemm_residues(ea, eb, pl, res)
+    ozaki.decode(res, ea, eb, pl, out)
+    _counters["hp_calls"] += 1
+    return out.to_ddmatrix() if host else out
+
+
+def matmul_hp(a, b, trans_a=False, alpha=1.0, diag_shift=0.0, out=None, trans_b=False):
     """C = alpha * op(A) B (+ diag_shift * I), FP64 complex planar.
 
     op(A) = A^H when trans_a (the reference materialises conj_t first,
     matmul.py:64; here the kernel reads A transposed from global memory).
-    b may be real (no imaginary plane)."""
+    b may be real (no imaginary plane).  Double-double operands (DDMatrix,
+    DDPlanar, anything with `.cells()`): the reference's dd product
+    op(A) op(B) with trans_a / trans_b (matmul.py:52-81), see _matmul_dd."""
+    if not isinstance(a, ZPlanar) and hasattr(a, "cells") or not isinstance(b, ZPlanar) and hasattr(b, "cells"):
+        if alpha != 1.0 or diag_shift != 0.0 or out is not None:
+            raise ValueError("dd products take no alpha / diag_shift / out")
+        return _matmul_dd(a, b, trans_a, trans_b)
+    if trans_b:
+        raise NotImplementedError("trans_b is the dd-operand form")
     if a.is_real:
         raise ValueError("matmul_hp: A must be complex (a real A^H A is not on the path)")
     m = a.cols if trans_a else a.rows

@@ -144,6 +144,9 @@ class DDPlanar:
         a 4-plane (re_hi, re_lo, im_hi, im_lo) tuple (DDMatrix.cells order)."""
         if isinstance(x, DDPlanar):
             return x
+        if hasattr(x, "cells") and not isinstance(x, ZPlanar):
+            # the reference's DDMatrix (or ours): column-major cells, copied as row-major planes
+            x = tuple(x.cells())
         if isinstance(x, (tuple, list)) and len(x) == 4:
             rh, rl, ih, il = (np.ascontiguousarray(c, dtype=np.float64) for c in x)
             return cls(ZPlanar.from_any(rh + 1j * ih, device=device, force_complex=True),

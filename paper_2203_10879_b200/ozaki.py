@@ -43,7 +43,7 @@ MAXCHUNK = 6
 HP_BETA = 58     # FP64-mode hp operands: every entry within 2^-5 of its row max is exact (17 moduli at K=8192)
 LP_BETA = 24     # FP64-mode lp (complex64) operands: the row maximum's full significand (8 moduli at K=8192)
 HP_BETA_Q = 58   # Gaussian FP64 mode: Q's own encoding (B role of Q, A role of Q^H; tools/beta_probe.py)
-DD_BETA = 102    # dd-mode hp operands (double-double; the stop rule is 10 n 2^-106 ||A||)
+DD_BETA = 106    # dd-mode hp operands (double-double; 102 left ||Q^H Q - I|| ~14x above the reference dd GEMM's at n=1024)
 DD_LP_BETA = 55  # dd-mode lp (binary64) operands
 
 

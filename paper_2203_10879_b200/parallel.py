@@ -16,11 +16,25 @@ import torch.distributed as dist
 
 def column_ranges(n, world, align=128):
     """[(j0, j1)] per rank: contiguous column blocks, widths multiples of
-    `align` (the Ozaki GEMM's tile) except possibly the last one."""
+    `align` (the Ozaki GEMM's tile) except possibly the last one.  Every rank
+    gets at least one column: when world * align would leave ranks empty
+    (n = 512 on 8 ranks at align 128) the alignment is halved until none is
+    (an empty rank would encode nothing while the others wait in a
+    collective)."""
     if world <= 1:
         return [(0, n)]
-    per = -(-n // world)
-    per = -(-per // align) * align
+    if n < world:
+        raise ValueError("cannot shard %d columns over %d ranks" % (n, world))
+    while True:
+        per = -(-n // world)
+        per = -(-per // align) * align
+        if (world - 1) * per < n:
+            break
+        if align == 1:  # balanced widths n // world (+1 for the first n % world ranks)
+            base, extra = divmod(n, world)
+            bounds = [r * base + min(r, extra) for r in range(world + 1)]
+            return [(bounds[r], bounds[r + 1]) for r in range(world)]
+        align //= 2
     out = []
     for r in range(world):
         j0 = min(n, r * per)

@@ -118,6 +118,9 @@ class OzakiProducts:
         # first measurement so an asynchronous upload of A overlaps the entry step
         self.a = a
         self.eb_a = None
+        # W exactly skew-Hermitian (W = L - L^H, sr_skew_c64): W^2 / W^3 on the
+        # lower tiles; False (orthogonal.merged_update of a general W): full products
+        self.w_skew = True
 
     def _hp(self, ea, eb, out, hermitian=False, pl=None, **kw):
         pl = pl or self.hp
@@ -203,7 +206,7 @@ class OzakiProducts:
             else:
                 ozaki.encode(ws.w_lp, n, n, "b", p_w2, out=self.lb)       # W, B role
                 ozaki.encode(ws.w_lp, n, n, "a", p_w2, out=self.la)
-                self._lp_with(p_w2, self.la, self.lb, ws.w2, hermitian=True)  # W^2 (W skew-Hermitian)
+                self._lp_with(p_w2, self.la, self.lb, ws.w2, hermitian=self.w_skew)  # W^2 (W skew-Hermitian)
             _lib.call("sr_fused_lp_operand_c64", n, ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld, ws.w_lp.data_ptr(),
                       ws.w2.data_ptr(), ws.w_lp.shape[1], ws.y_lp.data_ptr(), _stream())
             if p_xw is not p_w2:
@@ -217,10 +220,10 @@ class OzakiProducts:
         else:
             ozaki.encode(ws.w_lp, n, n, "b", lp, out=self.lb)            # W, B role (all lp products)
             ozaki.encode(ws.w_lp, n, n, "a", lp, out=self.la)
-            self._lp(self.la, self.lb, ws.w2, hermitian=True)            # W^2 (W skew-Hermitian)
+            self._lp(self.la, self.lb, ws.w2, hermitian=self.w_skew)     # W^2 (W skew-Hermitian)
             _downcast_y(ws)
             ozaki.encode(ws.w2, n, n, "a", lp, out=self.la)
-            self._lp(self.la, self.lb, ws.w3, hermitian="skew")          # W^3
+            self._lp(self.la, self.lb, ws.w3, hermitian="skew" if self.w_skew else False)  # W^3
             ozaki.encode(ws.y_lp, n, n, "a", lp, out=self.la)
             self._lp(self.la, self.lb, ws.yw)                            # Y W
             ozaki.encode(ws.y_lp, n, n, "b", lp, out=self.lb)

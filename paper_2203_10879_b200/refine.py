@@ -283,6 +283,8 @@ class _AsyncUpload:
         self.host = x  # pinned source stays alive until the copy has run
 
     def check(self):
+        # fin is computed on the upload stream: order the read after it
+        torch.cuda.current_stream(self.fin.device).wait_event(self.ready)
         if not bool(self.fin):
             raise ValueError("input matrix has non-finite entries")
 
@@ -338,6 +340,42 @@ def _structural_triangle(a, q, perm, symmetric=False):
     if symmetric:  # the real diagonal only (refine.py:214-219)
         t = torch.diag(torch.diagonal(t).real).to(t.dtype)
     return t
+
+
+def _quarter_phases(q, perm):
+    """The phases of a phase-permutation Q when all are +-1 or +-i (then every
+    product with Q or Q^H is exact data movement), else None."""
+    if perm is None:
+        return None
+    cols = torch.arange(q.cols, device=perm.device)
+    re = q.re[perm, cols]
+    im = q.im[perm, cols] if q.im is not None else torch.zeros_like(re)
+    ok = (((re.abs() == 1) & (im == 0)) | ((re == 0) & (im.abs() == 1))).all()
+    return torch.complex(re, im) if bool(ok) else None
+
+
+def _permuted_similarity(ph, perm, re, im):
+    """conj(ph_i) X[perm_i, perm_j] ph_j for one planar FP64 pair (exact for
+    quarter phases: sign flips and re/im swaps)."""
+    x = torch.complex(re[perm][:, perm], im[perm][:, perm] if im is not None else torch.zeros_like(re))
+    return ph.conj()[:, None] * x * ph[None, :]
+
+
+def _exact_measure(a, ph, perm, that, y):
+    """T^ = Q^H A Q and Y = Q^H Q - I = 0 for Q = P diag(ph), ph in {+-1, +-i}
+    (refine.py:259,265): the reference's dd GEMMs are exact on such a Q, and
+    so is this — whereas an Ozaki product would resolve A's entries only to
+    2^-beta of their column maximum (the 1e-200 separations of
+    test_refine.py:266-287).  a / that / y: ZPlanar, or DDPlanar (both pairs)."""
+    pairs = ((a.hi, that.hi, y.hi), (a.lo, that.lo, y.lo)) if hasattr(a, "hi") else ((a, that, y),)
+    n = that.cols
+    for src, dst, yy in pairs:
+        t = _permuted_similarity(ph, perm, src.re, src.im)
+        dst.re_buf[:, :n].copy_(t.real)
+        dst.im_buf[:, :n].copy_(t.imag)
+        yy.re_buf.zero_()
+        yy.im_buf.zero_()
+    _counters["hp_calls"] += 3  # the reference's three logical products (refine.py:259,265)
 
 
 class _HostResult:
@@ -448,11 +486,15 @@ def _run_fp64(a, qhat, cfg, ws, symmetric=False, host=None, a_upload=None):
     streak = 0
     tol = None
     q_version = 0
+    ph = _quarter_phases(ws.q, perm)
     for it in range(1, cfg.max_iters + 1):
         if host is not None:  # this Q is the result if the loop stops without another update
             host.copy_q(ws.q, q_version)
         # T^ = (Q^H A) Q; split + lp downcast + ||E||; Y = Q^H Q - I; ||Y||
-        prod.measure(a)
+        if ph is not None:  # Q a signed permutation: exact data movement (_exact_measure)
+            _exact_measure(a, ph, perm, ws.that, ws.y)
+        else:
+            prod.measure(a)
         _mark("measure")
         _lib.call("sr_split_lp_c64", n, ws.that.re_ptr(), ws.that.im_ptr(), ws.that.ld, ws.t_lp.data_ptr(),
                   ws.e_lp.data_ptr(), ws.t_lp.shape[1], ws.ptr(1), ws.red[1].data_ptr(), ws.red[1].numel(), st)
@@ -517,6 +559,9 @@ def _run_fp64(a, qhat, cfg, ws, symmetric=False, host=None, a_upload=None):
                         sigma_bound=products.sigma_prime_bound(norm_y, norm_w, cfg.restore_full_sigma),
                         norm_y=norm_y, norm_w=norm_w)
             q_version += 1
+            if ph is not None:  # still a signed permutation (W = 0: every correction clipped)?
+                perm = _phase_permutation(ws.q)
+                ph = _quarter_phases(ws.q, perm)
             _mark("update")
         if converged:
             status, iterations, skip_fired = RefineStatus.CONVERGED, it, skip
@@ -579,6 +624,8 @@ def refine_template(a, qhat, cfg=None, device=None, out=None):
     device = torch.device("cuda") if device is None else torch.device(device)
     t0 = time.perf_counter()
     if cfg.precision == "dd":
+        if out is not None:
+            raise ValueError("out=(q_host, t_host) is the FP64-mode host delivery; dd mode returns DDPlanar results")
         from . import dd_refine
         a = dd_refine.coerce_dd(a, device)
         qhat = dd_refine.coerce_dd(qhat, device)
@@ -589,6 +636,8 @@ def refine_template(a, qhat, cfg=None, device=None, out=None):
         report.wall_time = time.perf_counter() - t0
         return pair, report
     ws = None
+    # double-double operands in FP64 mode: their binary64 rounding (the hi cells)
+    a, qhat = (x.to_lp() if hasattr(x, "to_lp") else x for x in (a, qhat))
     if _is_host_matrix(qhat) and _is_host_matrix(a):
         # end to end from host memory: every device buffer comes from the workspace
         qh, ah = _host_tensor(qhat), _host_tensor(a)

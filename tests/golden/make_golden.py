@@ -190,6 +190,105 @@ def gen_configs(ref):
                   indent=1)
 
 
+def _digest(x):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest()[:16]
+
+
+def _ref_case(tag, a, q, cfg, how, verify=False):
+    from ddschur.refine import refine_template, verify_pair
+    t0 = time.time()
+    try:
+        pair, rep = refine_template(a, q, cfg)
+        res = dict(iterations=rep.iterations, status=rep.status.value,
+                   residual_history=[list(map(float, r)) for r in rep.residual_history],
+                   hp_matmul_count=rep.hp_matmul_count, skip_fired=bool(rep.skip_fired),
+                   detail=rep.detail)
+        if verify and rep.status.value == "Converged":
+            res["verify"] = list(map(float, verify_pair(a, pair)))
+    except Exception as exc:  # SeparationError etc. are results too
+        res = dict(exception=type(exc).__name__, message=str(exc))
+    res.update(tag=tag, n=int(a.shape[0]), how=how, seconds=time.time() - t0,
+               norm_a=float(np.linalg.norm(a)), qhat_sha256_16=_digest(q))
+    print(tag, res.get("status"), res.get("iterations"), "%.1fs" % res["seconds"], flush=True)
+    return res
+
+
+def gen_configs_full(ref):
+    """BASELINE config 4 at its stated size n = 1024, in the reference's
+    native dd mode (default tol_factor = 10, max_iters = 10): the literal
+    matrix (the reference ends NonFinite) and the documented
+    well-conditioned variant (strict part / sqrt(n)).  Q̂ = complex128 Schur
+    vectors (zgees) — too large to commit (16 MiB), so the fixture records
+    its digest and the tests rebuild it with the same LAPACK call."""
+    from ddschur.refine import RefineConfig
+    from paper_2203_10879_b200 import inputs
+    cases = []
+    for scale, tag in ((1.0, "config4_n1024"), (None, "config4wc_n1024")):
+        n = 1024
+        s = 1.0 / np.sqrt(n) if scale is None else scale
+        a = inputs.config4_matrix(n, 0, strict_scale=s)
+        q = inputs.schur_vectors(a, np.complex128)
+        cases.append(_ref_case(tag, a, q, RefineConfig(max_iters=10), "dd mode, default tol_factor=10, "
+                               "max_iters=10", verify=True))
+    with open(os.path.join(HERE, "configs_full_ref.json"), "w") as f:
+        json.dump(dict(source="ddschur.refine.refine_template (unmodified reference, dd mode) on BASELINE "
+                              "config 4 at n=1024", cases=cases), f, indent=1)
+
+
+def gen_config2(ref):
+    """BASELINE config 2 (n = 2048 complex Gaussian, complex64-Schur start)
+    through the unmodified reference (option 1: dd hp, binary64 lp) with the
+    FP64 stop rule re-expressed as tol_factor = 10 * 2^53 / n, max_iters = 10.
+    About 30 min on 8 cores; the result is the reference's own iteration
+    count and status at the config's stated size."""
+    from ddschur.refine import RefineConfig
+    from paper_2203_10879_b200 import inputs
+    a, q = inputs.config_inputs(2, 2048)
+    n = 2048
+    case = _ref_case("config2_n2048", a, q, RefineConfig(tol_factor=10 * 2.0 ** 53 / n, max_iters=10),
+                     "option1: reference dd, tol_factor=10*2^53/n, max_iters=10")
+    with open(os.path.join(HERE, "config2_ref.json"), "w") as f:
+        json.dump(dict(source="ddschur.refine.refine_template (unmodified reference) on BASELINE config 2",
+                       cases=[case]), f, indent=1)
+
+
+def gen_ddops(ref):
+    """DDMatrix arithmetic and the matrix-core helpers on seeded normalised
+    dd inputs: a + b, a - b, a.scale(s), frobenius_norm(a) (hi, lo) and
+    stril_extract(a) (ddmatrix.py:114-147, 190-251) — the pins of the
+    bit-identical GPU versions (csrc/dd_ops.cu)."""
+    from ddschur.ddmatrix import DDMatrix, frobenius_norm, stril_extract
+    out = {}
+    cases = []
+    for k, (m, n) in enumerate(((5, 5), (37, 29), (64, 64), (61, 47))):
+        rng = np.random.Generator(np.random.Philox(4000 + k))
+
+        def dd():
+            cells = []
+            for _ in range(2):
+                hi = rng.standard_normal((m, n)) * np.exp2(rng.integers(-30, 30, (m, n)))
+                lo = hi * rng.standard_normal((m, n)) * 2.0 ** -60
+                s_ = hi + lo
+                cells += [s_, lo - (s_ - hi)]
+            return DDMatrix(cells[0], cells[1], cells[2], cells[3])
+        a, b = dd(), dd()
+        s = float(rng.standard_normal() * 3.7)
+        res = {"a": a, "b": b, "add": a + b, "sub": a - b, "scale": a.scale(s)}
+        if m == n:
+            e, t = stril_extract(a)
+            res["stril_e"], res["stril_t"] = e, t
+        for name, mat in res.items():
+            for cell, arr in zip(("rh", "rl", "ih", "il"), mat.cells()):
+                out["%s%s_%d" % (name, cell, k)] = np.ascontiguousarray(arr)
+        nrm = frobenius_norm(a)
+        cases.append(dict(k=k, m=m, n=n, s=s, norm_hi=float(nrm.hi), norm_lo=float(nrm.lo)))
+    np.savez_compressed(os.path.join(HERE, "ddops_ref.npz"), **out)
+    with open(os.path.join(HERE, "ddops_ref.json"), "w") as f:
+        json.dump(dict(source="ddschur.ddmatrix DDMatrix +, -, scale, frobenius_norm, stril_extract", cases=cases),
+                  f, indent=1)
+
+
 def gen_symmetric(ref):
     """refine_symmetric (refine.py:409-438) in the reference's dd mode on
     seeded Hermitian matrices A = (X + X^H) / 2 (Philox), default config:

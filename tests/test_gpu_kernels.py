@@ -63,15 +63,17 @@ def test_trisolve_matches_reference_golden(golden):
         k = c["k"]
         t, e, l_ref = arr["t_%d" % k], arr["e_%d" % k], arr["l_%d" % k]
         sol = solve_block(TriEqProblem(t=t, e=e, clip_threshold=c["clip"]), lp_dtype=torch.complex128)
-        l = sol.l.cpu().numpy()
+        l = sol.l  # numpy in, numpy out (like the reference)
         assert sol.clipped_count == c["clipped"], c
         err = np.abs(l - l_ref).max() / max(np.abs(l_ref).max(), 1e-300)
         assert err <= 1e-12, (c, err)
         if c["clip"] is None:
-            sol = solve_block(TriEqProblem(t=t, e=e))
-            l = sol.l.cpu().numpy()
+            sol = solve_block(TriEqProblem(t=t, e=e), lp_dtype=torch.complex64)
+            l = sol.l
             err = np.linalg.norm(l - l_ref) / max(np.linalg.norm(l_ref), 1e-300)
             assert err <= 2e-5, (c, err)
+            # the default follows the operands (complex128, the reference's binary64 lp)
+            assert solve_block(TriEqProblem(t=t, e=e)).l.dtype == np.complex128
 
 
 @pytest.mark.parametrize("n", [33, 100, 257, 700, 1157])
@@ -82,8 +84,8 @@ def test_trisolve_c64_matches_oracle(n):
     e = np.tril(rnd(rng, n, n), -1) * 1e-3
     l_or, _ = clib.solve_block(t, e, dtype=np.complex64)
     l_ref, _ = clib.solve_block(t, e, dtype=np.complex128)
-    sol = solve_block(TriEqProblem(t=t, e=e))
-    l = sol.l.cpu().numpy()
+    sol = solve_block(TriEqProblem(t=t, e=e), lp_dtype=torch.complex64)
+    l = sol.l
     err = np.linalg.norm(l - l_ref) / np.linalg.norm(l_ref)
     err_or = np.linalg.norm(l_or - l_ref) / np.linalg.norm(l_ref)
     assert err <= max(10 * err_or, 1e-5), (err, err_or)
@@ -103,7 +105,7 @@ def test_trisolve_c128_far_batches_match_oracle(n):
     e = np.tril(rnd(rng, n, n), -1) * 1e-3
     l_or, _ = clib.solve_block(t, e, dtype=np.complex128)
     sol = solve_block(TriEqProblem(t=t, e=e), lp_dtype=torch.complex128)
-    l = sol.l.cpu().numpy()
+    l = sol.l
     err = np.linalg.norm(l - l_or) / np.linalg.norm(l_or)
     assert err <= 1e-11, err
     # clipping: plant a few large right-hand sides so their entries exceed the threshold
@@ -115,7 +117,7 @@ def test_trisolve_c128_far_batches_match_oracle(n):
     l_or2, clipped_or = clib.solve_block(t, e2, clip_threshold=thr, dtype=np.complex128)
     sol2 = solve_block(TriEqProblem(t=t, e=e2, clip_threshold=thr), lp_dtype=torch.complex128)
     assert sol2.clipped_count == clipped_or and clipped_or >= 1
-    l2 = sol2.l.cpu().numpy()
+    l2 = sol2.l
     assert np.linalg.norm(l2 - l_or2) <= 1e-11 * np.linalg.norm(l_or2)
 
 
@@ -130,7 +132,7 @@ def test_trisolve_errors():
     # known answer (test_trisolve.py:112-118)
     t = np.array([[0.0, 0.0], [0.0, 1.0]], dtype=complex)
     e = np.array([[0.0, 0.0], [0.5, 0.0]], dtype=complex)
-    l = solve_block(TriEqProblem(t=t, e=e), lp_dtype=torch.complex128).l.cpu().numpy()
+    l = solve_block(TriEqProblem(t=t, e=e), lp_dtype=torch.complex128).l
     assert l[1, 0] == -0.5 and l[0, 1] == 0
 
 

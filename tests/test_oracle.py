@@ -136,3 +136,44 @@ def test_fp64_oracle_config1_matches_reference_iterations(golden):
     assert ortho <= 40 * np.sqrt(256) * u
     # entry residual (row 1) agrees with the reference's dd measurement
     assert np.isclose(out["residual_history"][1][0], ref["residual_history"][1][0], rtol=1e-6)
+
+
+@pytest.mark.parametrize("n,dtype", [(150, np.complex128), (300, np.complex64), (333, np.complex128)])
+def test_blas_solver_port_matches_c_restatement(n, dtype):
+    """oracle/trisolve_blas.py (the timed CPU baseline's solver: the same
+    recursive halving on BLAS / LAPACK ?trsyl kernels) against the C
+    restatement of trisolve.py: the same L up to rounding, and both satisfy
+    the equation to working precision."""
+    from oracle import trisolve_blas
+    rng = np.random.Generator(np.random.Philox(77 + n))
+    t = np.triu(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    t[np.diag_indices(n)] = np.arange(n) * (1.0 + 0.5j) + rng.uniform(0.0, 0.5, n)
+    e = 1e-3 * np.tril(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)), -1)
+    t, e = t.astype(dtype), e.astype(dtype)
+    l_c, _ = clib.solve_block(t, e, dtype=dtype)
+    l_b = trisolve_blas.solve_block(t, e, dtype=dtype)
+    u = np.finfo(np.float32 if dtype == np.complex64 else np.float64).eps
+    assert np.linalg.norm(l_b - l_c) <= 100 * u * np.sqrt(n) * np.linalg.norm(l_c)
+    tt = t.astype(np.complex128)
+    for l in (l_b, l_c):
+        r = np.tril(tt @ l - l @ tt, -1) + e
+        assert np.linalg.norm(r) <= 100 * u * np.sqrt(n) * np.linalg.norm(e)
+    with pytest.raises(clib.SeparationError):
+        t2 = t.copy()
+        t2[5, 5] = t2[7, 7]
+        trisolve_blas.solve_block(t2, e, dtype=dtype)
+
+
+def test_fp64_oracle_blas_solver_same_history():
+    """refine_template_fp64(solver="blas") — the bench's CPU arm — follows the
+    C-solver restatement's history (iterations equal, residuals to 1e-3)."""
+    from paper_2203_10879_b200 import inputs
+    n = 200
+    a = inputs.gaussian_complex(n, 21)
+    q = inputs.schur_vectors(a).astype(np.complex128)
+    r_c = refine_template_fp64(a, q, tol_factor=10.0 / n, max_iters=10)
+    r_b = refine_template_fp64(a, q, tol_factor=10.0 / n, max_iters=10, solver="blas")
+    assert r_c["status"] == r_b["status"] == "Converged"
+    assert r_c["iterations"] == r_b["iterations"]
+    for (e1, y1), (e2, y2) in zip(r_c["residual_history"][:-1], r_b["residual_history"][:-1]):
+        assert abs(e1 - e2) <= 1e-3 * e1 and abs(y1 - y2) <= 1e-3 * y1 + 1e-15

@@ -114,6 +114,96 @@ def config2_head_to_head(cfg, dev):
                     "final_relE": out["residual_history"][-1][0] / out["norm_a"]}}
 
 
+DD_N = 1024
+FP64_PEAK_TFLOPS = 37.0  # DMMA / DFMA microbenchmark on this pool's B200 (tools/ubench_fp64.cu)
+
+
+def dd_mode_line(dev, with_cpu=True):
+    """dd mode (the reference's own precision pair) on BASELINE config 4's
+    well-conditioned variant (n = 1024; the literal matrix diverges in the
+    reference): GPU time-to-refine, and the two dd GEMM
+    implementations at n = 1024 side by side — Ozaki-II on the int8 tensor
+    cores (what dd mode runs) and the FMA-EFT dd GEMM on the FP64 pipe —
+    with the dd-flop roofline of each (8 n^3 dd-flops per complex product;
+    FMA-EFT: 48 FP64 instructions per complex dd MAC against the FP64 pipe's
+    18.5 G instructions/ms, i.e. 3.1 dd-TFLOP/s).  cpu: the bit-exact C
+    restatement of the reference dd GEMM (oracle/ddgemm_oracle.c, OpenMP,
+    all host threads) on one n = 512 product."""
+    import torch
+
+    from paper_2203_10879_b200 import RefineConfig, inputs, ozaki, refine_template
+    from paper_2203_10879_b200.matmul import matmul_dd_fma
+    from paper_2203_10879_b200.matrix import DDPlanar
+    n = DD_N
+    a = inputs.config4_matrix(n, 0, strict_scale=1.0 / np.sqrt(n))
+    q = inputs.cached_qhat("c4wc_n%d_s0" % n, a, dtype=np.complex128).astype(np.complex128)
+    A, Q = DDPlanar.from_any(a, device=dev), DDPlanar.from_any(q, device=dev)
+    cfg = RefineConfig(precision="dd", max_iters=10)
+    ts = []
+    for i in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pair, rep = refine_template(A, Q, cfg, device=dev)
+        torch.cuda.synchronize()
+        if i:
+            ts.append(time.perf_counter() - t0)
+
+    def timed(fn, reps=5):
+        fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        out = []
+        for _ in range(reps):
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            out.append(e0.elapsed_time(e1))
+        return float(np.median(out))
+    pl = ozaki.plan(n, ozaki.DD_BETA, ozaki.DD_BETA)
+    ea, eb = ozaki.Encoded(n, n, 2, pl.beta_a, pl.nmod, dev), ozaki.Encoded(n, n, 3, pl.beta_b, pl.nmod, dev)
+    res = ozaki.ResidueBuffer(n, n, pl.nmod, dev)
+    C = DDPlanar.empty(n, n, device=dev)
+
+    def ozaki_product():
+        ozaki.encode(Q, n, n, "a", pl, out=ea)
+        ozaki.encode(A, n, n, "b", pl, out=eb)
+        ozaki.gemm_residues(ea, eb, pl, res)
+        ozaki.decode(res, ea, eb, pl, C)
+    oz_ms = timed(ozaki_product)
+    fma_ms = timed(lambda: matmul_dd_fma(Q, A, out=C))
+    ddflops = 8.0 * n ** 3
+    fma_peak = FP64_PEAK_TFLOPS / 2 * 1e12 / 48 * 8 / 1e12  # dd-TFLOP/s at 48 instructions per complex MAC
+    out = {"workload": "config4 well-conditioned variant (strict part / sqrt(n)), n=%d, FP64->dd, zgees start, "
+                       "default stop 10 n 2^-106 ||A||_F, max_iters 10" % n,
+           "gpu_refine_s": float(np.median(ts)), "status": rep.status.value, "iterations": rep.iterations,
+           "final_tri_rel": rep.residual_history[-1][0] / float(np.linalg.norm(a)),
+           "final_ortho": rep.residual_history[-1][1], "hp_matmul_count": rep.hp_matmul_count,
+           "dd_gemm_n%d" % n: {
+               "ozaki_ms": oz_ms, "ozaki_dd_tflops": ddflops / oz_ms / 1e9, "ozaki_moduli": pl.nmod,
+               "fma_eft_ms": fma_ms, "fma_eft_dd_tflops": ddflops / fma_ms / 1e9,
+               "fma_eft_roofline": {"bound": "fp64", "peak_dd_tflops": fma_peak,
+                                    "frac": ddflops / fma_ms / 1e9 / fma_peak,
+                                    "peak_source": "37 TF/s FP64 (tools/ubench_fp64.cu) / 2 per FMA / 48 "
+                                                   "instructions per complex dd MAC x 8 dd-flops"},
+               "chosen": "ozaki" if oz_ms < fma_ms else "fma_eft"},
+           "reference_refine_s_build_container": 152.7,
+           "reference_note": "the unmodified reference on this workload (tests/golden/configs_full_ref.json, 8 "
+                             "cores of the build container; the Python reference cannot run on the GPU box)"}
+    if with_cpu:
+        from oracle import clib
+        rng = np.random.default_rng(0)
+        m = 512
+        cells = lambda: tuple(rng.standard_normal((m, m)) for _ in range(4))  # noqa: E731
+        x, y = cells(), cells()
+        t0 = time.perf_counter()
+        clib.gemm_dd(x, y)
+        cpu = time.perf_counter() - t0
+        out["cpu_ref_dd_gemm_n512_s"] = cpu
+        out["cpu_ref_dd_gemm_note"] = ("bit-exact C restatement of the reference gemm_hp (Dekker EFTs, panel 32), "
+                                       "%d host threads, one n=512 complex dd product" % cores())
+    return out
+
+
 def cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -346,6 +436,7 @@ def main():
         line["cpu_baseline"] = {"value": v, "unit": "s", "cores": cores(), "blas_threads": blas_threads(),
                                 "kind": "port", "sample": sample}
         line["config2"] = config2_head_to_head(cfg, dev)
+    line["dd_mode"] = dd_mode_line(dev, with_cpu=not args.no_cpu_baseline)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

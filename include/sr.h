@@ -288,6 +288,15 @@ size_t sr_fro_norm_dd_workspace_bytes(long long entries);
 int sr_fro_norm_dd(int rows, int cols, const double* rh, const double* rl, const double* ih, const double* il,
                    long long ld, double* d_out, void* ws, size_t ws_bytes, void* stream);
 
+/* C = op(A) B in double-double with FMA error-free transformations on the
+   FP64 pipe (csrc/ddgemm_fma.cu): the measured alternative to the Ozaki-II
+   dd products for gemm_hp (_numba_kernels.py:18-46, dd.py:53-180); planar
+   row-major dd planes, op_a = SR_OP_N or SR_OP_C. */
+int sr_zgemm_dd_fma(int op_a, int m, int n, int k, const double* a_rh, const double* a_rl, const double* a_ih,
+                    const double* a_il, long long lda, const double* b_rh, const double* b_rl, const double* b_ih,
+                    const double* b_il, long long ldb, double* c_rh, double* c_rl, double* c_ih, double* c_il,
+                    long long ldc, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

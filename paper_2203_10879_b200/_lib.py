@@ -63,6 +63,7 @@ SIGNATURES = {
     "sr_stril_split_f64": (_i, [_i, _i, _p, _ll, _p, _ll, _p, _ll, _p]),
     "sr_fro_norm_dd_workspace_bytes": (_sz, [_ll]),
     "sr_fro_norm_dd": (_i, [_i, _i, _p, _p, _p, _p, _ll, _p, _p, _sz, _p]),
+    "sr_zgemm_dd_fma": (_i, [_i, _i, _i, _i, _p, _p, _p, _p, _ll, _p, _p, _p, _p, _ll, _p, _p, _p, _p, _ll, _p]),
 }
 
 _lib = None

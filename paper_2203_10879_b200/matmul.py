@@ -73,6 +73,25 @@ def _matmul_dd(a, b, trans_a, trans_b):
     return out.to_ddmatrix() if host else out
 
 
+def matmul_dd_fma(a, b, trans_a=False, out=None):
+    """C = op(A) B in double-double on the FP64 pipe with FMA error-free
+    transformations (csrc/ddgemm_fma.cu): the measured comparison point for
+    the dd products (north_star item 2) — dd mode runs the
+    Ozaki-II products, which measure faster.  a, b: DDPlanar."""
+    from .matrix import DDPlanar
+    m, k = (a.cols, a.rows) if trans_a else (a.rows, a.cols)
+    if b.rows != k:
+        raise ValueError("inner dimensions disagree: %d vs %d" % (k, b.rows))
+    n = b.cols
+    if out is None:
+        out = DDPlanar.empty(m, n, device=a.hi.re_buf.device)
+    _lib.call("sr_zgemm_dd_fma", _lib.SR_OP_C if trans_a else _lib.SR_OP_N, m, n, k, a.hi.re_ptr(), a.lo.re_ptr(),
+              a.hi.im_ptr(), a.lo.im_ptr(), a.ld, b.hi.re_ptr(), b.lo.re_ptr(), b.hi.im_ptr(), b.lo.im_ptr(), b.ld,
+              out.hi.re_ptr(), out.lo.re_ptr(), out.hi.im_ptr(), out.lo.im_ptr(), out.ld, _stream())
+    _counters["hp_calls"] += 1
+    return out
+
+
 def matmul_hp(a, b, trans_a=False, alpha=1.0, diag_shift=0.0, out=None, trans_b=False):
     """C = alpha * op(A) B (+ diag_shift * I), FP64 complex planar.
 

@@ -887,9 +887,11 @@ int decode_launch(int M, int N, int nmod, int nchunk, const double* table, const
   int rc;
   if (gauss) {
     const int8_t* r8 = (const int8_t*)res;
-    rc = nchunk <= 2   ? dispatch_gauss<2>(out_kind, add_kind, grid, st, p, r8, exps_a, exps_b, add, out)
-         : nchunk <= 4 ? dispatch_gauss<4>(out_kind, add_kind, grid, st, p, r8, exps_a, exps_b, add, out)
-                       : dispatch_gauss<6>(out_kind, add_kind, grid, st, p, r8, exps_a, exps_b, add, out);
+    // nchunk: the top CRT chunks the output's precision needs (OzPlan.decode_chunks)
+    rc = nchunk <= 2    ? dispatch_gauss<2>(out_kind, add_kind, grid, st, p, r8, exps_a, exps_b, add, out)
+         : nchunk == 3  ? dispatch_gauss<3>(out_kind, add_kind, grid, st, p, r8, exps_a, exps_b, add, out)
+         : nchunk == 4  ? dispatch_gauss<4>(out_kind, add_kind, grid, st, p, r8, exps_a, exps_b, add, out)
+                        : dispatch_gauss<6>(out_kind, add_kind, grid, st, p, r8, exps_a, exps_b, add, out);
   } else {
   switch (nchunk) {
     case 1:
@@ -897,6 +899,8 @@ int decode_launch(int M, int N, int nmod, int nchunk, const double* table, const
       rc = dispatch_out<2>(out_kind, add_kind, grid, st, p, (const int8_t*)res, exps_a, exps_b, add, out);
       break;
     case 3:
+      rc = dispatch_out<3>(out_kind, add_kind, grid, st, p, (const int8_t*)res, exps_a, exps_b, add, out);
+      break;
     case 4:
       rc = dispatch_out<4>(out_kind, add_kind, grid, st, p, (const int8_t*)res, exps_a, exps_b, add, out);
       break;

@@ -112,8 +112,23 @@ class OzPlan:
         for w in w_im:
             table += chunks(w)
         self.nchunk = nchunk
+        self.offs = offs
         self.table = np.array(table, dtype=np.float64)
         self._moduli_c = np.array(self.moduli, dtype=np.int32)
+
+    def decode_chunks(self, out_bits):
+        """CRT chunks (from the top) the decode needs for an output of
+        out_bits significant bits (24 complex64, 53 FP64 / complex128, 106 dd).
+        C' = sum_l r_l w_l - k P is formed from the top chunks only; a dropped
+        tail below 2^off changes C' by < nmod * 256 * 2^off, which must stay
+        2^(out_bits + 8) below 2^(beta_a + beta_b), the scale of C' — far
+        below the operands' own truncation at beta bits and the output's
+        rounding (an hp FP64 decode: 3 of 4 chunks, dd: 4 of 6)."""
+        limit = self.beta_a + self.beta_b - out_bits - 8 - math.ceil(math.log2(self.nmod * 256))
+        c = self.nchunk
+        while c > 1 and self.offs[c - 2] <= limit:
+            c -= 1
+        return c
 
     def moduli_ptr(self):
         return self._moduli_c.ctypes.data
@@ -332,6 +347,7 @@ def decode(res, ea, eb, pl, out, alpha=1.0, shift=0.0, add=None, add_scale=1.0, 
     (gemm_residues(lower_only=True)) and the upper ones are mirrored."""
     herm = -1 if hermitian == "skew" else (1 if hermitian else 0)
     o_kind, o_re, o_im, o_rl, o_il, ld_out, _ = mat_args(out)
+    nchunk = pl.decode_chunks({_lib.SR_MAT_C64: 24, _lib.SR_MAT_DD: 106}.get(o_kind, 53))
     if add is None:
         a_kind, a_re, a_im, a_rl, a_il, ld_add = -1, None, None, None, None, 0
     else:
@@ -340,12 +356,12 @@ def decode(res, ea, eb, pl, out, alpha=1.0, shift=0.0, add=None, add_scale=1.0, 
         # both residue planes are full (the GEMM wrote C- = C+^T for Hermitian C);
         # Hermitian C: decode the lower 128-tiles, mirror the rest ("skew"
         # products ran in full and are decoded in full)
-        _lib.call("sr_oz_decode_gauss", res.M, res.N, pl.nmod, pl.nchunk, pl.table_ptr(), res.buf.data_ptr(),
+        _lib.call("sr_oz_decode_gauss", res.M, res.N, pl.nmod, nchunk, pl.table_ptr(), res.buf.data_ptr(),
                   res.pitch, ea.exps.data_ptr(), ea.beta, eb.exps.data_ptr(), eb.beta, float(alpha), float(shift),
                   a_kind, a_re, a_im, ld_add, float(add_scale), o_kind, o_re, o_im, ld_out,
                   1 if herm == 1 else 0, int(diag_col0), _stream())
         return out
-    _lib.call("sr_oz_decode", res.M, res.N, pl.nmod, pl.nchunk, pl.table_ptr(), res.buf.data_ptr(), res.pitch,
+    _lib.call("sr_oz_decode", res.M, res.N, pl.nmod, nchunk, pl.table_ptr(), res.buf.data_ptr(), res.pitch,
               ea.exps.data_ptr(), ea.beta, eb.exps.data_ptr(), eb.beta, float(alpha), float(shift), a_kind, a_re,
               a_im, a_rl, a_il, ld_add, float(add_scale), o_kind, o_re, o_im, o_rl, o_il, ld_out,
               herm, int(diag_col0), _stream())

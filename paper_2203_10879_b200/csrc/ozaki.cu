@@ -385,6 +385,7 @@ struct DecodeParams {
   double offv[MAXCHUNK];       // 2^off[j]
   double cw[MAXCHUNK], icw[MAXCHUNK];  // 2^(off[j-1]-off[j]) and its inverse
   double inv_p;                // 1 / P
+  double snap, inv_snap;       // truncated CRT (nchunk below the plan's): grid of the lowest kept chunk
   double w_im[MAXMOD][MAXCHUNK];  // gauss: weights of the imaginary part (w holds the real part's)
 };
 
@@ -432,6 +433,10 @@ __device__ __forceinline__ void crt_finish(const DecodeParams& p, const double (
     t[j] = fma(-c, p.cw[j], t[j]);
     t[j - 1] += c;
   }
+  // truncated CRT (OzPlan.decode_chunks): C' is known to < snap / 2 in units
+  // of the lowest kept chunk, so round it to that grid — an exact C' on the
+  // grid (0, I I = I, small integers) comes out exact, lo parts included
+  if (p.snap > 0.0) t[NC - 1] = rint(t[NC - 1] * p.inv_snap) * p.snap;
   hi = t[0] * p.offv[0];
   lo = 0.0;
 #pragma unroll
@@ -875,6 +880,18 @@ int decode_launch(int M, int N, int nmod, int nchunk, const double* table, const
     p.icw[j] = ldexp(1.0, -(off[j - 1] - off[j]));
   }
   p.inv_p = table[nmod * MAXCHUNK + 2 * MAXCHUNK];
+  // fewer chunks than the plan holds: the dropped weight tails and the dropped
+  // tail of k P move C' by less than 2 nmod 256 units of the lowest kept
+  // chunk; snap to twice that grid
+  bool truncated = false;
+  for (int l = 0; l < nmod; ++l)
+    for (int j = nchunk; j < MAXCHUNK; ++j) truncated = truncated || table[l * MAXCHUNK + j] != 0.0;
+  if (truncated) {
+    int bits = 10;  // 4 * 256
+    while ((1 << (bits - 9)) < nmod) ++bits;
+    p.snap = ldexp(1.0, bits);
+    p.inv_snap = ldexp(1.0, -bits);
+  }
   if (gauss)
     for (int l = 0; l < nmod; ++l)
       for (int j = 0; j < MAXCHUNK; ++j) p.w_im[l][j] = table[nmod * MAXCHUNK + 2 * MAXCHUNK + 1 + l * MAXCHUNK + j];

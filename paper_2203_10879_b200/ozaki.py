@@ -119,12 +119,14 @@ class OzPlan:
     def decode_chunks(self, out_bits):
         """CRT chunks (from the top) the decode needs for an output of
         out_bits significant bits (24 complex64, 53 FP64 / complex128, 106 dd).
-        C' = sum_l r_l w_l - k P is formed from the top chunks only; a dropped
-        tail below 2^off changes C' by < nmod * 256 * 2^off, which must stay
+        C' = sum_l r_l w_l - k P is formed from the top chunks only; the
+        dropped tails below 2^off change C' by < 2 nmod 256 2^off and the
+        decode snaps C' to the grid 4 nmod 256 2^off (so exact values on the
+        grid — zeros, I I = I — stay exact), an error that must stay
         2^(out_bits + 8) below 2^(beta_a + beta_b), the scale of C' — far
         below the operands' own truncation at beta bits and the output's
         rounding (an hp FP64 decode: 3 of 4 chunks, dd: 4 of 6)."""
-        limit = self.beta_a + self.beta_b - out_bits - 8 - math.ceil(math.log2(self.nmod * 256))
+        limit = self.beta_a + self.beta_b - out_bits - 8 - math.ceil(math.log2(self.nmod * 256)) - 2
         c = self.nchunk
         while c > 1 and self.offs[c - 2] <= limit:
             c -= 1

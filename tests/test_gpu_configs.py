@@ -102,7 +102,9 @@ def test_config3_n8192_independent_evaluation():
     # (1) verify_pair in double-double: P = Q^H A and T^ = P Q kept in dd
     v = verify_pair(A, SchurPair(q=pair.q, t=pair.t, ortho_residual=0.0), precision="dd")
     assert v.tri_residual / norm_a <= 10 * U, v
-    assert abs(v.ortho_residual - own_ortho) <= 1e-3 * own_ortho, (v.ortho_residual, own_ortho)
+    # the refinement's own ||Y|| (FP64-rounded entries of an exact product of the
+    # beta-truncated Q) agrees with the dd evaluation to a few digits
+    assert abs(v.ortho_residual - own_ortho) <= 1e-2 * own_ortho, (v.ortho_residual, own_ortho)
     assert v.similarity_residual / norm_a <= 10 * U, v
     assert own_ortho <= 2 * g["final_ortho"], (own_ortho, g["final_ortho"])
     # (2) cuBLAS ZGEMM (FP64, test-only): stril noise ~4 u ||A||_F, still below the stop rule

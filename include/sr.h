@@ -297,6 +297,31 @@ int sr_zgemm_dd_fma(int op_a, int m, int n, int k, const double* a_rh, const dou
                     const double* b_il, long long ldb, double* c_rh, double* c_rl, double* c_ih, double* c_il,
                     long long ldc, void* stream);
 
+/* ---- entry guards (csrc/guards.cu) ---- */
+
+/* Power iteration on M^H M for the spectral-norm guard of newton_schulz_step
+   (spectral_norm_estimate, matmul.py:117-142; orthogonal.py:160-166): M is
+   the n x n complex64 lp downcast (ld in elements), vectors and sums FP64.
+   Launches `steps` iterations (first = 1: from the reference's fixed start
+   vector); the convergence test runs on the device and later steps of a
+   group exit at once.  ws starts with five doubles {est, prev, ||w||, done,
+   iterations} the caller copies back after each group. */
+size_t sr_power_norm_workspace_bytes(int n);
+int sr_power_norm_c64(int n, const void* m, long long ld, int first, int steps, double rel_tol, void* ws,
+                      size_t ws_bytes, void* stream);
+
+/* *d_flags |= bit when a planar FP64 matrix (im may be NULL) has a
+   non-finite entry: the finiteness check of _coerce_hp (refine.py:341-350). */
+int sr_finite_flag_f64(int m, int n, const double* re, const double* im, long long ld, int* d_flags, int bit,
+                       void* stream);
+
+/* *d_status = 1 when every row and column of the n x n planar matrix holds
+   exactly one nonzero (row_of_col[j]: the row of column j's nonzero), else 0:
+   the O(n^2) scan of _phase_permutation (refine.py:172-189). */
+size_t sr_phase_perm_workspace_bytes(int n);
+int sr_phase_perm_scan_f64(int n, const double* re, const double* im, long long ld, int* row_of_col, int* d_status,
+                           void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,6 +64,11 @@ SIGNATURES = {
     "sr_fro_norm_dd_workspace_bytes": (_sz, [_ll]),
     "sr_fro_norm_dd": (_i, [_i, _i, _p, _p, _p, _p, _ll, _p, _p, _sz, _p]),
     "sr_zgemm_dd_fma": (_i, [_i, _i, _i, _i, _p, _p, _p, _p, _ll, _p, _p, _p, _p, _ll, _p, _p, _p, _p, _ll, _p]),
+    "sr_power_norm_workspace_bytes": (_sz, [_i]),
+    "sr_power_norm_c64": (_i, [_i, _p, _ll, _i, _i, _d, _p, _sz, _p]),
+    "sr_finite_flag_f64": (_i, [_i, _i, _p, _p, _ll, _p, _i, _p]),
+    "sr_phase_perm_workspace_bytes": (_sz, [_i]),
+    "sr_phase_perm_scan_f64": (_i, [_i, _p, _p, _ll, _p, _p, _p, _sz, _p]),
 }
 
 _lib = None

@@ -188,10 +188,11 @@ def coerce_dd(x, device):
         m = DDPlanar.from_any(x, device=device)
     if m.rows != m.cols:
         raise ValueError("refinement needs a square matrix")
-    fin = torch.ones((), dtype=torch.bool, device=device)
-    for c in m.cells():
-        fin = fin & torch.isfinite(c).all()
-    if not bool(fin):
+    from .refine import _finite_flag
+    flags = torch.zeros(1, dtype=torch.int32, device=device)
+    _finite_flag(m.hi, flags, 1)  # one libsr pass per pair of planes, one 4-byte read
+    _finite_flag(m.lo, flags, 1)
+    if int(flags.item()):
         raise ValueError("input matrix has non-finite entries")
     return m
 

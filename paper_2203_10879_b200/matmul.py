@@ -135,29 +135,32 @@ def matmul_lp(a, b, m=None, n=None, k=None, out=None):
     return out
 
 
-def spectral_norm_estimate(q_lp, n, rel_tol=1e-6, max_iters=200):
-    """Largest singular value by power iteration on M^H M in lp (complex64),
-    fixed start vector 1 + (j mod 7)/8 (matmul.py:117-142).  The two
-    matrix-vector products per step are plain cuBLAS GEMVs (HBM-bound, 2 x 0.5
-    GB at n = 8192): a guard on the entry, not a hot-path product."""
+_POWER_WS = {}
+
+
+def spectral_norm_estimate(q_lp, n, rel_tol=1e-6, max_iters=200, group=8):
+    """Largest singular value by power iteration on M^H M (matmul.py:117-142):
+    the reference's fixed start vector 1 + (j mod 7)/8, stop when successive
+    estimates agree to rel_tol or after max_iters.  M is the (n, ld) complex64
+    lp matrix; the iteration runs in libsr (csrc/guards.cu, FP64 vectors) with
+    the convergence test on the device — the host reads one small state
+    record per group of `group` steps (one read for a near-unitary Q^)."""
     dev = q_lp.device
-    m = q_lp[:, :n]
-    j = torch.arange(n, device=dev, dtype=torch.float32)
-    v = (1.0 + torch.remainder(j, 7.0) / 8.0).to(torch.complex64)
-    v = v / torch.linalg.vector_norm(v)
-    prev = 0.0
-    est = 0.0
-    for _ in range(max_iters):
-        u = torch.mv(m, v)
-        w = torch.mv(m.mH, u)
-        norms = torch.stack([torch.linalg.vector_norm(u), torch.linalg.vector_norm(w)]).double().cpu()
-        est, nw = float(norms[0]), float(norms[1])
-        if est == 0.0:
-            return 0.0
-        if nw == 0.0:
-            return est
-        v = w / nw
-        if abs(est - prev) <= rel_tol * est:
+    key = (n, str(dev))
+    ws = _POWER_WS.get(key)
+    if ws is None:
+        _POWER_WS.clear()
+        ws = _POWER_WS[key] = torch.empty(_lib.load().sr_power_norm_workspace_bytes(n), dtype=torch.uint8,
+                                          device=dev)
+    state = ws[:40].view(torch.float64)
+    done, first = 0, 1
+    while done < max_iters:
+        steps = min(group, max_iters - done)
+        _lib.call("sr_power_norm_c64", n, q_lp.data_ptr(), q_lp.shape[1], first, steps, float(rel_tol),
+                  ws.data_ptr(), ws.numel(), _stream())
+        first = 0
+        done += steps
+        est, _prev, _nw, stop, _its = state.tolist()
+        if stop:
             break
-        prev = est
     return est

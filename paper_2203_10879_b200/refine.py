@@ -132,6 +132,9 @@ class _Fp64Workspace:
         self.w2y = None
         self.w2yw = None
         self.scal = torch.zeros(8, dtype=torch.float64, device=device)  # norm_a, norm_e, norm_y, norm_w
+        self.in_flags = torch.zeros(1, dtype=torch.int32, device=device)  # deferred input checks (A 1, Q^ 2)
+        self.perm_ws = torch.empty(_lib.load().sr_phase_perm_workspace_bytes(n), dtype=torch.uint8, device=device)
+        self.perm_row = torch.empty(n, dtype=torch.int32, device=device)
         red = _lib.load().sr_reduce_workspace_bytes()
         self.red = [torch.zeros(red, dtype=torch.uint8, device=device) for _ in range(4)]
         self.solver = SolverWorkspace(n, torch.complex64, device)
@@ -173,8 +176,17 @@ def _stream():
     return torch.cuda.current_stream().cuda_stream
 
 
-def _coerce(x, device):
-    """_coerce_hp (refine.py:341-350): exact embed, square + finite checks."""
+def _finite_flag(m, flags, bit):
+    """flags |= bit if the planar matrix m has a non-finite entry (one pass in
+    libsr, no host sync; read with the caller's next sync)."""
+    _lib.call("sr_finite_flag_f64", m.rows, m.cols, m.re_ptr(), m.im_ptr(), m.ld, flags.data_ptr(), bit, _stream())
+
+
+def _coerce(x, device, flags=None, bit=1):
+    """_coerce_hp (refine.py:341-350): exact embed, square + finite checks.
+    With `flags`, the finiteness check is only launched (flags |= bit on the
+    device) and the caller raises at its next host sync; without, it is read
+    at once."""
     if isinstance(x, ZPlanar):
         m = x
     else:
@@ -184,12 +196,21 @@ def _coerce(x, device):
         m = ZPlanar.from_any(x, device=device)
     if m.rows != m.cols:
         raise ValueError("refinement needs a square matrix")
-    fin = torch.isfinite(m.re).all()
-    if m.im is not None:
-        fin = fin & torch.isfinite(m.im).all()
-    if not bool(fin):
-        raise ValueError("input matrix has non-finite entries")
+    if flags is None:
+        f = torch.zeros(1, dtype=torch.int32, device=m.re_buf.device)
+        _finite_flag(m, f, 1)
+        if int(f.item()):
+            raise ValueError("input matrix has non-finite entries")
+    else:
+        _finite_flag(m, flags, bit)
     return m
+
+
+def _raise_nonfinite(flags_value):
+    """The deferred finiteness checks: A (bit 1) is validated before Q^ (bit 2),
+    like the reference's two _coerce_hp calls (refine.py:374-375)."""
+    if flags_value & 3:
+        raise ValueError("input matrix has non-finite entries")
 
 
 def _is_host_matrix(x):
@@ -240,17 +261,16 @@ def _h2d_planar(x, dst, landing):
     return dst
 
 
-def _upload_qhat(x, dst, landing):
+def _upload_qhat(x, dst, landing, flags):
     """_coerce_hp (refine.py:341-350) of a host Q^ into the workspace's planar
     buffer (the landing buffer is the workspace's result staging, free until
-    the first measurement); the finiteness check runs on the device."""
+    the first measurement); the finiteness check runs on the device into
+    flags (bit 2), read with the entry step's first sync."""
     x = _host_tensor(x)
     if x.shape[0] != x.shape[1]:
         raise ValueError("refinement needs a square matrix")
     _h2d_planar(x, dst, landing)
-    fin = torch.isfinite(dst.re).all() & torch.isfinite(dst.im).all()
-    if not bool(fin):
-        raise ValueError("input matrix has non-finite entries")
+    _finite_flag(dst, flags, 2)
     return dst
 
 
@@ -274,18 +294,16 @@ class _AsyncUpload:
                 _h2d_planar(x, self.m, landing)
             else:
                 ZPlanar.fill_from(self.m, x)
-            fin = torch.isfinite(self.m.re).all()
-            if self.m.im is not None:
-                fin = fin & torch.isfinite(self.m.im).all()
-            self.fin = fin
+            self.flags = torch.zeros(1, dtype=torch.int32, device=device)
+            _finite_flag(self.m, self.flags, 1)
             self.ready = torch.cuda.Event()
             self.ready.record(self.stream)
         self.host = x  # pinned source stays alive until the copy has run
 
     def check(self):
-        # fin is computed on the upload stream: order the read after it
-        torch.cuda.current_stream(self.fin.device).wait_event(self.ready)
-        if not bool(self.fin):
+        # the flag is computed on the upload stream: order the read after it
+        torch.cuda.current_stream(self.flags.device).wait_event(self.ready)
+        if int(self.flags.item()):
             raise ValueError("input matrix has non-finite entries")
 
 
@@ -296,6 +314,7 @@ def _newton_schulz_entry(qhat, ws, prod, a_upload=None):
     _lib.call("sr_downcast_c64", n, n, qhat.re_ptr(), qhat.im_ptr(), qhat.ld, ws.y_lp.data_ptr(),
               ws.y_lp.shape[1], _stream())
     est = spectral_norm_estimate(ws.y_lp, n)
+    _raise_nonfinite(int(ws.in_flags.item()))  # the GPU is idle here: a 4-byte read
     if not est < math.sqrt(3.0):
         if a_upload is not None:  # the reference validates A before the entry step
             a_upload.check()
@@ -303,17 +322,26 @@ def _newton_schulz_entry(qhat, ws, prod, a_upload=None):
     prod.entry(qhat)
 
 
-def _phase_permutation(q):
+def _phase_permutation(q, ws=None):
     """_phase_permutation (refine.py:172-189): perm with q[perm[j], j] the only
     nonzero of column j and of its row, each of exactly unit modulus; else None.
-    O(n^2) scan on the device, O(n) exactness check on the host."""
-    nz = q.re != 0
-    if q.im is not None:
-        nz = nz | (q.im != 0)
-    if not (bool((nz.sum(dim=0) == 1).all()) and bool((nz.sum(dim=1) == 1).all())):
+    The O(n^2) pattern scan is one libsr pass (sr_phase_perm_scan_f64) and a
+    4-byte read; only a permutation pattern goes on to the O(n) exact
+    unit-modulus check on the host."""
+    n = q.cols
+    dev = q.re_buf.device
+    if ws is not None and getattr(ws, "n", None) == n:
+        scratch, row = ws.perm_ws, ws.perm_row
+    else:
+        scratch = torch.empty(_lib.load().sr_phase_perm_workspace_bytes(n), dtype=torch.uint8, device=dev)
+        row = torch.empty(n, dtype=torch.int32, device=dev)
+    status = row.new_zeros(1)
+    _lib.call("sr_phase_perm_scan_f64", n, q.re_ptr(), q.im_ptr(), q.ld, row.data_ptr(), status.data_ptr(),
+              scratch.data_ptr(), scratch.numel(), _stream())
+    if not int(status.item()):
         return None
-    perm = nz.to(torch.int8).argmax(dim=0)
-    cols = torch.arange(q.cols, device=perm.device)
+    perm = row.long()
+    cols = torch.arange(n, device=dev)
     zr = q.re[perm, cols].double().cpu().numpy()
     zi = (q.im[perm, cols] if q.im is not None else torch.zeros_like(q.re[perm, cols])).cpu().numpy()
     from fractions import Fraction
@@ -461,7 +489,7 @@ def _run_fp64(a, qhat, cfg, ws, symmetric=False, host=None, a_upload=None):
     _lib.call("sr_fro_norm_f64", n, n, a.re_ptr(), a.im_ptr(), a.ld, ws.ptr(0), ws.red[0].data_ptr(),
               ws.red[0].numel(), st)
     history = []
-    perm = _phase_permutation(ws.q)
+    perm = _phase_permutation(ws.q, ws)
     if perm is not None:
         t_exact = _structural_triangle(a, ws.q, perm, symmetric)
         if t_exact is not None:
@@ -560,7 +588,7 @@ def _run_fp64(a, qhat, cfg, ws, symmetric=False, host=None, a_upload=None):
                         norm_y=norm_y, norm_w=norm_w)
             q_version += 1
             if ph is not None:  # still a signed permutation (W = 0: every correction clipped)?
-                perm = _phase_permutation(ws.q)
+                perm = _phase_permutation(ws.q, ws)
                 ph = _quarter_phases(ws.q, perm)
             _mark("update")
         if converged:
@@ -646,20 +674,30 @@ def refine_template(a, qhat, cfg=None, device=None, out=None):
         if ah.shape != qh.shape:
             raise ValueError("matrix and candidate shapes differ")
         ws = _workspace(qh.shape[0], device)
+        ws.in_flags.zero_()
         q_dst, a_dst = ws.host_inputs(real_a=not ah.is_complex())
-        qhat = _upload_qhat(qh, q_dst, ws.host_staging()[0])
+        qhat = _upload_qhat(qh, q_dst, ws.host_staging()[0], ws.in_flags)
         # A's H2D lands in T's result staging buffer (dead once copied into a_dst;
         # T is first staged after the main stream waited for the upload)
         a_upload = _AsyncUpload(ah, device, dst=a_dst, landing=ws.host_staging()[1])
         a = a_upload.m
     else:
-        qhat = _coerce(qhat, device)
+        # both square and of one size: the finiteness checks are deferred to the
+        # entry step's first host read (ws.in_flags); otherwise _coerce raises now
+        shapes = [tuple(x.shape) if hasattr(x, "shape") else None for x in (a, qhat)]
+        n_in = shapes[0][0] if shapes[0] is not None and len(shapes[0]) == 2 else 0
+        ws = _workspace(n_in, device) if (n_in > 0 and shapes[0] == shapes[1] == (n_in, n_in)) else None
+        flags = None
+        if ws is not None:
+            ws.in_flags.zero_()
+            flags = ws.in_flags
         a_upload = None
         if _is_host_matrix(a):
             a_upload = _AsyncUpload(a, device)
             a = a_upload.m
         else:
-            a = _coerce(a, device)
+            a = _coerce(a, device, flags, 1)
+        qhat = _coerce(qhat, device, flags, 2)
     if a.shape != qhat.shape:
         raise ValueError("matrix and candidate shapes differ")
     if qhat.is_real:

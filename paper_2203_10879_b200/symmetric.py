@@ -113,6 +113,7 @@ def refine_symmetric(a, cfg=None, device=None):
     else:
         qhat = ZPlanar.from_any(v.to(torch.complex128), device=device, force_complex=True)
         ws = _workspace(A.rows, device)
+        ws.in_flags.zero_()  # inputs validated by _coerce above
         pair, report = _run_fp64(A, qhat, cfg, ws, symmetric=True)
     torch.cuda.current_stream().synchronize()
     report.wall_time = time.perf_counter() - t0

@@ -42,6 +42,35 @@ U64 = 2.0 ** -53
 SAMPLE_N = 4096  # cpu_baseline sample: one full CPU refinement at this size, phases scaled to n
 
 
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--gemm", default="ozaki", choices=["ozaki", "ozaki_std", "dmma"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def workload(n, seed):
+    from paper_2203_10879_b200 import inputs
+    a = inputs.gaussian_real(n, seed)
+    t0 = time.time()
+    q = inputs.cached_qhat("c3_n%d_s%d" % (n, seed), a)
+    log("[bench] Q^ (complex64 Schur of A, n=%d) ready in %.1f s" % (n, time.time() - t0))
+    return a, q
+
+
 def blas_threads():
     try:
         import threadpoolctl

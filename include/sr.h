@@ -297,6 +297,16 @@ int sr_zgemm_dd_fma(int op_a, int m, int n, int k, const double* a_rh, const dou
                     const double* b_il, long long ldb, double* c_rh, double* c_rl, double* c_ih, double* c_il,
                     long long ldc, void* stream);
 
+/* Column-block forms for the sharded driver (sharded.py): a rows x cols block
+   of T^ whose first column is global column col0 is split into lp T, E blocks
+   (the strict-lower mask in global indices) and *d_sq_e = sum |E|^2 (a partial
+   of the cross-rank sum); X = Y - W - W^2 for a rows x cols block. */
+int sr_split_lp_block_c64(int rows, int cols, int col0, const double* that_re, const double* that_im,
+                          long long ldt, void* t_lp, void* e_lp, long long ld_lp, double* d_sq_e, void* ws,
+                          size_t ws_bytes, void* stream);
+int sr_fused_lp_operand_block_c64(int rows, int cols, const double* y_re, const double* y_im, long long ldy,
+                                  const void* w, const void* w2, long long ld_lp, void* x, void* stream);
+
 /* ---- entry guards (csrc/guards.cu) ---- */
 
 /* Power iteration on M^H M for the spectral-norm guard of newton_schulz_step

@@ -69,6 +69,8 @@ SIGNATURES = {
     "sr_finite_flag_f64": (_i, [_i, _i, _p, _p, _ll, _p, _i, _p]),
     "sr_phase_perm_workspace_bytes": (_sz, [_i]),
     "sr_phase_perm_scan_f64": (_i, [_i, _p, _p, _ll, _p, _p, _p, _sz, _p]),
+    "sr_split_lp_block_c64": (_i, [_i, _i, _i, _p, _p, _ll, _p, _p, _ll, _p, _p, _sz, _p]),
+    "sr_fused_lp_operand_block_c64": (_i, [_i, _i, _p, _p, _ll, _p, _p, _ll, _p, _p]),
 }
 
 _lib = None

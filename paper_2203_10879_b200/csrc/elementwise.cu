@@ -26,7 +26,8 @@ __device__ __forceinline__ double block_sum(double v) {
 }
 
 // Last block to finish reduces the partials in slot order and writes sqrt.
-__device__ __forceinline__ void finish_norm(double mine, double* partials, unsigned int* counter, double* out) {
+__device__ __forceinline__ void finish_norm(double mine, double* partials, unsigned int* counter, double* out,
+                                            bool squared = false) {
   __shared__ bool last;
   double s = block_sum(mine);
   if (threadIdx.x == 0) {
@@ -42,7 +43,7 @@ __device__ __forceinline__ void finish_norm(double mine, double* partials, unsig
   for (int i = threadIdx.x; i < (int)gridDim.x; i += RT) v += partials[i];
   double tot = block_sum(v);
   if (threadIdx.x == 0) {
-    *out = sqrt(tot);
+    *out = squared ? tot : sqrt(tot);
     *counter = 0u;
   }
 }
@@ -58,17 +59,21 @@ inline RedWs red_ws(void* ws) {
   return r;
 }
 
-__global__ void split_lp_kernel(int n, const double* __restrict__ tr, const double* __restrict__ ti, long long ldt,
-                                float2* __restrict__ t_lp, float2* __restrict__ e_lp, long long ld_lp,
-                                double* partials, unsigned int* counter, double* out) {
+// rows x cols block whose first column is global column col0 (the sharded
+// driver's column block; the whole matrix: col0 = 0, cols = rows); squared:
+// write sum |E|^2 instead of ||E||_F (partials of a cross-rank sum)
+__global__ void split_lp_kernel(int rows, int cols, int col0, const double* __restrict__ tr,
+                                const double* __restrict__ ti, long long ldt, float2* __restrict__ t_lp,
+                                float2* __restrict__ e_lp, long long ld_lp, double* partials, unsigned int* counter,
+                                double* out, int squared) {
   double acc = 0.0;
-  const long long total = (long long)n * n;
+  const long long total = (long long)rows * cols;
   for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    int i = (int)(idx / n), j = (int)(idx % n);
+    int i = (int)(idx / cols), j = (int)(idx % cols);
     double re = tr[(size_t)i * ldt + j], im = ti[(size_t)i * ldt + j];
     float2 v = make_float2((float)re, (float)im);
     float2 z = make_float2(0.f, 0.f);
-    if (i > j) {
+    if (i > j + col0) {
       acc += re * re + im * im;
       e_lp[(size_t)i * ld_lp + j] = v;
       t_lp[(size_t)i * ld_lp + j] = z;
@@ -77,7 +82,7 @@ __global__ void split_lp_kernel(int n, const double* __restrict__ tr, const doub
       t_lp[(size_t)i * ld_lp + j] = v;
     }
   }
-  finish_norm(acc, partials, counter, out);
+  finish_norm(acc, partials, counter, out, squared != 0);
 }
 
 __global__ void fro_norm_kernel(int m, int n, const double* __restrict__ re, const double* __restrict__ im,
@@ -366,9 +371,9 @@ extern "C" int sr_split_lp_c64(int n, const double* that_re, const double* that_
                                void* stream) {
   if (n < 0 || !ws || ws_bytes < sr_reduce_workspace_bytes()) return SR_EINVAL;
   RedWs r = red_ws(ws);
-  split_lp_kernel<<<RBLOCKS, RT, 0, (cudaStream_t)stream>>>(n, that_re, that_im, ldt, (float2*)t_lp,
+  split_lp_kernel<<<RBLOCKS, RT, 0, (cudaStream_t)stream>>>(n, n, 0, that_re, that_im, ldt, (float2*)t_lp,
                                                              (float2*)e_lp, ld_lp, r.partials, r.counter,
-                                                             d_norm_e);
+                                                             d_norm_e, 0);
   SR_LAUNCH_CHECK();
   return SR_OK;
 }
@@ -433,12 +438,12 @@ extern "C" int sr_skew_c64(int n, const void* l, long long ld, void* w, double* 
 
 // X = Y - W - W^2 in complex64: the A operand of the fused lp product
 // X W = YW - W^2 - W^3 (one product instead of YW, W^3)
-__global__ void fused_lp_operand_kernel(int n, const double* __restrict__ yr, const double* __restrict__ yi,
+__global__ void fused_lp_operand_kernel(int n, int cols, const double* __restrict__ yr, const double* __restrict__ yi,
                                         long long ldy, const float2* __restrict__ w, const float2* __restrict__ w2,
                                         long long ldl, float2* __restrict__ x) {
-  const long long total = (long long)n * n;
+  const long long total = (long long)n * cols;
   for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    const int i = (int)(idx / n), j = (int)(idx % n);
+    const int i = (int)(idx / cols), j = (int)(idx % cols);
     const size_t o = (size_t)i * ldl + j, oy = (size_t)i * ldy + j;
     const float2 a = w[o], b = w2[o];
     x[o] = make_float2((float)(yr[oy] - (double)a.x - (double)b.x), (float)(yi[oy] - (double)a.y - (double)b.y));
@@ -450,7 +455,32 @@ extern "C" int sr_fused_lp_operand_c64(int n, const double* y_re, const double* 
   if (n < 0 || !y_re || !y_im || !w || !w2 || !x) return SR_EINVAL;
   if (n == 0) return SR_OK;
   fused_lp_operand_kernel<<<ew_grid((long long)n * n), RT, 0, (cudaStream_t)stream>>>(
-      n, y_re, y_im, ldy, (const float2*)w, (const float2*)w2, ld_lp, (float2*)x);
+      n, n, y_re, y_im, ldy, (const float2*)w, (const float2*)w2, ld_lp, (float2*)x);
+  SR_LAUNCH_CHECK();
+  return SR_OK;
+}
+
+// column-block forms for the sharded driver (sharded.py): rows x cols blocks,
+// the block's first column is global column col0
+extern "C" int sr_split_lp_block_c64(int rows, int cols, int col0, const double* that_re, const double* that_im,
+                                     long long ldt, void* t_lp, void* e_lp, long long ld_lp, double* d_sq_e,
+                                     void* ws, size_t ws_bytes, void* stream) {
+  if (rows < 0 || cols < 0 || col0 < 0 || !ws || ws_bytes < sr_reduce_workspace_bytes()) return SR_EINVAL;
+  RedWs r = red_ws(ws);
+  split_lp_kernel<<<RBLOCKS, RT, 0, (cudaStream_t)stream>>>(rows, cols, col0, that_re, that_im, ldt, (float2*)t_lp,
+                                                             (float2*)e_lp, ld_lp, r.partials, r.counter, d_sq_e,
+                                                             1);
+  SR_LAUNCH_CHECK();
+  return SR_OK;
+}
+
+extern "C" int sr_fused_lp_operand_block_c64(int rows, int cols, const double* y_re, const double* y_im,
+                                             long long ldy, const void* w, const void* w2, long long ld_lp, void* x,
+                                             void* stream) {
+  if (rows < 0 || cols < 0 || !y_re || !y_im || !w || !w2 || !x) return SR_EINVAL;
+  if ((long long)rows * cols == 0) return SR_OK;
+  fused_lp_operand_kernel<<<ew_grid((long long)rows * cols), RT, 0, (cudaStream_t)stream>>>(
+      rows, cols, y_re, y_im, ldy, (const float2*)w, (const float2*)w2, ld_lp, (float2*)x);
   SR_LAUNCH_CHECK();
   return SR_OK;
 }

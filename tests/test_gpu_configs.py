@@ -107,14 +107,17 @@ def test_config3_n8192_independent_evaluation():
     assert abs(v.ortho_residual - own_ortho) <= 1e-2 * own_ortho, (v.ortho_residual, own_ortho)
     assert v.similarity_residual / norm_a <= 10 * U, v
     assert own_ortho <= 2 * g["final_ortho"], (own_ortho, g["final_ortho"])
-    # (2) cuBLAS ZGEMM (FP64, test-only): stril noise ~4 u ||A||_F, still below the stop rule
+    # (2) cuBLAS ZGEMM (FP64, test-only): its own accumulation noise on
+    # stril(Q^H A Q) is ~20 u ||A||_F at n = 8192 (measured 2.4e-15 — above
+    # the 10 u stop rule, the reason the products are exact Ozaki-II ones,
+    # DESIGN.md §3.1), so it confirms the residual only to that noise floor
     qd = pair.q
     ad = torch.from_numpy(a).to(dev).to(torch.complex128)
     that = (qd.conj().T @ ad) @ qd
     rel_z = float(torch.linalg.norm(torch.tril(that, -1))) / norm_a
     ortho_z = float(torch.linalg.norm(qd.conj().T @ qd - torch.eye(n, dtype=torch.complex128, device=dev)))
     del that, ad
-    assert rel_z <= 10 * U, rel_z
+    assert rel_z <= 50 * U, rel_z
     assert ortho_z <= 2 * g["final_ortho"], (ortho_z, g["final_ortho"])
 
 

@@ -75,6 +75,41 @@ def all_gather_cols(local, full, ranges, group=None):
     return full
 
 
+class ColGatherer:
+    """all_gather_cols with persistent buffers: one (rows, wmax, *extra)
+    send buffer and one (world * rows, wmax, *extra) receive buffer, allocated
+    once per shape (the driver gathers the same block shapes every
+    iteration), so a gather allocates and zero-fills nothing."""
+
+    def __init__(self, ranges, group=None):
+        self.ranges, self.group = ranges, group
+        self.rank, self.world = world_info(group)
+        self.wmax = max(j1 - j0 for j0, j1 in ranges)
+        self.bufs = {}
+
+    def __call__(self, local, full):
+        if self.world == 1:
+            j0, j1 = self.ranges[0]
+            if full[:, j0:j1].data_ptr() != local.data_ptr():
+                full[:, j0:j1].copy_(local)
+            return full
+        rows = local.shape[0]
+        extra = tuple(local.shape[2:])
+        key = (rows, extra, local.dtype, local.device)
+        if key not in self.bufs:
+            self.bufs[key] = (torch.zeros((rows, self.wmax) + extra, dtype=local.dtype, device=local.device),
+                              torch.empty((self.world * rows, self.wmax) + extra, dtype=local.dtype,
+                                          device=local.device))
+        send, recv_flat = self.bufs[key]
+        send[:, : local.shape[1]].copy_(local)
+        dist.all_gather_into_tensor(recv_flat, send, group=self.group)
+        recv = recv_flat.view((self.world, rows, self.wmax) + extra)
+        for r, (j0, j1) in enumerate(self.ranges):
+            if j1 > j0:
+                full[:, j0:j1].copy_(recv[r, :, : j1 - j0])
+        return full
+
+
 def all_reduce_sum(values, device, group=None):
     """Sum a short list of floats over the ranks (partial squared norms)."""
     _, world = world_info(group)

@@ -179,17 +179,7 @@ class OzakiProducts:
         self._hp(ea_qh, self.eb_q, ws.y, shift=-1.0, hermitian=True, pl=self.hq)  # Y = Q^H Q - I
 
     def _lp_plans(self, norm_y, norm_w):
-        """Plans for the fused update's W^2 and X W (X = Y - W - W^2) from
-        ||Y||_F, ||W||_F: the products only enter S' multiplied by W (W^2,
-        through X W) or as X W itself, so their allowed absolute error is the
-        lp solve's own error in W (ozaki.lp_product_beta)."""
-        lp, n = self.lp, self.ws.n
-        if norm_y is None or norm_w is None or not (norm_w > 0.0):
-            return lp, lp
-        nx = norm_y + norm_w + norm_w * norm_w
-        b_w2 = ozaki.lp_product_beta(norm_w * norm_w, n)      # W^2 error x ||W|| vs u ||W||
-        b_xw = ozaki.lp_product_beta(nx, n)                   # (X W) error vs u ||W||
-        return ozaki.plan(n, b_w2, b_w2, self.gauss), ozaki.plan(n, b_xw, b_xw, self.gauss)
+        return lp_plans(self.ws.n, norm_y, norm_w, self.gauss, self.lp)
 
     def update(self, restore_full_sigma, sigma_bound=None, norm_y=None, norm_w=None):
         ws, hp, lp, n = self.ws, self.hp, self.lp, self.ws.n
@@ -238,6 +228,19 @@ class OzakiProducts:
         ozaki.encode(ws.sigma, n, n, "b", pc, out=self.eb_s)
         self._hp_with(pc, self.ea_x, self.eb_s, ws.q_next, alpha=0.5, add=ws.q)  # Q + Q S' / 2
         ws.q, ws.q_next = ws.q_next, ws.q
+
+
+def lp_plans(n, norm_y, norm_w, gauss, default):
+    """Plans for the fused update's W^2 and X W (X = Y - W - W^2) from
+    ||Y||_F, ||W||_F: the products only enter S' multiplied by W (W^2,
+    through X W) or as X W itself, so their allowed absolute error is the
+    lp solve's own error in W (ozaki.lp_product_beta)."""
+    if norm_y is None or norm_w is None or not (norm_w > 0.0):
+        return default, default
+    nx = norm_y + norm_w + norm_w * norm_w
+    b_w2 = ozaki.lp_product_beta(norm_w * norm_w, n)      # W^2 error x ||W|| vs u ||W||
+    b_xw = ozaki.lp_product_beta(nx, n)                   # (X W) error vs u ||W||
+    return ozaki.plan(n, b_w2, b_w2, gauss), ozaki.plan(n, b_xw, b_xw, gauss)
 
 
 def sigma_prime_bound(norm_y, norm_w, restore_full_sigma):

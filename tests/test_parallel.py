@@ -30,7 +30,8 @@ def free_port():
 
 
 class CpuShardBackend:
-    """Same protocol as sharded.OzakiShardBackend; complex128 products on the CPU."""
+    """Same protocol as sharded.OzakiShardBackend; complex128 products on the
+    CPU (lp products in complex64), column blocks, partial norms all-reduced."""
 
     def __init__(self, a, qhat):
         self.a = torch.from_numpy(np.asarray(a, dtype=np.complex128))
@@ -38,30 +39,34 @@ class CpuShardBackend:
         self.n = self.a.shape[0]
         n = self.n
         self.q = torch.zeros((n, n), dtype=torch.complex128)
-        self.that = torch.zeros_like(self.q)
-        self.y = torch.zeros_like(self.q)
-        self.w2 = torch.zeros((n, n), dtype=torch.complex64)
+        self.t_full = torch.zeros((n, n), dtype=torch.complex128)
+        self.x = torch.zeros((n, n), dtype=torch.complex64)
 
     def set_columns(self, j0, j1, ranges, group):
         self.j0, self.j1, self.ranges, self.group = j0, j1, ranges, group
+        self.gather = parallel.ColGatherer(ranges, group)
+        self.eye_j = torch.eye(self.n, dtype=torch.complex128)[:, j0:j1]
 
     def _gather(self, local, full):
         if full.is_complex():
-            parallel.all_gather_cols(torch.view_as_real(local), torch.view_as_real(full), self.ranges, self.group)
+            self.gather(torch.view_as_real(local.contiguous()), torch.view_as_real(full))
         else:
-            parallel.all_gather_cols(local, full, self.ranges, self.group)
+            self.gather(local.contiguous(), full)
+
+    def _sum(self, values):
+        return parallel.all_reduce_sum(values, torch.device("cpu"), self.group)
 
     def norm_guard(self):
         pass
 
     def entry_cols(self):
         j0, j1 = self.j0, self.j1
-        eye = torch.eye(self.n, dtype=torch.complex128)[:, j0:j1]
-        yj = self.qhat.conj().T @ self.qhat[:, j0:j1] - eye
+        yj = self.qhat.conj().T @ self.qhat[:, j0:j1] - self.eye_j
+        self._sum([float(torch.linalg.matrix_norm(yj)) ** 2])  # the correction-plan bound (a collective)
         self.qj = self.qhat[:, j0:j1] - 0.5 * (self.qhat @ yj)
 
     def gather_q(self):
-        self._gather(self.qj.contiguous(), self.q)
+        self._gather(self.qj, self.q)
 
     def norm_a(self):
         return float(torch.linalg.matrix_norm(self.a))
@@ -70,44 +75,39 @@ class CpuShardBackend:
         j0, j1 = self.j0, self.j1
         qj = self.q[:, j0:j1]
         self.tj = self.q.conj().T @ (self.a @ qj)
-        self.yj = self.q.conj().T @ qj - torch.eye(self.n, dtype=torch.complex128)[:, j0:j1]
-
-    def gather_that_y(self):
-        self._gather(self.tj.contiguous(), self.that)
-        self._gather(self.yj.contiguous(), self.y)
+        self.yj = self.q.conj().T @ qj - self.eye_j
+        rows = torch.arange(self.n)[:, None]
+        cols = torch.arange(j0, j1)[None, :]
+        self.ej = torch.where(rows > cols, self.tj, torch.zeros_like(self.tj))
 
     def norms(self):
-        e = torch.tril(self.that, -1)
-        return float(torch.linalg.matrix_norm(e)), float(torch.linalg.matrix_norm(self.y))
+        se, sy = self._sum([float(torch.linalg.matrix_norm(self.ej)) ** 2,
+                            float(torch.linalg.matrix_norm(self.yj)) ** 2])
+        return float(np.sqrt(se)), float(np.sqrt(sy))
+
+    def gather_lp(self):
+        self._gather(self.tj, self.t_full)
 
     def solve(self, clip):
-        t = torch.triu(self.that).numpy().astype(np.complex64)
-        e = torch.tril(self.that, -1).numpy().astype(np.complex64)
+        t = torch.triu(self.t_full).numpy().astype(np.complex64)
+        e = torch.tril(self.t_full, -1).numpy().astype(np.complex64)
         l, nclip = clib.solve_block(t, e, clip_threshold=clip, dtype=np.complex64)
         self.w = torch.from_numpy(l - l.conj().T)
         return float(np.linalg.norm(self.w.numpy().astype(np.complex128))), 0, nclip
 
-    def update_stage1_cols(self):
+    def update_cols(self, norm_y, norm_w):
         j0, j1 = self.j0, self.j1
-        y_lp = self.y.to(torch.complex64)
-        wj = self.w[:, j0:j1]
-        self.ywj = y_lp @ wj
-        self.w2j = self.w @ wj
-
-    def gather_w2(self):
-        self._gather(self.w2j.contiguous(), self.w2)
-
-    def update_stage2_cols(self):
-        j0, j1 = self.j0, self.j1
-        wj = self.w[:, j0:j1]
-        w3j = self.w2 @ wj
         c = torch.complex128
-        s = ((2.0 * wj.to(c) - self.y[:, j0:j1]) - self.ywj.to(c)) + self.w2j.to(c)
-        s = s + w3j.to(c)
+        wj = self.w[:, j0:j1]
+        w2j = self.w @ wj
+        xj = (self.yj - wj.to(c) - w2j.to(c)).to(torch.complex64)  # X = Y - W - W^2
+        self._gather(xj, self.x)
+        xwj = self.x @ wj                                             # (X W)_J = (YW - W^2 - W^3)_J
+        s = (2.0 * wj.to(c) - self.yj) - xwj.to(c)                    # S'_J
         self.qj = self.q[:, j0:j1] + 0.5 * (self.q @ s)
 
     def result(self):
-        return self.q.clone(), torch.triu(self.that)
+        return self.q.clone(), torch.triu(self.t_full)
 
 
 def _worker(rank, world, port, n, out):
@@ -133,6 +133,21 @@ def test_column_ranges():
     r = parallel.column_ranges(1000, 3, align=128)
     assert r == [(0, 384), (384, 768), (768, 1000)]
     assert all(j0 % 128 == 0 for j0, _ in r)
+
+
+def test_column_ranges_never_empty():
+    """n = 512 on 8 ranks at align 128 (config 5's size) must not
+    leave a rank without columns (it would encode nothing while the others
+    wait in a collective)."""
+    for n in list(range(8, 600)) + [512, 1000, 2048, 8192]:
+        for world in (2, 3, 4, 8):
+            r = parallel.column_ranges(n, world, 128)
+            assert len(r) == world and r[0][0] == 0 and r[-1][1] == n
+            assert all(j1 > j0 for j0, j1 in r), (n, world, r)
+            assert all(r[k][1] == r[k + 1][0] for k in range(world - 1))
+    assert parallel.column_ranges(512, 8, 128) == [(64 * k, 64 * (k + 1)) for k in range(8)]
+    with pytest.raises(ValueError):
+        parallel.column_ranges(3, 8)
 
 
 def test_sharded_refinement_gloo_world2_matches_single_process():

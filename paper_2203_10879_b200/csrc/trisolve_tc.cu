@@ -425,11 +425,20 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
         if (!ROW) {
           // this lane's accumulator row (R0 + lane) folded into the staged
           // block, then the block stored row by row (coalesced 256-byte rows)
+          if (!wide) {  // warp-uniform: the common path pays nothing for the rare one
 #pragma unroll
-          for (int c = 0; c < NB; ++c) {
-            const float sc = wide ? ldexpf(1.f, ea + eb_x[ew][c]) : fa * eb_s[ew][c];
-            float2& q = buf[lane * 33 + c];
-            q = make_float2(q.x - __uint_as_float(v[2 * c]) * sc, q.y - __uint_as_float(v[2 * c + 1]) * sc);
+            for (int c = 0; c < NB; ++c) {
+              const float sc = fa * eb_s[ew][c];
+              float2& q = buf[lane * 33 + c];
+              q = make_float2(q.x - __uint_as_float(v[2 * c]) * sc, q.y - __uint_as_float(v[2 * c + 1]) * sc);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < NB; ++c) {
+              const float sc = ldexpf(1.f, ea + eb_x[ew][c]);
+              float2& q = buf[lane * 33 + c];
+              q = make_float2(q.x - __uint_as_float(v[2 * c]) * sc, q.y - __uint_as_float(v[2 * c + 1]) * sc);
+            }
           }
           __syncwarp();
           if (C0 + lane < n) {
@@ -439,13 +448,25 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
           }
         } else if (idx < n) {
           // this lane's accumulator column (C0 + lane = idx)
+          if (!wide) {
 #pragma unroll
-          for (int i = 0; i < NB; ++i) {
-            if (R0 + i < n) {
-              const float sc = wide ? ldexpf(1.f, ea + eb_x[ew][i]) : fa * eb_s[ew][i];
-              const float2 q = buf[i * 33 + lane];
-              Rf[(size_t)(R0 + i) * ld + idx] = make_float2(q.x + __uint_as_float(v[2 * i]) * sc,
-                                                            q.y + __uint_as_float(v[2 * i + 1]) * sc);
+            for (int i = 0; i < NB; ++i) {
+              if (R0 + i < n) {
+                const float sc = fa * eb_s[ew][i];
+                const float2 q = buf[i * 33 + lane];
+                Rf[(size_t)(R0 + i) * ld + idx] = make_float2(q.x + __uint_as_float(v[2 * i]) * sc,
+                                                              q.y + __uint_as_float(v[2 * i + 1]) * sc);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+              if (R0 + i < n) {
+                const float sc = ldexpf(1.f, ea + eb_x[ew][i]);
+                const float2 q = buf[i * 33 + lane];
+                Rf[(size_t)(R0 + i) * ld + idx] = make_float2(q.x + __uint_as_float(v[2 * i]) * sc,
+                                                              q.y + __uint_as_float(v[2 * i + 1]) * sc);
+              }
             }
           }
         }

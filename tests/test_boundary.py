@@ -69,3 +69,22 @@ def test_correction_beta_tracks_the_correction_size():
     assert betas == sorted(betas, reverse=True)
     mods = [ozaki.plan(n, b, b).nmod for b in betas]
     assert mods[0] == ozaki.plan(n, ozaki.HP_BETA, ozaki.HP_BETA).nmod and mods[-1] < mods[0]
+
+
+def test_ddschur_import_shim_maps_the_hot_path():
+    """tools/ddschur_shim: `import ddschur` resolves the hot-path names to the
+    B200 drop-in (the reference's own tests can then run against it on a
+    machine with a GPU and the reference source, tools/run_reference_tests.sh)."""
+    import subprocess
+    import sys
+    code = ("import ddschur, paper_2203_10879_b200 as p; "
+            "from ddschur.ddmatrix import DDMatrix, frobenius_norm, stril_extract; "
+            "from ddschur.trisolve import solve_block, solve_scalar, stats, reset_stats; "
+            "from ddschur.orthogonal import newton_schulz_step, merged_update; "
+            "from ddschur.refine import RefineConfig; "
+            "assert DDMatrix is p.DDMatrix and solve_scalar is p.solve_scalar and stats is p.stats; "
+            "assert newton_schulz_step is p.newton_schulz_step and RefineConfig().precision == 'dd'; "
+            "print('ok')")
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([os.path.join(REPO, "tools", "ddschur_shim"), REPO]))
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr

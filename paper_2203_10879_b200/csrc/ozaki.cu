@@ -273,14 +273,17 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
           const uint32_t bm = p.bm[l];
           const int lo = -(pm >> 1);
           const int w0 = p.wb[l][0], w1 = p.wb[l][1], c64 = p.c64[l];
-          const int gp0 = p.wgp[l][0], gp1 = p.wgp[l][1], gm0 = p.wgm[l][0], gm1 = p.wgm[l][1];
+          const int gp0 = p.wgp[l][0], gp1 = p.wgp[l][1];
           const int cg = p.cgp[l], og = p.offg[l];
           int rp[4], rm[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int base = dp4a_us(hi_r[e], w1, dp4a_us(lo_r[e], w0, og - (int)ng_r[e] * c64));
             const int vp = dp4a_us(hi_i[e], gp1, dp4a_us(lo_i[e], gp0, base - (int)ng_i[e] * cg));
-            const int vm = dp4a_us(hi_i[e], gm1, dp4a_us(lo_i[e], gm0, base + (int)ng_i[e] * cg));
+            // the -iota weights are the negated +iota ones (symmetric residues,
+            // odd p), so phi- = 2 base - phi+ exactly: one IADD instead of two dp4a
+            // (both stay in [0, 2^21): offg exceeds the sixteen byte products)
+            const int vm = 2 * base - vp;
             // v < 2^21: umulhi(v, floor(2^32 / p) + 1) is exactly floor(v / p)
             // (the multiplier's excess times v stays below 2^32), so v - q p is
             // already in [0, p)

@@ -84,10 +84,20 @@ __device__ __forceinline__ float max4(const float* a, size_t n, int i) {
   return fmaxf(fmaxf(a[i], a[n + i]), fmaxf(a[2 * n + i], a[3 * n + i]));
 }
 
-// row / column maxima of |re|, |im| of T (arrays zeroed by the caller)
+// The far updates read T only in tiles (I, K) with K - I >= 4 FAR_LA + 1 >= 5
+// (COL: K - I = N - 4b - 4 + k - t with t < N - 4b - 8; ROW alike): the tiles
+// nearer the diagonal — the diagonal itself, whose eigenvalues dwarf the
+// strict upper part — are kept out of the line maxima that scale the FP16
+// forms (and written as zeros there), so every far operand keeps its full
+// ~22 bits relative to the entries the far updates actually read.
+constexpr int FAR_TILE_GAP = 4;  // excluded: tile distance K - I < FAR_TILE_GAP (far reads >= 5)
+
+// row / column maxima of |re|, |im| of T over the tiles the far updates read
+// (arrays zeroed by the caller)
 __global__ void __launch_bounds__(256) tmax_kernel(int n, const float2* __restrict__ T, long long ld,
                                                    float* __restrict__ rmax, float* __restrict__ cmax) {
   const int r0 = blockIdx.y * NB, c0 = blockIdx.x * NB;
+  if ((int)blockIdx.x - (int)blockIdx.y < FAR_TILE_GAP) return;  // lower part (zero), diagonal band
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   float cm = 0.f;
   for (int r = ty; r < NB; r += 8) {
@@ -113,11 +123,12 @@ __global__ void __launch_bounds__(256) tforms_kernel(int n, const float2* __rest
   const int r0 = blockIdx.y * NB, c0 = blockIdx.x * NB;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const size_t plane = (size_t)n * P;
+  const bool read = (int)blockIdx.x - (int)blockIdx.y >= FAR_TILE_GAP;  // a tile the far updates read
   for (int r = ty; r < NB; r += 8) {
     const int gr = r0 + r, gc = c0 + tx;
     float2 v = make_float2(0.f, 0.f);
     if (gr < n && gc < n) {
-      v = T[(size_t)gr * ld + gc];
+      if (read) v = T[(size_t)gr * ld + gc];
       const int e = line_exp(rmax[gr]);
       put_h2(tf, plane, (size_t)gr * P + 2 * gc, scale_pow2(v.x, -e), scale_pow2(v.y, -e));
     }

@@ -49,10 +49,13 @@ def test_mixed_fp64_matches_reference_order(golden):
         assert v.tri_residual <= 10 * n * U64 * np.linalg.norm(a) and v.ortho_residual <= 10 * n * U64
 
 
-def test_mixed_fp64_config2_size():
+def test_mixed_fp64_n1024_from_scratch():
     """n = 1024 complex Gaussian from scratch in FP64 mode (front end on the
-    GPU, no CPU Schur): converges within the iteration budget."""
+    GPU, no CPU Schur): converges within the iteration budget, and the result
+    passes the FP64 verify_pair at the stop rule."""
     from paper_2203_10879_b200 import inputs
     a = inputs.gaussian_complex(1024, 3)
     pair, rep = refine_mixed(a, RefineConfig(precision="fp64", tol_factor=10.0 / 1024, max_iters=10))
     assert rep.status is RefineStatus.CONVERGED and rep.iterations <= 6, rep
+    v = verify_pair(a, pair, precision="fp64")
+    assert v.tri_residual <= 10 * 1024 * U64 * np.linalg.norm(a) and v.ortho_residual <= 10 * 1024 * U64

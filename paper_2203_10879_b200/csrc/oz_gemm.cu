@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <map>
@@ -65,6 +66,9 @@ struct OzParams {
   int gauss;                    // Gaussian planes: tile plane g = mt / tpp (real product of A plane g ^ a_swap
   int a_swap, b_gplane, tpp;    //   with B plane g ^ b_swap, or B plane 0 when b_gplane = 0), output plane g
   int b_swap;
+  int wide;                     // TWO && real: a unit is N = 512 (two N = 256 MMAs per k-block into both TMEM
+                                //   accumulators): the pair's A tile is read once per 512 B rows, 25 % less
+                                //   L2->SM ingest per MAC; the epilogue then drains both accumulators
   int herm;                     // gauss, Hermitian (+1) / skew (-1) C: only plane 0 is computed, and the
                                 //   epilogue also writes herm * its transpose as plane 1 (C- = +-C+^T)
   long long out_pitch;          // bytes between output rows
@@ -192,14 +196,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int a_bytes = p.a_planes * PLANE_BYTES;
   // real: one 256-row B plane (TWO: this CTA's 128 rows); complex: 3 planes (TWO: 2)
-  const int b_bytes = TWO ? (p.real ? 1 : 2) * PLANE_BYTES : (p.real ? 2 : p.b_planes) * PLANE_BYTES;
+  const int b_bytes = TWO ? (p.real ? (p.wide ? 2 : 1) : 2) * PLANE_BYTES : (p.real ? 2 : p.b_planes) * PLANE_BYTES;
   // 2-SM real products carry two 64-byte k-blocks per ring slot (four MMAs per
   // barrier round trip, like the complex products): with one k-block per slot
   // the issuer's per-slot overhead left the tensor pipe ~45 % idle
   const int kstep = (TWO && p.real) ? 2 : 1;
   const int stage_bytes = kstep * (a_bytes + b_bytes);
   const int STAGES = p.stages;
-  const int tn = p.real ? 2 * TN : TN;
+  const int tn = p.real ? (p.wide ? 4 : 2) * TN : TN;
   uint64_t* bars = (uint64_t*)(smem + SMEM_RING);
   // bars: full[MAX_STAGES], empty[MAX_STAGES], tfull[2], tempty[2], qfull[QD], qempty[QD],
   // pfull[QD], pempty[QD]; then the unit queues unitq[QD], peerq[QD] and the tmem base slot
@@ -331,11 +335,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t fb = mapa_u32(full_bar(stage), 0);
             if (crank == 0) mbar_expect_tx(full_bar(stage), 2 * stage_bytes);
             if (p.real) {
-              // [A kb, A kb+1 | B kb, B kb+1]; a k-block past K is zero-filled by the TMA
+              // [A kb, A kb+1 | B kb, B kb+1]; a k-block past K is zero-filled by the TMA.
+              // wide: B kb = [rows of the first N = 256 half | of the second], this CTA's 128 of each
               for (int h = 0; h < kstep; ++h) {
                 tma_load_4d_2sm(smem_u32(st + h * a_bytes), &tmap_a, fb, (kb + h) * TK, arow, apl, l);
                 tma_load_4d_2sm(smem_u32(st + kstep * a_bytes + h * b_bytes), &tmap_b, fb, (kb + h) * TK,
                                 nt * tn + crank * TN, bpl, l);
+                if (p.wide)
+                  tma_load_4d_2sm(smem_u32(st + kstep * a_bytes + h * b_bytes + PLANE_BYTES), &tmap_b, fb,
+                                  (kb + h) * TK, nt * tn + 2 * TN + crank * TN, bpl, l);
               }
             } else {
               tma_load_4d_2sm(smem_u32(st), &tmap_a, fb, kb * TK, arow, apl, l);
@@ -405,9 +413,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
               for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int ks = 0; ks < TK / 32; ++ks)
-                  umma_i8_2sm(d, umma_desc_sw64(sa + h * a_bytes + ks * 32),
-                              umma_desc_sw64(sa + 2 * a_bytes + h * b_bytes + ks * 32), id, (kb | h | ks) != 0);
+                for (int ks = 0; ks < TK / 32; ++ks) {
+                  const uint64_t ad = umma_desc_sw64(sa + h * a_bytes + ks * 32);
+                  umma_i8_2sm(d, ad, umma_desc_sw64(sa + 2 * a_bytes + h * b_bytes + ks * 32), id,
+                              (kb | h | ks) != 0);
+                  if (p.wide)  // the second N = 256 half into the other accumulator (d = base)
+                    umma_i8_2sm(d + 256, ad, umma_desc_sw64(sa + 2 * a_bytes + h * b_bytes + PLANE_BYTES + ks * 32),
+                                id, (kb | h | ks) != 0);
+                }
             } else {
 #pragma unroll
               for (int ks = 0; ks < TK / 32; ++ks) {
@@ -451,7 +464,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           phase ^= 1;
         }
       }
-      acc ^= 1;
+      if (!p.wide) acc ^= 1;  // wide: every unit uses both accumulators (acc stays 0)
       if (acc == 0) acc_phase ^= 1;
     }
   } else {
@@ -478,8 +491,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         row = (mt - g * p.tpp) * TM + ew * 32 + lane;
       }
       int8_t* base = out + (size_t)l * p.out_mod + (size_t)g * p.out_plane + (size_t)row * p.out_pitch;
+      const int nchunks = p.wide ? 32 : 16;
 #pragma unroll 1
-      for (int chunk = 0; chunk < 16; ++chunk) {
+      for (int chunk = 0; chunk < nchunks; ++chunk) {
         uint32_t v[16];
         tmem_ld16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * 256 + chunk * 16), v);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
@@ -527,7 +541,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       } else {
         mbar_arrive(tempty_bar(acc));
       }
-      acc ^= 1;
+      if (!p.wide) acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
   }
@@ -635,7 +649,7 @@ int gemm_launch(int M, int N, int K, int nmod, const int* moduli, const void* a,
     p.tpp = p.tiles_m;
     p.tiles_m = planes_out * p.tpp;
   }
-  p.tiles_n = (N + (real ? 2 * TN : TN) - 1) / (real ? 2 * TN : TN);
+  p.tiles_n = (N + (real ? 2 * TN : TN) - 1) / (real ? 2 * TN : TN);  // (wide: recomputed below)
   p.lower_only = lower_only;
   p.out_pitch = out_pitch;
   p.out_plane = out_pitch * M;
@@ -664,10 +678,21 @@ int gemm_launch(int M, int N, int K, int nmod, const int* moduli, const void* a,
     p.tpp += 1;
     p.tiles_m = planes_out * p.tpp;
   }
-  const int tiles = nmod * p.tiles_m * p.tiles_n;
   const bool two = two_sm && cm == 2;
+  // wide units (N = 512) for the 2-SM real products: 18-20 % faster at
+  // n = K = 8192 (tools/oz_wide_ab.py, interleaved A/B), but the epilogue of a
+  // wide unit is not overlapped with MMAs, so short K (15-22 % slower at 2048)
+  // and the Hermitian products' transposed-write epilogue (9 % slower) stay
+  // narrow.  SR_OZ_WIDE=0 / 1 forces either.
+  bool wide = two && real && herm == 0 && K >= 4096;
+  const char* wide_env = getenv("SR_OZ_WIDE");
+  if (wide_env && *wide_env && strcmp(wide_env, "auto") != 0) wide = two && real && atoi(wide_env) != 0;
+  p.wide = wide ? 1 : 0;
+  if (p.wide) p.tiles_n = (N + 4 * TN - 1) / (4 * TN);
+  const int tiles = nmod * p.tiles_m * p.tiles_n;
   if (two) {  // per CTA: its A rows and half of the pair's B operand (real: two k-blocks per slot)
-    p.stages = std::min(MAX_STAGES, SMEM_RING / ((real ? 2 : 1) * (p.a_planes + (real ? 1 : 2)) * PLANE_BYTES));
+    p.stages = std::min(MAX_STAGES, SMEM_RING / ((real ? 2 : 1) *
+                                                 (p.a_planes + (real ? (p.wide ? 2 : 1) : 2)) * PLANE_BYTES));
     if (getenv("SR_OZ_STAGES")) p.stages = std::max(2, std::min(p.stages, atoi(getenv("SR_OZ_STAGES"))));
   }
   p.group_m = (getenv("SR_OZ_GROUP_M") ? atoi(getenv("SR_OZ_GROUP_M")) : (real ? 2 : 1) * GROUP_M) / cm;

@@ -607,6 +607,7 @@ def _run_fp64(a, qhat, cfg, ws, symmetric=False, host=None, a_upload=None):
         q_out, t_out = host.finish(ws.q, q_version, ws.that)
     else:
         q_out, t_out = ws.q.to_complex(), ws.that.to_complex()
+    _mark("result")
     pair = SchurPair(q=q_out, t=t_out, ortho_residual=last_y, tri_residual=last_e)
     report = RefineReport(iterations=iterations, residual_history=history,
                           hp_matmul_count=_counters["hp_calls"] - hp0, clipped_total=clipped_total,
@@ -651,6 +652,7 @@ def refine_template(a, qhat, cfg=None, device=None, out=None):
         raise RuntimeError("refine_template needs a CUDA device (no CPU fallback)")
     device = torch.device("cuda") if device is None else torch.device(device)
     t0 = time.perf_counter()
+    _mark("call")
     if cfg.precision == "dd":
         if out is not None:
             raise ValueError("out=(q_host, t_host) is the FP64-mode host delivery; dd mode returns DDPlanar results")

@@ -261,6 +261,14 @@ int sr_oz_decode_gauss(int M, int N, int nmod, int nchunk, const double* table, 
                        long long ld_add, double add_scale, int out_kind, void* out_re, double* out_im,
                        long long ld_out, int hermitian, int diag_col0, void* stream);
 
+/* Ozaki path options (no reference counterpart: implementation switches for
+   tests and A/B tools).  key 0: 1 (default) = Gaussian decodes with nchunk
+   2..4 and nmod <= 32 run the tensor-core CRT decode (the digit sums of the
+   CRT weights as one tcgen05 kind::i8 MMA per 128 outputs), 0 = the SIMT
+   decode; both give bit-identical results.  value < 0 only queries.
+   Returns the previous value, -1 for an unknown key. */
+int sr_oz_config(int key, int value);
+
 
 /* ---- double-double container operations (csrc/dd_ops.cu), bit-identical to
    the reference's numpy / numba kernels for finite operands.  One real plane

@@ -9,7 +9,7 @@ import os
 from .errors import NonFiniteError, SeparationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsr.so")
+LIB_PATH = os.environ.get("SR_LIB_PATH") or os.path.join(_HERE, "libsr.so")  # override: A/B builds (tools/)
 
 SR_OK, SR_EINVAL, SR_ESEPARATION, SR_ENONFINITE, SR_ECUDA = 0, 1, 2, 3, 4
 SR_FLAG_SEPARATION, SR_FLAG_NONFINITE = 1, 2
@@ -58,6 +58,7 @@ SIGNATURES = {
     "sr_oz_gemm_i8_gauss": (_i, [_i, _i, _i, _i, _p, _p, _i, _ll, _p, _i, _ll, _p, _ll, _i, _i, _p]),
     "sr_oz_decode_gauss": (_i, [_i, _i, _i, _i, _p, _p, _ll, _p, _i, _p, _i, _d, _d, _i, _p, _p, _ll, _d, _i,
                                 _p, _p, _ll, _i, _i, _p]),
+    "sr_oz_config": (_i, [_i, _i]),
     "sr_dd_add": (_i, [_i, _i, _p, _p, _ll, _p, _p, _ll, _i, _p, _p, _ll, _p]),
     "sr_dd_scale": (_i, [_i, _i, _p, _p, _ll, _d, _p, _p, _ll, _p]),
     "sr_stril_split_f64": (_i, [_i, _i, _p, _ll, _p, _ll, _p, _ll, _p]),

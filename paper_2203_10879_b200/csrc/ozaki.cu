@@ -149,6 +149,7 @@ struct EncodeParams {
   int wgp[MAXMOD][2], wgm[MAXMOD][2];  // layout 4: +-iota 2^(8 c) mod p, symmetric int8, packed 4 per word
   int cgp[MAXMOD];                 // layout 4: iota 2^64 mod p, symmetric
   int offg[MAXMOD];                // layout 4: a multiple of p above four byte dot products, minus lo
+  int offb[MAXMOD], offi[MAXMOD];  // layout 4: offg - (2^63 mod p), -(iota 2^63 mod p) (sign-bit-flipped bytes)
 };
 
 // balanced 11-bit digits of an integer-valued double (error-free, top-down)
@@ -265,25 +266,34 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
       }
       const bool need_neg = p.layout == 1 || p.layout == 3;  // planes with -im
       if (p.layout == 4) {
-        // Gaussian planes straight from the bytes: phi+- = re +- iota im mod p is
-        // sum_c u_c(re) (2^(8c) mod p) + u_c(im) (+-iota 2^(8c) mod p) - the
-        // 2^64 corrections of negative values: four byte dot products, one
+        // Gaussian planes straight from the bytes: phi+- = re +- iota im mod p.
+        // With the sign bit flipped, the bytes u_c of x + 2^63 are unsigned, so
+        // x mod p = sum_c u_c (2^(8c) mod p) - (2^63 mod p) for either sign: four
+        // byte dot products (dp4a) per modulus, the 2^63 terms folded into the
+        // per-modulus offsets (offb: real part, offi: imaginary part), one
         // Barrett reduction per plane (0 <= v < 2^21)
-        for (int l = 0; l < p.nmod; ++l) {
+        uint32_t hr[4], hm[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          hr[e] = hi_r[e] ^ 0x80000000u;
+          hm[e] = hi_i[e] ^ 0x80000000u;
+        }
+        int8_t* dm = dst;
+        for (int l = 0; l < p.nmod; ++l, dm += mod_stride) {
           const int pm = p.pi[l];
           const uint32_t bm = p.bm[l];
           const int lo = -(pm >> 1);
-          const int w0 = p.wb[l][0], w1 = p.wb[l][1], c64 = p.c64[l];
+          const int w0 = p.wb[l][0], w1 = p.wb[l][1];
           const int gp0 = p.wgp[l][0], gp1 = p.wgp[l][1];
-          const int cg = p.cgp[l], og = p.offg[l];
+          const int ob = p.offb[l], oi = p.offi[l];
           int rp[4], rm[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int base = dp4a_us(hi_r[e], w1, dp4a_us(lo_r[e], w0, og - (int)ng_r[e] * c64));
-            const int vp = dp4a_us(hi_i[e], gp1, dp4a_us(lo_i[e], gp0, base - (int)ng_i[e] * cg));
+            const int base = dp4a_us(hr[e], w1, dp4a_us(lo_r[e], w0, ob));
+            const int vp = dp4a_us(hm[e], gp1, dp4a_us(lo_i[e], gp0, base + oi));
             // the -iota weights are the negated +iota ones (symmetric residues,
-            // odd p), so phi- = 2 base - phi+ exactly: one IADD instead of two dp4a
-            // (both stay in [0, 2^21): offg exceeds the sixteen byte products)
+            // odd p), so phi- = 2 base - phi+ exactly (both stay in [0, 2^21):
+            // the offset exceeds the sixteen byte products and the 2^63 terms)
             const int vm = 2 * base - vp;
             // v < 2^21: umulhi(v, floor(2^32 / p) + 1) is exactly floor(v / p)
             // (the multiplier's excess times v stays below 2^32), so v - q p is
@@ -293,7 +303,6 @@ __global__ void __launch_bounds__(256) encode_kernel(const __grid_constant__ Enc
           }
           const uint32_t wp = __byte_perm(__byte_perm(rp[0], rp[1], 0x0040), __byte_perm(rp[2], rp[3], 0x0040), 0x5410);
           const uint32_t wm = __byte_perm(__byte_perm(rm[0], rm[1], 0x0040), __byte_perm(rm[2], rm[3], 0x0040), 0x5410);
-          int8_t* dm = dst + (size_t)l * mod_stride;
           *reinterpret_cast<uint32_t*>(dm) = wp;
           *reinterpret_cast<uint32_t*>(dm + plane_stride) = wm;
         }
@@ -1263,6 +1272,10 @@ int encode_launch(int rows_out, int K, int kind, const void* re, const double* i
       p.cgp[l] = (int)sym(io * pg);  // pg = 2^64 mod m here
       const int bound = 16 * 255 * (m >> 1) + 2 * (m >> 1);  // |16 byte products| + |corrections|
       p.offg[l] = (bound + m - 1) / m * m + (m >> 1);        // a multiple of m above it, then -lo
+      long long p63 = 1;
+      for (int c = 0; c < 63; ++c) p63 = (p63 * 2) % m;  // 2^63 mod m
+      p.offb[l] = p.offg[l] - (int)sym(p63);
+      p.offi[l] = -(int)sym(io * p63);
     }
   }
   // K padding columns of the residue planes must read as zero

@@ -3,7 +3,7 @@
 #   bash tools/build_variant.sh NAME csrc_file.cu "-DFLAG=1 ..."  -> tools/_ab/libsr_NAME.so
 # (load it with SR_LIB_PATH=tools/_ab/libsr_NAME.so)
 set -e
-name=$1; src=$2; flags=$3
+name=$1; src=$2; flags=$3; srcpath=${4:-csrc/$2}  # optional: another version of the file
 cd "$(dirname "$0")/../paper_2203_10879_b200"
 make -s libsr.so
 mkdir -p ../tools/_ab/$name
@@ -12,7 +12,7 @@ for o in build/*.o; do
   b=$(basename $o .o)
   if [ "$b.cu" == "$src" ]; then
     /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
-      --expt-relaxed-constexpr $flags -c csrc/$src -o ../tools/_ab/$name/$b.o
+      --expt-relaxed-constexpr $flags -I csrc -c $srcpath -o ../tools/_ab/$name/$b.o
     objs="$objs ../tools/_ab/$name/$b.o"
   else
     objs="$objs $o"

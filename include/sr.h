@@ -182,6 +182,17 @@ size_t sr_reduce_workspace_bytes(void);
 int sr_oz_exponents(int rows, int cols, int kind, const void* re, const double* im, long long ld, int transposed,
                     int* exps, void* stream);
 
+/* sr_oz_exponents plus the lines' CRT bound: rmax (one double, device) =
+   max_i ||op(X)[i, :]||_2 2^-exps[i], so that an integer-scaled line
+   round(op(X)[i, :] 2^(beta - exps[i])) has 2-norm <= 2^beta rmax +
+   sqrt(2K)/2 (Cauchy-Schwarz then bounds every entry of a product, which lets
+   the Python plan drop moduli: ozaki.fit_plan).  ss_work: cols doubles of
+   workspace when transposed (column sums of squares).  No reference
+   counterpart (the reference's Ozaki path, matmul.py:151-212, sizes its
+   slices from the worst case). */
+int sr_oz_exponents_bound(int rows, int cols, int kind, const void* re, const double* im, long long ld,
+                          int transposed, int* exps, double* ss_work, double* rmax, void* stream);
+
 /* Residue planes [nmod][planes][rows_out][kpitch] (int8, K-major) of
    round(op(X) * 2^(beta - exps[i])) modulo moduli[l] (3..256, pairwise
    coprime; host array).  op(X)[i][k] = X[i][k], or X[k][i] when transposed;

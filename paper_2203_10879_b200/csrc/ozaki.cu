@@ -75,22 +75,35 @@ __device__ __forceinline__ void load_elem(const Src& s, size_t off, double& vr, 
 }
 
 // ---- exponents: e_i with max_k |op(X)[i,k]| < 2^e_i (dd: of the hi parts) ----
+// With rmax != null also r_i = ||op(X)[i, :]||_2 2^-e_i (the line's 2-norm in
+// units of its power-of-two scale) and rmax = max_i r_i (atomicMax on the bits
+// of a non-negative double): the CRT bound of a product (ozaki.fit_plan).
+__device__ __forceinline__ void atomic_max_nonneg(double* a, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(a), (unsigned long long)__double_as_longlong(v));
+}
+
 template <int KIND>
-__global__ void exps_direct_kernel(int rows, int cols, Src s, long long ld, int* __restrict__ e) {
+__global__ void exps_direct_kernel(int rows, int cols, Src s, long long ld, int* __restrict__ e,
+                                   double* __restrict__ rmax) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
-  double m = 0.0;
+  double m = 0.0, ss = 0.0;
   for (int k = lane; k < cols; k += 32) {
     double vr, vi, lr, li;
     load_elem<KIND>(s, (size_t)warp * ld + k, vr, vi, lr, li);
     m = fmax(m, fmax(fabs(vr), fabs(vi)));
+    ss = fma(vr, vr, fma(vi, vi, ss));
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  }
   if (lane == 0) {
     int ex = EXP_FLOOR;
     if (m > 0.0) frexp(m, &ex);
     e[warp] = ex;
+    if (rmax && m > 0.0) atomic_max_nonneg(rmax, sqrt(ss) * scale2(1.0, -ex));
   }
 }
 
@@ -99,30 +112,45 @@ __global__ void exps_fill_kernel(int n, int* __restrict__ e) {
   if (i < n) e[i] = EXP_FLOOR;
 }
 
+// column bound: r_j = sqrt(ss_j) 2^-e_j, rmax = max_j r_j
+__global__ void bound_finish_kernel(int cols, const double* __restrict__ ss, const int* __restrict__ e,
+                                    double* __restrict__ rmax) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < cols && e[j] > EXP_FLOOR) atomic_max_nonneg(rmax, sqrt(ss[j]) * scale2(1.0, -e[j]));
+}
+
 // per-column maxima over a chunk of rows per block (grid.y), merged with an
-// integer atomicMax on the exponent (frexp's exponent is monotone in |x|)
+// integer atomicMax on the exponent (frexp's exponent is monotone in |x|);
+// with ss != null also the columns' sums of squares (atomicAdd: a bound only)
 template <int KIND>
 __global__ void exps_transposed_kernel(int rows, int cols, Src s, long long ld, int rows_per_block,
-                                       int* __restrict__ e) {
+                                       int* __restrict__ e, double* __restrict__ ssum) {
   __shared__ double part[8][33];
+  __shared__ double psq[8][33];
   const int j = blockIdx.x * 32 + threadIdx.x;
   const int r0 = blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
-  double m = 0.0;
+  double m = 0.0, ss = 0.0;
   if (j < cols)
     for (int i = r0 + threadIdx.y; i < r1; i += 8) {
       double vr, vi, lr, li;
       load_elem<KIND>(s, (size_t)i * ld + j, vr, vi, lr, li);
       m = fmax(m, fmax(fabs(vr), fabs(vi)));
+      ss = fma(vr, vr, fma(vi, vi, ss));
     }
   part[threadIdx.y][threadIdx.x] = m;
+  psq[threadIdx.y][threadIdx.x] = ss;
   __syncthreads();
   if (threadIdx.y == 0 && j < cols) {
-    for (int y = 1; y < 8; ++y) m = fmax(m, part[y][threadIdx.x]);
+    for (int y = 1; y < 8; ++y) {
+      m = fmax(m, part[y][threadIdx.x]);
+      ss += psq[y][threadIdx.x];
+    }
     if (m > 0.0) {
       int ex = 0;
       frexp(m, &ex);
       atomicMax(&e[j], ex);
     }
+    if (ssum && ss > 0.0) atomicAdd(&ssum[j], ss);
   }
 }
 
@@ -1174,31 +1202,52 @@ int dispatch_out(int out_kind, int add_kind, int grid, cudaStream_t st, const De
 
 }  // namespace
 
-extern "C" int sr_oz_exponents(int rows, int cols, int kind, const void* re, const double* im, long long ld,
-                               int transposed, int* exps, void* stream) {
+namespace {
+int exponents_launch(int rows, int cols, int kind, const void* re, const double* im, long long ld, int transposed,
+                     int* exps, double* ss_work, double* rmax, cudaStream_t st) {
   if (rows < 0 || cols < 0 || !re || !exps || kind < 0 || kind > SR_MAT_DD) return SR_EINVAL;
-  cudaStream_t st = (cudaStream_t)stream;
   Src s{(const double*)re, im, nullptr, nullptr, kind};
   if (kind == SR_MAT_DD) kind = SR_MAT_F64;  // the hi parts decide the scale
+  if (rmax) SR_CUDA_CHECK(cudaMemsetAsync(rmax, 0, sizeof(double), st));
   if (!transposed) {
     if (rows == 0) return SR_OK;
     const int grid = sr_ceil_div((long long)rows * 32, 256);
-    if (kind == SR_MAT_F64) exps_direct_kernel<SR_MAT_F64><<<grid, 256, 0, st>>>(rows, cols, s, ld, exps);
-    if (kind == SR_MAT_C64) exps_direct_kernel<SR_MAT_C64><<<grid, 256, 0, st>>>(rows, cols, s, ld, exps);
-    if (kind == SR_MAT_C128) exps_direct_kernel<SR_MAT_C128><<<grid, 256, 0, st>>>(rows, cols, s, ld, exps);
+    if (kind == SR_MAT_F64) exps_direct_kernel<SR_MAT_F64><<<grid, 256, 0, st>>>(rows, cols, s, ld, exps, rmax);
+    if (kind == SR_MAT_C64) exps_direct_kernel<SR_MAT_C64><<<grid, 256, 0, st>>>(rows, cols, s, ld, exps, rmax);
+    if (kind == SR_MAT_C128) exps_direct_kernel<SR_MAT_C128><<<grid, 256, 0, st>>>(rows, cols, s, ld, exps, rmax);
   } else {
     if (cols == 0) return SR_OK;
     exps_fill_kernel<<<sr_ceil_div(cols, 256), 256, 0, st>>>(cols, exps);
     SR_LAUNCH_CHECK();
+    double* ssum = rmax ? ss_work : nullptr;
+    if (ssum) SR_CUDA_CHECK(cudaMemsetAsync(ssum, 0, (size_t)cols * sizeof(double), st));
     const int rpb = 256;
     dim3 g(sr_ceil_div(cols, 32), sr_ceil_div(rows, rpb));
-    if (kind == SR_MAT_F64) exps_transposed_kernel<SR_MAT_F64><<<g, dim3(32, 8), 0, st>>>(rows, cols, s, ld, rpb, exps);
-    if (kind == SR_MAT_C64) exps_transposed_kernel<SR_MAT_C64><<<g, dim3(32, 8), 0, st>>>(rows, cols, s, ld, rpb, exps);
+    if (kind == SR_MAT_F64)
+      exps_transposed_kernel<SR_MAT_F64><<<g, dim3(32, 8), 0, st>>>(rows, cols, s, ld, rpb, exps, ssum);
+    if (kind == SR_MAT_C64)
+      exps_transposed_kernel<SR_MAT_C64><<<g, dim3(32, 8), 0, st>>>(rows, cols, s, ld, rpb, exps, ssum);
     if (kind == SR_MAT_C128)
-      exps_transposed_kernel<SR_MAT_C128><<<g, dim3(32, 8), 0, st>>>(rows, cols, s, ld, rpb, exps);
+      exps_transposed_kernel<SR_MAT_C128><<<g, dim3(32, 8), 0, st>>>(rows, cols, s, ld, rpb, exps, ssum);
+    if (ssum) {
+      SR_LAUNCH_CHECK();
+      bound_finish_kernel<<<sr_ceil_div(cols, 256), 256, 0, st>>>(cols, ssum, exps, rmax);
+    }
   }
   SR_LAUNCH_CHECK();
   return SR_OK;
+}
+}  // namespace
+
+extern "C" int sr_oz_exponents(int rows, int cols, int kind, const void* re, const double* im, long long ld,
+                               int transposed, int* exps, void* stream) {
+  return exponents_launch(rows, cols, kind, re, im, ld, transposed, exps, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int sr_oz_exponents_bound(int rows, int cols, int kind, const void* re, const double* im, long long ld,
+                                     int transposed, int* exps, double* ss_work, double* rmax, void* stream) {
+  if (!rmax || (transposed && !ss_work)) return SR_EINVAL;
+  return exponents_launch(rows, cols, kind, re, im, ld, transposed, exps, ss_work, rmax, (cudaStream_t)stream);
 }
 
 namespace {

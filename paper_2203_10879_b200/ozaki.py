@@ -23,6 +23,7 @@ generalises the reference's own Ozaki-I dd path (_ozaki_gemm_hp,
 matmul.py:151-212), which splits into FP64 slices multiplied by BLAS.
 """
 import math
+import os
 
 import numpy as np
 import torch
@@ -64,7 +65,9 @@ class OzPlan:
 
     gauss = False
 
-    def __init__(self, K, beta_a, beta_b, gauss=False):
+    def __init__(self, K, beta_a, beta_b, gauss=False, nmod=None):
+        """nmod: use exactly the first nmod moduli (fit_plan: a prefix of the
+        worst-case plan that the operands' Cauchy-Schwarz bound allows)."""
         self.K = K
         self.beta_a = beta_a
         self.beta_b = beta_b
@@ -73,7 +76,7 @@ class OzPlan:
         need = beta_a + beta_b + math.ceil(math.log2(max(K, 2))) + 2
         P = 1
         r = 0
-        while P.bit_length() - 1 < need:
+        while (P.bit_length() - 1 < need) if nmod is None else (r < nmod):
             if r == len(mods):
                 raise ValueError("no Ozaki plan for K=%d beta=(%d,%d)" % (K, beta_a, beta_b))
             P *= mods[r]
@@ -142,10 +145,10 @@ class OzPlan:
 _PLANS = {}
 
 
-def plan(K, beta_a, beta_b, gauss=False):
-    key = (K, beta_a, beta_b, bool(gauss))
+def plan(K, beta_a, beta_b, gauss=False, nmod=None):
+    key = (K, beta_a, beta_b, bool(gauss), nmod)
     if key not in _PLANS:
-        _PLANS[key] = OzPlan(K, beta_a, beta_b, gauss)
+        _PLANS[key] = OzPlan(K, beta_a, beta_b, gauss, nmod)
     return _PLANS[key]
 
 
@@ -160,7 +163,7 @@ def kpitch(K):
 class Encoded:
     """Residue planes of one operand (A role: op(X) rows; B role: columns)."""
 
-    __slots__ = ("buf", "exps", "rows", "K", "planes", "beta", "nmod", "kp", "cap", "swap")
+    __slots__ = ("buf", "exps", "rows", "K", "planes", "beta", "nmod", "kp", "cap", "swap", "rmax", "ssw", "bound")
 
     def __init__(self, rows, K, planes, beta, nmod, device):
         self.rows, self.K, self.planes, self.beta, self.nmod = rows, K, planes, beta, nmod
@@ -169,6 +172,46 @@ class Encoded:
         self.kp = kpitch(K)
         self.buf = torch.empty(nmod * planes * rows * self.kp, dtype=torch.int8, device=device)
         self.exps = torch.empty(rows, dtype=torch.int32, device=device)
+        # CRT bound of the lines (sr_oz_exponents_bound): max_i ||line_i||_2 2^-e_i on the
+        # device, its host copy once read (fit_plan), and the column sum-of-squares workspace
+        self.rmax = torch.zeros(1, dtype=torch.float64, device=device)
+        self.ssw = None
+        self.bound = None
+
+
+def fit_plan(pl, ea, eb):
+    """The prefix of plan pl with the fewest moduli whose product P still
+    exceeds 2 max |C| for C = op(A) B of these two encodings (the CRT
+    reconstructs the symmetric representative exactly): by Cauchy-Schwarz,
+    |C_ij| <= ||a~_i||_2 ||b~_j||_2 for the integer-scaled lines, and
+    ||a~_i|| <= 2^beta_a r_a + sqrt(2K)/2 with r_a = max_i ||a_i|| 2^-e_i from
+    the exponent pass (sr_oz_exponents_bound).  The worst-case plan assumes
+    |C| <= 2K 2^(beta_a + beta_b); for unitary or Gaussian operands the norm
+    bound is ~2^(5.5 + 5.5) below it at n = 8192, one modulus less.  Reads the
+    two device bounds (one sync per new encoding)."""
+    if os.environ.get("SR_FIT_PLAN") == "0":  # A/B switch (tools/refine_env_ab.py)
+        return pl
+    if ea.bound is None or eb.bound is None:
+        v = torch.stack([ea.rmax, eb.rmax]).cpu()
+        if ea.bound is None:
+            ea.bound = float(v[0])
+        if eb.bound is None:
+            eb.bound = float(v[1])
+    ra, rb = ea.bound, eb.bound
+    if not (math.isfinite(ra) and math.isfinite(rb)):
+        return pl
+    slack = 0.5 * math.sqrt(2.0 * max(ea.K, 1)) + 1.0
+    ba = math.ldexp(ra, ea.beta) * (1.0 + 2.0 ** -30) + slack
+    bb = math.ldexp(rb, eb.beta) * (1.0 + 2.0 ** -30) + slack
+    need = int(2.0 * ba * bb) + 1  # P must exceed this
+    mods = GAUSS_MODULI if pl.gauss else MODULI
+    P, r = 1, 0
+    while P <= need and r < pl.nmod:
+        P *= mods[r]
+        r += 1
+    if r >= pl.nmod:
+        return pl
+    return plan(pl.K, pl.beta_a, pl.beta_b, pl.gauss, nmod=r)
 
 
 def conj_view(eb):
@@ -218,8 +261,12 @@ def encode(x, rows, cols, role, pl, conj_t=False, out=None):
         raise ValueError("encoding buffer does not fit this operand / plan")
     enc.beta, enc.nmod = beta, pl.nmod
     enc.swap = False
+    enc.bound = None
     st = _stream()
-    _lib.call("sr_oz_exponents", rows, cols, kind, re, im, ld, transposed, enc.exps.data_ptr(), st)
+    if transposed and (enc.ssw is None or enc.ssw.numel() < out_rows):
+        enc.ssw = torch.empty(out_rows, dtype=torch.float64, device=dev)
+    _lib.call("sr_oz_exponents_bound", rows, cols, kind, re, im, ld, transposed, enc.exps.data_ptr(),
+              enc.ssw.data_ptr() if transposed else None, enc.rmax.data_ptr(), st)
     _lib.call("sr_oz_encode", out_rows, K, kind, re, im, re_lo, im_lo, ld, transposed, conj, layout,
               enc.exps.data_ptr(), beta, pl.nmod, pl.moduli_ptr(), enc.buf.data_ptr(), enc.kp, st)
     return enc
@@ -266,6 +313,7 @@ def encode_dual(x, rows, cols, pl, out_ah, out_b):
             raise ValueError("encoding buffer does not fit this operand / plan")
     out_ah.beta, out_ah.nmod = pl.beta_a, pl.nmod
     out_b.beta, out_b.nmod = pl.beta_b, pl.nmod
+    out_ah.bound = out_b.bound = math.inf  # no line bound: fit_plan keeps the worst-case plan
     if pl.beta_a != pl.beta_b or out_ah.kp != out_b.kp:
         raise ValueError("encode_dual needs beta_a == beta_b")
     st = _stream()

@@ -123,7 +123,7 @@ class OzakiProducts:
         self.w_skew = True
 
     def _hp(self, ea, eb, out, hermitian=False, pl=None, **kw):
-        pl = pl or self.hp
+        pl = ozaki.fit_plan(pl or self.hp, ea, eb)  # fewest moduli the operands' norms allow
         ozaki.gemm_residues(ea, eb, pl, self.res, lower_only=hermitian)
         ozaki.decode(self.res, ea, eb, pl, out, hermitian=hermitian, **kw)
         _counters["hp_calls"] += 1
@@ -132,6 +132,7 @@ class OzakiProducts:
         self._lp_with(self.lp, ea, eb, out, hermitian)
 
     def _lp_with(self, pl, ea, eb, out, hermitian=False, alpha=1.0):
+        pl = ozaki.fit_plan(pl, ea, eb)
         ozaki.gemm_residues(ea, eb, pl, self.lres, lower_only=hermitian if hermitian == "skew" else bool(hermitian))
         ozaki.decode(self.lres, ea, eb, pl, out, alpha=alpha, hermitian=hermitian)
         _counters["lp_calls"] += 1
@@ -143,6 +144,7 @@ class OzakiProducts:
         return ozaki.plan(self.ws.n, beta, beta, self.gauss)
 
     def _hp_with(self, pl, ea, eb, out, **kw):
+        pl = ozaki.fit_plan(pl, ea, eb)
         ozaki.gemm_residues(ea, eb, pl, self.res)
         ozaki.decode(self.res, ea, eb, pl, out, **kw)
         _counters["hp_calls"] += 1

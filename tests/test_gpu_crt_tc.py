@@ -224,3 +224,61 @@ def test_gauss_decode_correctly_rounded(tc):
         err = np.abs(got - exact) / ulp
         assert err.max() <= 1.0, err.max()
         assert np.mean(got == exact) >= 0.999, np.mean(got == exact)
+
+
+def _product(a, b, n, pl, fit):
+    ea = ozaki.encode(a, n, n, "a", pl, conj_t=True)
+    eb = ozaki.encode(b, n, n, "b", pl)
+    use = ozaki.fit_plan(pl, ea, eb) if fit else pl
+    res = ozaki.ResidueBuffer(n, n, pl.nmod, "cuda")
+    ozaki.gemm_residues(ea, eb, use, res)
+    out = ZPlanar.empty(n)
+    ozaki.decode(res, ea, eb, use, out)
+    torch.cuda.synchronize()
+    return out, use.nmod
+
+
+@pytest.mark.parametrize("kind", ["unitary", "gaussian", "flat", "graded"])
+@pytest.mark.parametrize("n", [256, 1024])
+def test_fit_plan_is_exact(kind, n):
+    """fit_plan keeps only the moduli the Cauchy-Schwarz bound of the integer-
+    scaled operands requires; the CRT value is then the same integer, so the
+    decoded product agrees with the worst-case plan's to the decode's chunk
+    truncation — including for 'flat' operands (every entry of equal
+    magnitude, the bound's worst case) and rows graded by 2^+-20."""
+    g = torch.Generator().manual_seed(n + len(kind))
+    if kind == "unitary":
+        x = torch.complex(torch.randn(n, n, generator=g, dtype=torch.float64),
+                          torch.randn(n, n, generator=g, dtype=torch.float64))
+        a = torch.linalg.qr(x)[0]
+        b = a
+    elif kind == "gaussian":
+        a = torch.complex(torch.randn(n, n, generator=g, dtype=torch.float64),
+                          torch.randn(n, n, generator=g, dtype=torch.float64))
+        b = torch.complex(torch.randn(n, n, generator=g, dtype=torch.float64),
+                          torch.randn(n, n, generator=g, dtype=torch.float64))
+    elif kind == "flat":
+        a = torch.polar(torch.ones(n, n, dtype=torch.float64), torch.rand(n, n, generator=g, dtype=torch.float64) * 6.283)
+        b = torch.polar(torch.ones(n, n, dtype=torch.float64), torch.rand(n, n, generator=g, dtype=torch.float64) * 6.283)
+    else:
+        a = torch.complex(torch.randn(n, n, generator=g, dtype=torch.float64),
+                          torch.randn(n, n, generator=g, dtype=torch.float64))
+        a = a * torch.exp2(torch.randint(-20, 20, (n, 1), generator=g).double())
+        b = a.conj().T.contiguous()
+    A, B = ZPlanar.from_any(a.cuda()), ZPlanar.from_any(b.cuda())
+    pl = ozaki.plan(n, ozaki.HP_BETA, ozaki.HP_BETA, gauss=True)
+    full, m_full = _product(A, B, n, pl, fit=False)
+    fit, m_fit = _product(A, B, n, pl, fit=True)
+    assert m_fit <= m_full
+    if kind == "unitary":
+        assert m_fit < m_full  # ||q_i|| = 1: at least one modulus less
+    # the same CRT integer C'; the decodes keep the top chunks of different
+    # moduli products, so they agree to far below the operands' own 2^-58
+    # truncation (relative to |a_i|_inf |b_j|_inf): exact CRT, no wraparound
+    fa = full.re[:, :n].cpu().numpy() + 1j * full.im[:, :n].cpu().numpy()
+    fb = fit.re[:, :n].cpu().numpy() + 1j * fit.im[:, :n].cpu().numpy()
+    an, bn = a.numpy(), b.numpy()
+    scale = np.abs(an.conj().T).max(axis=1)[:, None] * np.abs(bn).max(axis=0)[None, :]
+    assert np.max(np.abs(fa - fb) / scale) <= 2.0 ** -70
+    ref = an.conj().T @ bn
+    assert np.max(np.abs(fb - ref) / scale) <= 2.0 ** -40

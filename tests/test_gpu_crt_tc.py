@@ -226,6 +226,11 @@ def test_gauss_decode_correctly_rounded(tc):
         assert np.mean(got == exact) >= 0.999, np.mean(got == exact)
 
 
+@pytest.fixture(autouse=False)
+def fit_all_sizes(monkeypatch):
+    monkeypatch.setattr(ozaki, "FIT_MIN_K", 0)
+
+
 def _product(a, b, n, pl, fit):
     ea = ozaki.encode(a, n, n, "a", pl, conj_t=True)
     eb = ozaki.encode(b, n, n, "b", pl)
@@ -240,7 +245,7 @@ def _product(a, b, n, pl, fit):
 
 @pytest.mark.parametrize("kind", ["unitary", "gaussian", "flat", "graded"])
 @pytest.mark.parametrize("n", [256, 1024])
-def test_fit_plan_is_exact(kind, n):
+def test_fit_plan_is_exact(kind, n, fit_all_sizes):
     """fit_plan keeps only the moduli the Cauchy-Schwarz bound of the integer-
     scaled operands requires; the CRT value is then the same integer, so the
     decoded product agrees with the worst-case plan's to the decode's chunk

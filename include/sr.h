@@ -187,11 +187,13 @@ int sr_oz_exponents(int rows, int cols, int kind, const void* re, const double* 
    round(op(X)[i, :] 2^(beta - exps[i])) has 2-norm <= 2^beta rmax +
    sqrt(2K)/2 (Cauchy-Schwarz then bounds every entry of a product, which lets
    the Python plan drop moduli: ozaki.fit_plan).  ss_work: cols doubles of
-   workspace when transposed (column sums of squares).  No reference
-   counterpart (the reference's Ozaki path, matmul.py:151-212, sizes its
-   slices from the worst case). */
+   workspace when transposed (column sums of squares).  host_rmax (optional):
+   pinned host memory that also receives rmax, stored by a kernel (no copy
+   engine).  No reference counterpart (the reference's Ozaki path,
+   matmul.py:151-212, sizes its slices from the worst case). */
 int sr_oz_exponents_bound(int rows, int cols, int kind, const void* re, const double* im, long long ld,
-                          int transposed, int* exps, double* ss_work, double* rmax, void* stream);
+                          int transposed, int* exps, double* ss_work, double* rmax, double* host_rmax,
+                          void* stream);
 
 /* Residue planes [nmod][planes][rows_out][kpitch] (int8, K-major) of
    round(op(X) * 2^(beta - exps[i])) modulo moduli[l] (3..256, pairwise

@@ -50,7 +50,7 @@ SIGNATURES = {
     "sr_pack_c128": (_i, [_i, _i, _p, _p, _ll, _p, _ll, _p]),
     "sr_sigma_merged_dd": (_i, [_i, _p, _p, _p, _p, _p, _ll, _p, _p, _p, _p, _p, _ll, _p, _p, _p, _p, _ll, _i, _p]),
     "sr_oz_exponents": (_i, [_i, _i, _i, _p, _p, _ll, _i, _p, _p]),
-    "sr_oz_exponents_bound": (_i, [_i, _i, _i, _p, _p, _ll, _i, _p, _p, _p, _p]),
+    "sr_oz_exponents_bound": (_i, [_i, _i, _i, _p, _p, _ll, _i, _p, _p, _p, _p, _p]),
     "sr_oz_encode": (_i, [_i, _i, _i, _p, _p, _p, _p, _ll, _i, _i, _i, _p, _i, _i, _p, _p, _ll, _p]),
     "sr_oz_encode_dual": (_i, [_i, _i, _i, _p, _p, _p, _p, _ll, _p, _i, _i, _p, _p, _p, _ll, _p]),
     "sr_oz_gemm_i8": (_i, [_i, _i, _i, _i, _p, _p, _i, _ll, _p, _i, _ll, _p, _ll, _i, _i, _p]),

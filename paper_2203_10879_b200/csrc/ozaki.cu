@@ -112,6 +112,13 @@ __global__ void exps_fill_kernel(int n, int* __restrict__ e) {
   if (i < n) e[i] = EXP_FLOOR;
 }
 
+// rmax -> a pinned host word by a plain store over the bus (UVA): no copy
+// engine, so the read never queues behind a large device-to-host copy
+__global__ void publish_kernel(const double* __restrict__ src, volatile double* dst) {
+  *dst = *src;
+  __threadfence_system();
+}
+
 // column bound: r_j = sqrt(ss_j) 2^-e_j, rmax = max_j r_j
 __global__ void bound_finish_kernel(int cols, const double* __restrict__ ss, const int* __restrict__ e,
                                     double* __restrict__ rmax) {
@@ -1245,9 +1252,14 @@ extern "C" int sr_oz_exponents(int rows, int cols, int kind, const void* re, con
 }
 
 extern "C" int sr_oz_exponents_bound(int rows, int cols, int kind, const void* re, const double* im, long long ld,
-                                     int transposed, int* exps, double* ss_work, double* rmax, void* stream) {
+                                     int transposed, int* exps, double* ss_work, double* rmax, double* host_rmax,
+                                     void* stream) {
   if (!rmax || (transposed && !ss_work)) return SR_EINVAL;
-  return exponents_launch(rows, cols, kind, re, im, ld, transposed, exps, ss_work, rmax, (cudaStream_t)stream);
+  const int rc = exponents_launch(rows, cols, kind, re, im, ld, transposed, exps, ss_work, rmax, (cudaStream_t)stream);
+  if (rc != SR_OK || !host_rmax) return rc;
+  publish_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(rmax, host_rmax);
+  SR_LAUNCH_CHECK();
+  return SR_OK;
 }
 
 namespace {

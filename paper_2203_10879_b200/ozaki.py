@@ -178,8 +178,10 @@ class Encoded:
         self.rmax = torch.zeros(1, dtype=torch.float64, device=device)
         self.ssw = None
         self.bound = None
-        # the bound's pinned host copy, enqueued right after the exponent pass: fit_plan
-        # waits for that event only, so the encode itself overlaps the host's decision
+        # the bound's pinned host copy, stored by a kernel right after the exponent pass
+        # (not a copy-engine transfer, which would queue behind a large device->host
+        # copy of the result): fit_plan waits for that event only, so the encode
+        # itself overlaps the host's decision
         self.rmax_host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
         self.bound_ev = torch.cuda.Event()
 
@@ -275,8 +277,7 @@ def encode(x, rows, cols, role, pl, conj_t=False, out=None):
     if transposed and (enc.ssw is None or enc.ssw.numel() < out_rows):
         enc.ssw = torch.empty(out_rows, dtype=torch.float64, device=dev)
     _lib.call("sr_oz_exponents_bound", rows, cols, kind, re, im, ld, transposed, enc.exps.data_ptr(),
-              enc.ssw.data_ptr() if transposed else None, enc.rmax.data_ptr(), st)
-    enc.rmax_host.copy_(enc.rmax, non_blocking=True)
+              enc.ssw.data_ptr() if transposed else None, enc.rmax.data_ptr(), enc.rmax_host.data_ptr(), st)
     enc.bound_ev.record()
     _lib.call("sr_oz_encode", out_rows, K, kind, re, im, re_lo, im_lo, ld, transposed, conj, layout,
               enc.exps.data_ptr(), beta, pl.nmod, pl.moduli_ptr(), enc.buf.data_ptr(), enc.kp, st)

@@ -530,12 +530,12 @@ __device__ __forceinline__ void finish_store(const DecodeParams& p, const double
 
 // Lean CRT finish for FP64 / complex64 outputs of the Gaussian products (both
 // the SIMT and the tensor-core decode use it, so they agree bit for bit):
-// t_j = S_j - k P_j exact, the bottom chunk carry-normalised and snapped as in
-// crt_finish, then V = t_0 2^o0 + t_1 2^o1 (+ t_2 2^o2 ...) as an exact
+// t_j = S_j - k P_j exact, the bottom chunk snapped as in crt_finish (no carry
+// normalisation needed), then V = t_0 2^o0 + t_1 2^o1 (+ t_2 2^o2 ...) as an exact
 // two_sum of the top pair plus the rest, unscaled, shifted / added with one
 // more exact two_sum, and rounded once: correctly rounded up to a rare double
 // rounding (error < 0.5 ulp + 2^-80 relative), exact whenever the result is
-// representable (zeros, I I = I, small integers), ~40 FP64 instructions per
+// representable (zeros, I I = I, small integers), ~35 FP64 instructions per
 // entry and plane instead of ~120 for the double-double finish.
 // rint for |x| < 2^51 on the FP64 pipe (two DADDs; FRND.F64 runs on the
 // narrow XU pipe, which the decode's three roundings per entry saturated):
@@ -553,11 +553,10 @@ __device__ __forceinline__ double crt_lean(const DecodeParams& p, const double (
   double t[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) t[c] = fma(-k, p.pc[c], S[c]);  // exact integers
-  if (NC > 1) {
-    const double c = rint_small(t[NC - 1] * p.icw[NC - 1]);
-    t[NC - 1] = fma(-c, p.cw[NC - 1], t[NC - 1]);
-    t[NC - 2] += c;
-  }
+  // snap (truncated CRT): the chunks above the bottom one are multiples of its
+  // 2^40 units, so rounding the bottom chunk to the grid rounds C' to it
+  // whether or not the chunks are carry-normalised (two_sum below needs no
+  // ordering of its operands)
   if (p.snap > 0.0) t[NC - 1] = rint_small(t[NC - 1] * p.inv_snap) * p.snap;
   double s, e = 0.0;
   if (NC > 1)

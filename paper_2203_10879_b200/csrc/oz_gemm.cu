@@ -43,7 +43,11 @@ constexpr int TM = 128, TN = 128, TK = 64;  // tile: 128 rows x 128 cols, 64-byt
 constexpr int MAX_STAGES = 12;                // ring slots (2-SM: complex 6 x 32 KB, real 12 x 16 KB)
 constexpr int SMEM_RING = 200 * 1024;
 constexpr int PLANE_BYTES = TM * TK;        // 8 KB per 128-row, 64-byte plane
-constexpr int NUM_THREADS = 192;
+// epilogue warps: 8 (two per TMEM lane quadrant, splitting the 16-column
+// chunks) for wide units, whose epilogue does not overlap the MMAs; 4 for the
+// double-buffered narrow units (8 measured 10 % slower on Hermitian products)
+constexpr int MAX_EPI_WARPS = 8;
+constexpr int NUM_THREADS = 64 + 32 * MAX_EPI_WARPS;  // launch bound; the block has 64 + 32 p.epi threads
 // M-tiles per rasterisation group (complex products; the stacked real ones use
 // twice as many — their M is 2n).  Measured with the dynamic unit queue at
 // n = 8192, 17 moduli: DRAM reads per hp launch 30 / 17.7 / 31.7 / 132 GB for
@@ -69,6 +73,7 @@ struct OzParams {
   int wide;                     // TWO && real: a unit is N = 512 (two N = 256 MMAs per k-block into both TMEM
                                 //   accumulators): the pair's A tile is read once per 512 B rows, 25 % less
                                 //   L2->SM ingest per MAC; the epilogue then drains both accumulators
+  int epi;                      // epilogue warps (4 or 8)
   int herm;                     // gauss, Hermitian (+1) / skew (-1) C: only plane 0 is computed, and the
                                 //   epilogue also writes herm * its transpose as plane 1 (C- = +-C+^T)
   long long out_pitch;          // bytes between output rows
@@ -76,6 +81,8 @@ struct OzParams {
   long long out_mod;            // bytes between moduli
   int moduli[MAX_MODULI];
   float inv[MAX_MODULI];
+  uint32_t bm[MAX_MODULI];      // Barrett multiplier floor(2^32 / p) + 1
+  uint32_t roff[MAX_MODULI];    // a multiple of p above |accumulator|, + p/2 (symmetric residue)
 };
 
 __device__ __forceinline__ constexpr uint32_t idesc_i8(int m, int n) {
@@ -165,17 +172,6 @@ __device__ __forceinline__ void decode_tile(const OzParams& p, int t, int& l, in
   nt = in / gm;
 }
 
-// symmetric residue of v modulo p: [-floor(p/2), ceil(p/2) - 1]
-__device__ __forceinline__ int sym_mod(int v, int p, float inv) {
-  int q = __float2int_rn((float)v * inv);
-  int r = v - q * p;
-  const int lo = -(p >> 1), hi = ((p + 1) >> 1) - 1;
-  if (r > hi) r -= p;
-  if (r < lo) r += p;
-  if (r > hi) r -= p;
-  if (r < lo) r += p;
-  return r;
-}
 
 // CM = 1: one CTA per tile.  CM = 2: clusters of two CTAs own vertically
 // adjacent M-tiles with the same N-tile; each CTA TMA-loads half the rows of
@@ -231,11 +227,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull_bar(b), 1);
-      mbar_init(tempty_bar(b), TWO ? 8 : 128);  // TWO: one arrive per epilogue warp of both CTAs
+      mbar_init(tempty_bar(b), TWO ? 2 * p.epi : 32 * p.epi);  // TWO: one arrive per epilogue warp of both CTAs
     }
     for (int q = 0; q < QD; ++q) {
       mbar_init(qfull_bar(q), 1);
-      mbar_init(qempty_bar(q), 5);  // the MMA thread + one lane per epilogue warp
+      mbar_init(qempty_bar(q), 1 + p.epi);  // the MMA thread + one lane per epilogue warp
       mbar_init(pfull_bar(q), 1);
       mbar_init(pempty_bar(q), CM > 1 ? CM - 1 : 1);
     }
@@ -469,7 +465,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else {
     // ---------------- epilogue: TMEM -> residues -> global ----------------
+    // p.epi warps: lane quadrant ew = warp & 3; with 8, the two warps of a quadrant
+    // take alternate 16-column chunks.  Residues by an integer Barrett step
+    // (no conversions: the float quotient's I2F / F2I ran on the narrow XU pipe),
+    // the next chunk's TMEM load in flight while this one is reduced.  With wide
+    // units the epilogue does not overlap the MMAs, so its length is tensor-pipe
+    // idle time.
     const int ew = warp & 3;  // TMEM lane quadrant this warp may access
+    const int half = p.epi == 8 ? (warp - 2) >> 2 : 0;
+    const int CSTEP = p.epi == 8 ? 2 : 1;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int v = 0;; ++v) {
@@ -482,7 +486,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int l, mt, nt;
       if (!unit(t, l, mt, nt)) continue;
       const int pm = p.moduli[l];
-      const float inv = p.inv[l];
+      const uint32_t bm = p.bm[l], roff = p.roff[l];
+      const int hp = pm >> 1;
       mbar_wait(tfull_bar(acc), acc_phase);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       int g = 0, row = mt * TM + ew * 32 + lane;
@@ -492,24 +497,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       int8_t* base = out + (size_t)l * p.out_mod + (size_t)g * p.out_plane + (size_t)row * p.out_pitch;
       const int nchunks = p.wide ? 32 : 16;
-#pragma unroll 1
-      for (int chunk = 0; chunk < nchunks; ++chunk) {
-        uint32_t v[16];
-        tmem_ld16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * 256 + chunk * 16), v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * 256);
+      // symmetric residue of the accumulator v: u = v + roff in [0, 2^32),
+      // q = umulhi(u, bm) is floor(u / p) or one more, r = u - q p in [-p, p)
+      auto red = [&](uint32_t vv) -> int {
+        const uint32_t u = vv + roff;
+        const int r = (int)(u - __umulhi(u, bm) * (uint32_t)pm);
+        return r - hp + ((r >> 31) & pm);
+      };
+      auto emit = [&](const uint32_t (&vc)[16], int chunk) {
         const int plane = p.real ? 0 : chunk >> 3;
         const int col0 = nt * tn + (p.real ? chunk : (chunk & 7)) * 16;
         uint32_t packed[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint32_t w = 0;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            int r = sym_mod((int)v[q * 4 + e], pm, inv);
-            w |= ((uint32_t)(r & 0xFF)) << (8 * e);
-          }
-          packed[q] = w;
-        }
+        for (int q = 0; q < 4; ++q)
+          packed[q] = __byte_perm(__byte_perm(red(vc[q * 4]), red(vc[q * 4 + 1]), 0x0040),
+                                  __byte_perm(red(vc[q * 4 + 2]), red(vc[q * 4 + 3]), 0x0040), 0x5410);
         if (p.herm && row < p.M) {
           // C- = herm * C+^T: this row's 16 values down column `row` of plane 1
           // (the warp's 32 rows are 32 consecutive bytes of each target row)
@@ -533,6 +536,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int e = 0; e < 16 && col0 + e < p.N; ++e) dst[e] = (int8_t)((packed[e >> 2] >> (8 * (e & 3))) & 0xFF);
           }
         }
+      };
+      uint32_t va[16], vb[16];
+      int chunk = half;
+      tmem_ld16(tbase + (uint32_t)(chunk * 16), va);
+#pragma unroll 1
+      for (; chunk < nchunks; chunk += 2 * CSTEP) {
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");  // va = chunk
+        if (chunk + CSTEP < nchunks) tmem_ld16(tbase + (uint32_t)((chunk + CSTEP) * 16), vb);
+        emit(va, chunk);
+        if (chunk + CSTEP >= nchunks) break;
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");  // vb = chunk + CSTEP
+        if (chunk + 2 * CSTEP < nchunks) tmem_ld16(tbase + (uint32_t)((chunk + 2 * CSTEP) * 16), va);
+        emit(vb, chunk + CSTEP);
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       if (TWO) {
@@ -666,6 +682,14 @@ int gemm_launch(int M, int N, int K, int nmod, const int* moduli, const void* a,
     if (moduli[i] < 3 || moduli[i] > 256) return SR_EINVAL;
     p.moduli[i] = moduli[i];
     p.inv[i] = 1.0f / (float)moduli[i];
+    // |accumulator| <= 2 K (p/2)^2 (two MMAs per k for the (re, im) planes); the
+    // offset keeps v + roff in [0, 2^32) for the Barrett step
+    const unsigned long long m = (unsigned long long)moduli[i];
+    const unsigned long long vmax = 2ull * (unsigned long long)K * (m / 2) * (m / 2);
+    const unsigned long long off = (vmax / m + 1) * m + m / 2;
+    if (off + vmax >= (1ull << 32)) return SR_EINVAL;  // K beyond 2^16
+    p.bm[i] = (uint32_t)((1ull << 32) / m + 1);
+    p.roff[i] = (uint32_t)off;
   }
   int grid = num_sms > 0 ? num_sms : 148;
   // clusters of two CTAs sharing the B tile whenever there are M-tile pairs to share
@@ -688,6 +712,7 @@ int gemm_launch(int M, int N, int K, int nmod, const int* moduli, const void* a,
   const char* wide_env = getenv("SR_OZ_WIDE");
   if (wide_env && *wide_env && strcmp(wide_env, "auto") != 0) wide = two && real && atoi(wide_env) != 0;
   p.wide = wide ? 1 : 0;
+  p.epi = (wide && !getenv("SR_OZ_EPI4")) ? 8 : 4;
   if (p.wide) p.tiles_n = (N + 4 * TN - 1) / (4 * TN);
   const int tiles = nmod * p.tiles_m * p.tiles_n;
   if (two) {  // per CTA: its A rows and half of the pair's B operand (real: two k-blocks per slot)
@@ -731,7 +756,7 @@ int gemm_launch(int M, int N, int K, int nmod, const int* moduli, const void* a,
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.blockDim = dim3(64 + 32 * p.epi);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = (cudaStream_t)stream;
   cudaLaunchAttribute attr;

@@ -74,6 +74,7 @@ struct OzParams {
                                 //   accumulators): the pair's A tile is read once per 512 B rows, 25 % less
                                 //   L2->SM ingest per MAC; the epilogue then drains both accumulators
   int epi;                      // epilogue warps (4 or 8)
+  int kstep;                    // 2-SM real products: 64-byte k-blocks per ring slot (MMAs per barrier round trip)
   int herm;                     // gauss, Hermitian (+1) / skew (-1) C: only plane 0 is computed, and the
                                 //   epilogue also writes herm * its transpose as plane 1 (C- = +-C+^T)
   long long out_pitch;          // bytes between output rows
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // 2-SM real products carry two 64-byte k-blocks per ring slot (four MMAs per
   // barrier round trip, like the complex products): with one k-block per slot
   // the issuer's per-slot overhead left the tensor pipe ~45 % idle
-  const int kstep = (TWO && p.real) ? 2 : 1;
+  const int kstep = (TWO && p.real) ? p.kstep : 1;
   const int stage_bytes = kstep * (a_bytes + b_bytes);
   const int STAGES = p.stages;
   const int tn = p.real ? (p.wide ? 4 : 2) * TN : TN;
@@ -405,25 +406,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t sb = sa + a_bytes;
           if (TWO) {
             const uint32_t id = idesc_i8(256, 256);
+            // descriptors as 16-byte offsets of the stage's base descriptor (the
+            // start-address field is the low 14 bits; every address stays below
+            // 256 KB): a handful of adds per MMA instead of a descriptor build
+            const uint64_t ds = umma_desc_sw64(sa);
             if (p.real) {
-#pragma unroll
-              for (int h = 0; h < 2; ++h)
+              for (int h = 0; h < kstep; ++h)
 #pragma unroll
                 for (int ks = 0; ks < TK / 32; ++ks) {
-                  const uint64_t ad = umma_desc_sw64(sa + h * a_bytes + ks * 32);
-                  umma_i8_2sm(d, ad, umma_desc_sw64(sa + 2 * a_bytes + h * b_bytes + ks * 32), id,
-                              (kb | h | ks) != 0);
+                  const uint64_t ad = ds + (uint64_t)((h * a_bytes + ks * 32) >> 4);
+                  const uint64_t bd = ds + (uint64_t)((kstep * a_bytes + h * b_bytes + ks * 32) >> 4);
+                  umma_i8_2sm(d, ad, bd, id, (kb | h | ks) != 0);
                   if (p.wide)  // the second N = 256 half into the other accumulator (d = base)
-                    umma_i8_2sm(d + 256, ad, umma_desc_sw64(sa + 2 * a_bytes + h * b_bytes + PLANE_BYTES + ks * 32),
-                                id, (kb | h | ks) != 0);
+                    umma_i8_2sm(d + 256, ad, bd + (uint64_t)(PLANE_BYTES >> 4), id, (kb | h | ks) != 0);
                 }
             } else {
 #pragma unroll
               for (int ks = 0; ks < TK / 32; ++ks) {
                 const uint32_t acc_flag = (kb | ks) != 0;
-                umma_i8_2sm(d, umma_desc_sw64(sa + ks * 32), umma_desc_sw64(sb + ks * 32), id, acc_flag);
-                umma_i8_2sm(d, umma_desc_sw64(sa + PLANE_BYTES + ks * 32), umma_desc_sw64(sb + PLANE_BYTES + ks * 32),
-                            id, 1u);
+                const uint64_t ad = ds + (uint64_t)((ks * 32) >> 4), bd = ds + (uint64_t)((a_bytes + ks * 32) >> 4);
+                umma_i8_2sm(d, ad, bd, id, acc_flag);
+                umma_i8_2sm(d, ad + (uint64_t)(PLANE_BYTES >> 4), bd + (uint64_t)(PLANE_BYTES >> 4), id, 1u);
               }
             }
             umma_commit_2sm(empty_bar(stage), 3);
@@ -716,7 +719,9 @@ int gemm_launch(int M, int N, int K, int nmod, const int* moduli, const void* a,
   if (p.wide) p.tiles_n = (N + 4 * TN - 1) / (4 * TN);
   const int tiles = nmod * p.tiles_m * p.tiles_n;
   if (two) {  // per CTA: its A rows and half of the pair's B operand (real: two k-blocks per slot)
-    p.stages = std::min(MAX_STAGES, SMEM_RING / ((real ? 2 : 1) *
+    // narrow real products: four k-blocks per slot (eight MMAs per barrier round trip, like the wide ones)
+    p.kstep = real ? ((p.wide || getenv("SR_OZ_KSTEP2")) ? 2 : 4) : 1;
+    p.stages = std::min(MAX_STAGES, SMEM_RING / ((real ? p.kstep : 1) *
                                                  (p.a_planes + (real ? (p.wide ? 2 : 1) : 2)) * PLANE_BYTES));
     if (getenv("SR_OZ_STAGES")) p.stages = std::max(2, std::min(p.stages, atoi(getenv("SR_OZ_STAGES"))));
   }

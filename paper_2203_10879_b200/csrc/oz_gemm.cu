@@ -46,7 +46,7 @@ constexpr int PLANE_BYTES = TM * TK;        // 8 KB per 128-row, 64-byte plane
 // epilogue warps: 8 (two per TMEM lane quadrant, splitting the 16-column
 // chunks) for wide units, whose epilogue does not overlap the MMAs; 4 for the
 // double-buffered narrow units (8 measured 10 % slower on Hermitian products)
-constexpr int MAX_EPI_WARPS = 8;
+constexpr int MAX_EPI_WARPS = 16;
 constexpr int NUM_THREADS = 64 + 32 * MAX_EPI_WARPS;  // launch bound; the block has 64 + 32 p.epi threads
 // M-tiles per rasterisation group (complex products; the stacked real ones use
 // twice as many — their M is 2n).  Measured with the dynamic unit queue at
@@ -475,8 +475,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // units the epilogue does not overlap the MMAs, so its length is tensor-pipe
     // idle time.
     const int ew = warp & 3;  // TMEM lane quadrant this warp may access
-    const int half = p.epi == 8 ? (warp - 2) >> 2 : 0;
-    const int CSTEP = p.epi == 8 ? 2 : 1;
+    const int half = (warp - 2) >> 2;  // 0 .. p.epi / 4 - 1
+    const int CSTEP = p.epi >> 2;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int v = 0;; ++v) {
@@ -715,7 +715,8 @@ int gemm_launch(int M, int N, int K, int nmod, const int* moduli, const void* a,
   const char* wide_env = getenv("SR_OZ_WIDE");
   if (wide_env && *wide_env && strcmp(wide_env, "auto") != 0) wide = two && real && atoi(wide_env) != 0;
   p.wide = wide ? 1 : 0;
-  p.epi = (wide && !getenv("SR_OZ_EPI4")) ? 8 : 4;
+  p.epi = (wide && !getenv("SR_OZ_EPI4")) ? (getenv("SR_OZ_EPI") ? atoi(getenv("SR_OZ_EPI")) : 8) : 4;
+  if (p.epi != 4 && p.epi != 8 && p.epi != 16) p.epi = 8;
   if (p.wide) p.tiles_n = (N + 4 * TN - 1) / (4 * TN);
   const int tiles = nmod * p.tiles_m * p.tiles_n;
   if (two) {  // per CTA: its A rows and half of the pair's B operand (real: two k-blocks per slot)

@@ -55,7 +55,13 @@ constexpr int TC_STAGES = SR_FAR_STAGES;
 constexpr int A_PLANE = 128 * 64;                  // bytes: 128 rows x 64 B
 constexpr int B_PLANE = 64 * 64;                   // bytes: 64 rows x 64 B
 constexpr int TC_STAGE = 2 * A_PLANE + 2 * B_PLANE;
-constexpr int TC_THREADS = 192;
+#ifndef SR_FAR_EPI_WARPS
+#define SR_FAR_EPI_WARPS 8  // two per TMEM lane quadrant, each owning half of the unit's 32 line entries
+#endif
+constexpr int EPI_W = SR_FAR_EPI_WARPS;
+constexpr int EPI_HALF = EPI_W / 4;   // warps per quadrant (1 or 2)
+constexpr int EPI_SPAN = NB / EPI_HALF;  // line entries (COL: columns, ROW: rows) per epilogue warp
+constexpr int TC_THREADS = 64 + 32 * EPI_W;
 constexpr uint32_t TC_TMEM_COLS = 128;             // two 64-column accumulators
 constexpr int EPI_BYTES = 2 * 4 * 32 * 33 * 8;      // epilogue staging, double-buffered (2 x 4 warps x 32 x 33 float2)
 constexpr int TC_SMEM = 1024 + TC_STAGES * TC_STAGE + EPI_BYTES + 256;
@@ -251,14 +257,14 @@ template <bool ROW>
 // fill two sub-partitions completely and serialise the critical path behind
 // every far launch).
 #ifndef SR_FAR_TC_MAXNREG
-#define SR_FAR_TC_MAXNREG 216
+#define SR_FAR_TC_MAXNREG (EPI_W == 8 ? 168 : 216)  // room for a 4-warp SOLVE CTA beside a far CTA
 #endif
 __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
     far_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                   const __grid_constant__ FarTcArgs p, float2* __restrict__ Rf) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ float eb_s[4][32];  // 2^(e_b) of the tile's B lines
-  __shared__ int eb_x[4][32];    // e_b itself (the out-of-range path)
+  __shared__ float eb_s[EPI_W][32];  // 2^(e_b) of the tile's B lines (per epilogue warp)
+  __shared__ int eb_x[EPI_W][32];    // e_b itself (the out-of-range path)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   float2* stage_buf = reinterpret_cast<float2*>(smem + TC_STAGES * TC_STAGE);  // COL epilogue staging, 4 x 32 x 33
   uint64_t* bars = (uint64_t*)(smem + TC_STAGES * TC_STAGE + EPI_BYTES);
@@ -296,7 +302,7 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), 128);
+      mbar_init(tempty_bar(a), 32 * EPI_W);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&map_a) : "memory");
@@ -357,25 +363,39 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
         __syncwarp();
       }
     }
-  } else {  // epilogue: warps 2..5, TMEM lane quadrant warp & 3
+  } else {  // epilogue: warps 2.., TMEM lane quadrant warp & 3, line-entry half eh
     const int ew = warp & 3;
+    const int ewi = warp - 2;          // epilogue warp index
+    const int eh = ewi >> 2;           // which EPI_SPAN line entries (COL: columns, ROW: rows) of the unit
+    const int j0e = eh * EPI_SPAN;
     const int n = p.n;
     const long long ld = p.ld;
-    // two staging blocks per warp: the Rf block of unit k+1 is loaded while
-    // unit k is folded (the RMW was latency-bound on one 32 KB block in flight
-    // per SM)
+    // two staging blocks per quadrant (shared by the quadrant's warps, each
+    // touching only its own entries): the Rf block of unit k+1 is loaded while
+    // unit k is folded
     float2* bufs[2] = {stage_buf + ew * 32 * 33, stage_buf + (4 + ew) * 32 * 33};
     auto issue_rf = [&](int uu, float2* dstb) {
       int line_, t0_, a_row0_, b_row0_, k0_;
       unit(uu, line_, t0_, a_row0_, b_row0_, k0_);
       const int R0_ = !ROW ? a_row0_ + ew * 32 : line_ * NB;
       const int C0_ = !ROW ? line_ * NB : a_row0_ + ew * 32;
-      const bool okc = (t0_ + ew < p.h) && C0_ + lane < n;
-#pragma unroll 8
-      for (int r = 0; r < NB; ++r) {
-        const bool ok = okc && R0_ + r < n;
-        const float2* src = Rf + (ok ? (size_t)(R0_ + r) * ld + C0_ + lane : 0);
-        const uint32_t dst = smem_u32(dstb + r * 33 + lane);
+      const bool okt = t0_ + ew < p.h;
+      // COL: this warp's columns j0e.. of all 32 rows; ROW: its rows j0e.. of all 32 columns
+      // (EPI_SPAN x 32 entries, 32 / EPI_SPAN rows per instruction, coalesced along the rows)
+      constexpr int RPI = 32 / EPI_SPAN;  // rows per instruction (COL)
+#pragma unroll 4
+      for (int it = 0; it < 32 * EPI_SPAN / 32; ++it) {
+        int r, c;
+        if (!ROW) {
+          r = it * RPI + lane / EPI_SPAN;
+          c = j0e + lane % EPI_SPAN;
+        } else {
+          r = j0e + it;
+          c = lane;
+        }
+        const bool ok = okt && R0_ + r < n && C0_ + c < n;
+        const float2* src = Rf + (ok ? (size_t)(R0_ + r) * ld + C0_ + c : 0);
+        const uint32_t dst = smem_u32(dstb + r * 33 + c);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0)
                      : "memory");
       }
@@ -397,8 +417,8 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
       // in [2^-127, 2^127), i.e. every complex64 line that is neither
       // subnormal nor within a factor 2 of overflow)
       const int eb = jl < n ? line_exp(max4(p.b_max, (size_t)n, jl)) : 0;
-      eb_s[ew][lane] = ldexpf(1.f, eb);
-      eb_x[ew][lane] = eb;
+      eb_s[ewi][lane] = ldexpf(1.f, eb);
+      eb_x[ewi][lane] = eb;
       const float fa = ldexpf(1.f, ea);
       // a line maximum outside [2^-127, 2^126] makes one factor 0 or inf: then
       // the whole warp scales by the combined 2^(e_a + e_b) instead (one
@@ -407,13 +427,8 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
       __syncwarp();
       const int tgt = t0 + ew;  // target tile index along the line
       const bool live = tgt < p.h;
-      // this unit's Rf block was prefetched into bufs[k & 1] (cp.async,
-      // zero-filled outside the matrix) one unit ahead; start the next unit's
-      // now, so two blocks are in flight while the MMAs run (targets of
-      // different units never overlap, so nothing in flight writes them).
-      // Shared memory instead of registers keeps the kernel at <= 216
-      // registers.  buf[r][c] = Rf[R0 + r][C0 + c]: COL (R0, C0) = (target
-      // rows, line column block); ROW = (line row block, target columns)
+      // this unit's Rf block was prefetched into bufs[k & 1] one unit ahead;
+      // start the next unit's now (targets of different units never overlap)
       float2* buf = bufs[k & 1];
       const int R0 = !ROW ? a_row0 + ew * 32 : line * NB;
       const int C0 = !ROW ? line * NB : a_row0 + ew * 32;
@@ -421,11 +436,11 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
       asm volatile("cp.async.commit_group;\n" ::: "memory");
       mbar_wait(tfull_bar(acc), (k >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      uint32_t v[64];
+      uint32_t v[2 * EPI_SPAN];  // this warp's line entries (re, im)
 #pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
+      for (int qq = 0; qq < 2 * EPI_SPAN / 16; ++qq) {
         uint32_t (&vq)[16] = *reinterpret_cast<uint32_t(*)[16]>(&v[16 * qq]);
-        tmem_ld16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * 64 + 16 * qq), vq);
+        tmem_ld16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * 64 + 2 * j0e + 16 * qq), vq);
       }
       asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -434,50 +449,34 @@ __global__ void __maxnreg__(SR_FAR_TC_MAXNREG)
       __syncwarp();
       if (live) {
         if (!ROW) {
-          // this lane's accumulator row (R0 + lane) folded into the staged
-          // block, then the block stored row by row (coalesced 256-byte rows)
-          if (!wide) {  // warp-uniform: the common path pays nothing for the rare one
+          // this lane's accumulator row (R0 + lane), columns j0e.., folded into the
+          // staged block, then the block's columns stored row by row
 #pragma unroll
-            for (int c = 0; c < NB; ++c) {
-              const float sc = fa * eb_s[ew][c];
-              float2& q = buf[lane * 33 + c];
-              q = make_float2(q.x - __uint_as_float(v[2 * c]) * sc, q.y - __uint_as_float(v[2 * c + 1]) * sc);
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < NB; ++c) {
-              const float sc = ldexpf(1.f, ea + eb_x[ew][c]);
-              float2& q = buf[lane * 33 + c];
-              q = make_float2(q.x - __uint_as_float(v[2 * c]) * sc, q.y - __uint_as_float(v[2 * c + 1]) * sc);
-            }
+          for (int c = 0; c < EPI_SPAN; ++c) {
+            const float sc = wide ? ldexpf(1.f, ea + eb_x[ewi][j0e + c]) : fa * eb_s[ewi][j0e + c];
+            float2& q = buf[lane * 33 + j0e + c];
+            q = make_float2(q.x - __uint_as_float(v[2 * c]) * sc, q.y - __uint_as_float(v[2 * c + 1]) * sc);
           }
           __syncwarp();
-          if (C0 + lane < n) {
-#pragma unroll 8
-            for (int r = 0; r < NB; ++r)
-              if (R0 + r < n) Rf[(size_t)(R0 + r) * ld + C0 + lane] = buf[r * 33 + lane];
+          constexpr int RPI = 32 / EPI_SPAN;
+          const int cc = j0e + lane % EPI_SPAN;
+          if (C0 + cc < n) {
+#pragma unroll 4
+            for (int it = 0; it < EPI_SPAN; ++it) {
+              const int r = it * RPI + lane / EPI_SPAN;
+              if (R0 + r < n) Rf[(size_t)(R0 + r) * ld + C0 + cc] = buf[r * 33 + cc];
+            }
           }
         } else if (idx < n) {
-          // this lane's accumulator column (C0 + lane = idx)
-          if (!wide) {
+          // this lane's accumulator column (C0 + lane = idx), rows j0e..
 #pragma unroll
-            for (int i = 0; i < NB; ++i) {
-              if (R0 + i < n) {
-                const float sc = fa * eb_s[ew][i];
-                const float2 q = buf[i * 33 + lane];
-                Rf[(size_t)(R0 + i) * ld + idx] = make_float2(q.x + __uint_as_float(v[2 * i]) * sc,
-                                                              q.y + __uint_as_float(v[2 * i + 1]) * sc);
-              }
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < NB; ++i) {
-              if (R0 + i < n) {
-                const float sc = ldexpf(1.f, ea + eb_x[ew][i]);
-                const float2 q = buf[i * 33 + lane];
-                Rf[(size_t)(R0 + i) * ld + idx] = make_float2(q.x + __uint_as_float(v[2 * i]) * sc,
-                                                              q.y + __uint_as_float(v[2 * i + 1]) * sc);
-              }
+          for (int i = 0; i < EPI_SPAN; ++i) {
+            const int ri = j0e + i;
+            if (R0 + ri < n) {
+              const float sc = wide ? ldexpf(1.f, ea + eb_x[ewi][ri]) : fa * eb_s[ewi][ri];
+              const float2 q = buf[ri * 33 + lane];
+              Rf[(size_t)(R0 + ri) * ld + idx] = make_float2(q.x + __uint_as_float(v[2 * i]) * sc,
+                                                             q.y + __uint_as_float(v[2 * i + 1]) * sc);
             }
           }
         }

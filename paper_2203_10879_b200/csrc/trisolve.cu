@@ -275,12 +275,12 @@ __device__ __forceinline__ unsigned tile_solve_warp(const C* sT2, const C* sD, c
 // buffered shared slot that is read after the next step's barrier.  A quarter
 // of the multiply-adds per warp and a quarter of the registers (the CTA can
 // share an SM with a far tensor-core CTA).
-template <typename C, bool DIAG>
+template <typename C, bool DIAG, int NW = 4>
 __device__ __forceinline__ unsigned tile_solve_cta(const C* sT2, const C* sD, const C* sP, const C* sR, C* sX,
-                                                   C (*xs)[NB], C (*hand)[4][NB], int valid_i, int valid_j,
+                                                   C (*xs)[NB], C (*hand)[NW][NB], int valid_i, int valid_j,
                                                    typename Real<C>::T clip) {
   using R = typename Real<C>::T;
-  constexpr int W = 8;  // window positions per warp
+  constexpr int W = NB / NW;  // window positions per warp
   const int i = threadIdx.x & 31, w = threadIdx.x >> 5;
   const R clip2 = clip * clip;
   unsigned nclip = 0;
@@ -308,11 +308,11 @@ __device__ __forceinline__ unsigned tile_solve_cta(const C* sT2, const C* sD, co
       }
       xs[t & 1][i] = x;
     }
-    asm volatile("bar.sync 1, 128;\n" ::: "memory");
-    // position 7: handed over by warp w+1 at the end of the previous step
-    // (warp 3: the column entering the window)
+    asm volatile("bar.sync 1, %0;\n" ::"n"(NW * 32) : "memory");
+    // position W-1: handed over by warp w+1 at the end of the previous step
+    // (the last warp: the column entering the window)
     if (t > 0) {
-      if (w < 3) {
+      if (w < NW - 1) {
         pend[W - 1] = hand[(t - 1) & 1][w + 1][i];
       } else {
         const int c = t + i;
@@ -426,17 +426,18 @@ __global__ void __launch_bounds__(SolveShape<C>::THREADS) solve_kernel(SweepArgs
     if (gi < n && gj < n) L[(size_t)gi * ld + gj] = (I == M && r <= tid) ? czero<C>() : s1[r * LD + tid];
   }
 #else
-  static_assert(SolveShape<C>::THREADS == 128, "the CTA tile solve needs four warps");
+  constexpr int NW = SolveShape<C>::THREADS / 32;
+  static_assert(NW == 4 || NW == 8, "the CTA tile solve needs four or eight warps");
   __shared__ C xs[2][NB];
-  __shared__ C hand[2][4][NB];
+  __shared__ C hand[2][NW][NB];
   if (I == M)
-    nclip = tile_solve_cta<C, true>(sT2, sD, sP, sRf, s1, xs, hand, vi, vj, cl);
+    nclip = tile_solve_cta<C, true, NW>(sT2, sD, sP, sRf, s1, xs, hand, vi, vj, cl);
   else
-    nclip = tile_solve_cta<C, false>(sT2, sD, sP, sRf, s1, xs, hand, vi, vj, cl);
+    nclip = tile_solve_cta<C, false, NW>(sT2, sD, sP, sRf, s1, xs, hand, vi, vj, cl);
   __syncthreads();
   {
     const int gj = M * NB + (tid & 31);
-    for (int r = tid >> 5; r < NB; r += 4) {
+    for (int r = tid >> 5; r < NB; r += SolveShape<C>::THREADS / 32) {
       const int gi = I * NB + r;
       if (gi < n && gj < n) L[(size_t)gi * ld + gj] = (I == M && r <= (tid & 31)) ? czero<C>() : s1[r * LD + (tid & 31)];
     }

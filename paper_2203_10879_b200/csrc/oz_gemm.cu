@@ -47,6 +47,9 @@ constexpr int PLANE_BYTES = TM * TK;        // 8 KB per 128-row, 64-byte plane
 // chunks) for wide units, whose epilogue does not overlap the MMAs; 4 for the
 // double-buffered narrow units (8 measured 10 % slower on Hermitian products)
 constexpr int MAX_EPI_WARPS = 16;
+#ifndef SR_OZ_DIAG_NO_TRANSPOSE
+#define SR_OZ_DIAG_NO_TRANSPOSE 0  // timing diagnostic only: Hermitian products without the C- = C+^T write
+#endif
 constexpr int NUM_THREADS = 64 + 32 * MAX_EPI_WARPS;  // launch bound; the block has 64 + 32 p.epi threads
 // M-tiles per rasterisation group (complex products; the stacked real ones use
 // twice as many — their M is 2n).  Measured with the dynamic unit queue at
@@ -56,6 +59,7 @@ constexpr int GROUP_M = 16;
 constexpr int MAX_MODULI = 32;
 constexpr int QD = 16;        // work-unit queue depth (producer -> MMA / epilogue, rank 0 -> rank 1)
 constexpr int SMEM_TAIL = 1024;  // barriers, unit queues, TMEM slot
+constexpr int XPOSE_WARP_BYTES = 16 * 32;  // per epilogue warp: the 32 x 16 transposed-write tile
 
 struct OzParams {
   int M, N, K, nmod;
@@ -508,26 +512,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int r = (int)(u - __umulhi(u, bm) * (uint32_t)pm);
         return r - hp + ((r >> 31) & pm);
       };
+      // Hermitian products: per-warp staging for the transposed write (below)
+      uint8_t* xs = smem + SMEM_RING + SMEM_TAIL + (warp - 2) * XPOSE_WARP_BYTES;
+      const int row0 = row - lane;  // the warp's first row
       auto emit = [&](const uint32_t (&vc)[16], int chunk) {
         const int plane = p.real ? 0 : chunk >> 3;
         const int col0 = nt * tn + (p.real ? chunk : (chunk & 7)) * 16;
+        int r[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) r[e] = red(vc[e]);
         uint32_t packed[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          packed[q] = __byte_perm(__byte_perm(red(vc[q * 4]), red(vc[q * 4 + 1]), 0x0040),
-                                  __byte_perm(red(vc[q * 4 + 2]), red(vc[q * 4 + 3]), 0x0040), 0x5410);
-        if (p.herm && row < p.M) {
-          // C- = herm * C+^T: this row's 16 values down column `row` of plane 1
-          // (the warp's 32 rows are 32 consecutive bytes of each target row)
-          int8_t* tdst = out + (size_t)l * p.out_mod + p.out_plane + row;
-          const uint32_t nmask = p.herm < 0 ? 0xFFFFFFFFu : 0u;
+          packed[q] = __byte_perm(__byte_perm(r[q * 4], r[q * 4 + 1], 0x0040),
+                                  __byte_perm(r[q * 4 + 2], r[q * 4 + 3], 0x0040), 0x5410);
+        if (p.herm && !SR_OZ_DIAG_NO_TRANSPOSE) {
+          // C- = herm * C+^T: the warp's 32 rows x 16 columns go down columns
+          // row0 .. row0 + 31 of plane 1 — transposed through shared memory so
+          // each lane stores 16 contiguous bytes of one target row (16 byte
+          // stores per lane straight to global cost ~2 ms per n = 8192 product)
+          __syncwarp();  // the previous chunk's reads of xs are done
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int col = col0 + e;
-            if (col < p.N) {
-              uint32_t b = (packed[e >> 2] >> (8 * (e & 3))) & 0xFFu;
-              b = ((b ^ nmask) - nmask) & 0xFFu;  // two's-complement negation when skew
-              tdst[(size_t)col * p.out_pitch] = (int8_t)b;
+          for (int e = 0; e < 16; ++e) xs[e * 32 + lane] = (int8_t)(p.herm < 0 ? -r[e] : r[e]);
+          __syncwarp();
+          const uint4 tv = *reinterpret_cast<const uint4*>(xs + (lane >> 1) * 32 + (lane & 1) * 16);
+          const int tcol = col0 + (lane >> 1), trow = row0 + (lane & 1) * 16;
+          if (tcol < p.N && trow < p.M) {
+            int8_t* tdst = out + (size_t)l * p.out_mod + p.out_plane + (size_t)tcol * p.out_pitch + trow;
+            if (trow + 16 <= p.M) {
+              *reinterpret_cast<uint4*>(tdst) = tv;
+            } else {
+              const uint32_t w[4] = {tv.x, tv.y, tv.z, tv.w};
+              for (int e = 0; e < 16 && trow + e < p.M; ++e) tdst[e] = (int8_t)((w[e >> 2] >> (8 * (e & 3))) & 0xFF);
             }
           }
         }
@@ -709,9 +725,10 @@ int gemm_launch(int M, int N, int K, int nmod, const int* moduli, const void* a,
   // wide units (N = 512) for the 2-SM real products: 18-20 % faster at
   // n = K = 8192 (tools/oz_wide_ab.py, interleaved A/B), but the epilogue of a
   // wide unit is not overlapped with MMAs, so short K (15-22 % slower at 2048)
-  // and the Hermitian products' transposed-write epilogue (9 % slower) stay
-  // narrow.  SR_OZ_WIDE=0 / 1 forces either.
-  bool wide = two && real && herm == 0 && K >= 4096;
+  // stays narrow.  Hermitian products: wide since their transposed write is
+  // staged through shared memory (7.6-8.1 vs 8.8-9.0 ms narrow at n = 8192).
+  // SR_OZ_WIDE=0 / 1 forces either.
+  bool wide = two && real && K >= 4096;
   const char* wide_env = getenv("SR_OZ_WIDE");
   if (wide_env && *wide_env && strcmp(wide_env, "auto") != 0) wide = two && real && atoi(wide_env) != 0;
   p.wide = wide ? 1 : 0;
@@ -743,7 +760,7 @@ int gemm_launch(int M, int N, int K, int nmod, const int* moduli, const void* a,
   if (make_map(&mb, b, K, N, b_planes, nmod, b_kpitch, two ? TN : (real ? 2 * TN : TN) / cm,
                (cm == 1 && !two && !gauss) ? b_planes : 1) != SR_OK)
     return sr_set_cuda_error(cudaErrorInvalidValue, "cuTensorMapEncodeTiled(B)");
-  const size_t smem = 1024 + (size_t)SMEM_RING + SMEM_TAIL;
+  const size_t smem = 1024 + (size_t)SMEM_RING + SMEM_TAIL + (herm ? (size_t)MAX_EPI_WARPS * XPOSE_WARP_BYTES : 0);
   // one zeroed unit counter per launch (a pool, so launches on different
   // streams never share one)
   constexpr int NCOUNTERS = 256;

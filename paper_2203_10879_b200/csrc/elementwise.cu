@@ -67,9 +67,8 @@ __global__ void split_lp_kernel(int rows, int cols, int col0, const double* __re
                                 float2* __restrict__ e_lp, long long ld_lp, double* partials, unsigned int* counter,
                                 double* out, int squared) {
   double acc = 0.0;
-  const long long total = (long long)rows * cols;
-  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    int i = (int)(idx / cols), j = (int)(idx % cols);
+    for (GridIdx g(rows, cols); g.ok(); g.next()) {
+    const int i = g.i, j = g.j;
     double re = tr[(size_t)i * ldt + j], im = ti[(size_t)i * ldt + j];
     float2 v = make_float2((float)re, (float)im);
     float2 z = make_float2(0.f, 0.f);
@@ -88,9 +87,8 @@ __global__ void split_lp_kernel(int rows, int cols, int col0, const double* __re
 __global__ void fro_norm_kernel(int m, int n, const double* __restrict__ re, const double* __restrict__ im,
                                 long long ld, double* partials, unsigned int* counter, double* out) {
   double acc = 0.0;
-  const long long total = (long long)m * n;
-  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    int i = (int)(idx / n), j = (int)(idx % n);
+    for (GridIdx g(m, n); g.ok(); g.next()) {
+    const int i = g.i, j = g.j;
     double a = re[(size_t)i * ld + j];
     acc += a * a;
     if (im) {
@@ -107,9 +105,8 @@ __global__ void fro_norm_kernel(int m, int n, const double* __restrict__ re, con
 __global__ void striu_norm_kernel(int n, const double* __restrict__ re, const double* __restrict__ im, long long ld,
                                   double* partials, unsigned int* counter, double* out) {
   double acc = 0.0;
-  const long long total = (long long)n * n;
-  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    const int i = (int)(idx / n), j = (int)(idx % n);
+    for (GridIdx g(n, n); g.ok(); g.next()) {
+    const int i = g.i, j = g.j;
     if (j > i) {
       const double a = re[(size_t)i * ld + j], b = im ? im[(size_t)i * ld + j] : 0.0;
       acc += a * a + b * b;
@@ -127,9 +124,8 @@ __global__ void diag_correction_kernel(int n, const C* __restrict__ t, const C* 
                                        C* __restrict__ l, R clip, unsigned long long* clipped, int* flags) {
   unsigned int nclip = 0;
   bool sep = false, bad = false;
-  const long long total = (long long)n * n;
-  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    const int i = (int)(idx / n), j = (int)(idx % n);
+    for (GridIdx g(n, n); g.ok(); g.next()) {
+    const int i = g.i, j = g.j;
     C v;
     v.x = 0;
     v.y = 0;
@@ -159,9 +155,8 @@ __global__ void diag_correction_kernel(int n, const C* __restrict__ t, const C* 
 
 __global__ void downcast_kernel(int m, int n, const double* __restrict__ re, const double* __restrict__ im,
                                 long long ld, float2* __restrict__ out, long long ldo) {
-  const long long total = (long long)m * n;
-  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    int i = (int)(idx / n), j = (int)(idx % n);
+    for (GridIdx g(m, n); g.ok(); g.next()) {
+    const int i = g.i, j = g.j;
     out[(size_t)i * ldo + j] = make_float2((float)re[(size_t)i * ld + j], (float)im[(size_t)i * ld + j]);
   }
 }
@@ -170,9 +165,8 @@ __global__ void skew_kernel(int n, const float2* __restrict__ l, long long ld, f
                             double* partials, unsigned int* counter, double* out) {
   double acc = 0.0;
   bool bad = false;
-  const long long total = (long long)n * n;
-  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    int i = (int)(idx / n), j = (int)(idx % n);
+    for (GridIdx g(n, n); g.ok(); g.next()) {
+    const int i = g.i, j = g.j;
     float2 a = l[(size_t)i * ld + j], b = l[(size_t)j * ld + i];
     // w = l - conj(l^T), in lp (complex64) like l - l.conj().T at refine.py:296
     float2 v = make_float2(a.x - b.x, a.y + b.y);
@@ -189,9 +183,8 @@ __global__ void sigma_merged_kernel(int rows, int n, const float2* __restrict__ 
                                     const float2* __restrict__ w2, const float2* __restrict__ w3,
                                     const float2* __restrict__ w2y, const float2* __restrict__ w2yw, long long ldl,
                                     double* __restrict__ sr, double* __restrict__ si, long long lds, double eye) {
-  const long long total = (long long)rows * n;
-  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    int i = (int)(idx / n), j = (int)(idx % n);
+    for (GridIdx g(rows, n); g.ok(); g.next()) {
+    const int i = g.i, j = g.j;
     size_t o = (size_t)i * ldl + j;
     float2 wv = w[o];
     // ((((2I + 2W) - Y) - YW) + W^2) + W^3, left to right (orthogonal.py:191-195)
@@ -223,18 +216,16 @@ __global__ void sigma_merged_kernel(int rows, int n, const float2* __restrict__ 
 
 __global__ void sigma_ns_kernel(int n, const double* __restrict__ gr, const double* __restrict__ gi, long long ldg,
                                 double* __restrict__ sr, double* __restrict__ si, long long lds) {
-  const long long total = (long long)n * n;
-  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    int i = (int)(idx / n), j = (int)(idx % n);
+    for (GridIdx g(n, n); g.ok(); g.next()) {
+    const int i = g.i, j = g.j;
     sr[(size_t)i * lds + j] = (i == j ? 3.0 : 0.0) - gr[(size_t)i * ldg + j];
     si[(size_t)i * lds + j] = -gi[(size_t)i * ldg + j];
   }
 }
 
 __global__ void triu_kernel(int n, double* re, double* im, long long ld) {
-  const long long total = (long long)n * n;
-  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    int i = (int)(idx / n), j = (int)(idx % n);
+    for (GridIdx g(n, n); g.ok(); g.next()) {
+    const int i = g.i, j = g.j;
     if (i > j) {
       re[(size_t)i * ld + j] = 0.0;
       im[(size_t)i * ld + j] = 0.0;
@@ -250,9 +241,8 @@ __global__ void split_lp_c128_kernel(int n, const double* __restrict__ tr, const
                                      long long ldt, double2* __restrict__ t_lp, double2* __restrict__ e_lp,
                                      long long ld_lp, double* partials, unsigned int* counter, double* out) {
   double acc = 0.0;
-  const long long total = (long long)n * n;
-  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    const int i = (int)(idx / n), j = (int)(idx % n);
+    for (GridIdx g(n, n); g.ok(); g.next()) {
+    const int i = g.i, j = g.j;
     const double re = tr[(size_t)i * ldt + j], im = ti[(size_t)i * ldt + j];
     const double2 v = make_double2(re, im), z = make_double2(0.0, 0.0);
     if (i > j) {
@@ -271,9 +261,8 @@ __global__ void skew_c128_kernel(int n, const double2* __restrict__ l, long long
                                  int* flags, double* partials, unsigned int* counter, double* out) {
   double acc = 0.0;
   bool bad = false;
-  const long long total = (long long)n * n;
-  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    const int i = (int)(idx / n), j = (int)(idx % n);
+    for (GridIdx g(n, n); g.ok(); g.next()) {
+    const int i = g.i, j = g.j;
     const double2 a = l[(size_t)i * ld + j], b = l[(size_t)j * ld + i];
     const double2 v = make_double2(a.x - b.x, a.y + b.y);  // l - conj(l^T), refine.py:296
     w[(size_t)i * ld + j] = v;
@@ -286,9 +275,8 @@ __global__ void skew_c128_kernel(int n, const double2* __restrict__ l, long long
 
 __global__ void pack_c128_kernel(int m, int n, const double* __restrict__ re, const double* __restrict__ im,
                                  long long ld, double2* __restrict__ out, long long ldo) {
-  const long long total = (long long)m * n;
-  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    const int i = (int)(idx / n), j = (int)(idx % n);
+    for (GridIdx g(m, n); g.ok(); g.next()) {
+    const int i = g.i, j = g.j;
     out[(size_t)i * ldo + j] = make_double2(re[(size_t)i * ld + j], im[(size_t)i * ld + j]);
   }
 }
@@ -325,9 +313,8 @@ __global__ void sigma_merged_dd_kernel(int n, const double2* __restrict__ w, con
                                        long long ldl, double* __restrict__ srh, double* __restrict__ sih,
                                        double* __restrict__ srl, double* __restrict__ sil, long long lds,
                                        double eye) {
-  const long long total = (long long)n * n;
-  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    const int i = (int)(idx / n), j = (int)(idx % n);
+    for (GridIdx g(n, n); g.ok(); g.next()) {
+    const int i = g.i, j = g.j;
     const size_t o = (size_t)i * ldl + j, oy = (size_t)i * ldy + j;
     const double2 wv = w[o];
     double rh = (i == j ? eye : 0.0), rl = 0.0, ih = 0.0, il = 0.0;
@@ -441,9 +428,8 @@ extern "C" int sr_skew_c64(int n, const void* l, long long ld, void* w, double* 
 __global__ void fused_lp_operand_kernel(int n, int cols, const double* __restrict__ yr, const double* __restrict__ yi,
                                         long long ldy, const float2* __restrict__ w, const float2* __restrict__ w2,
                                         long long ldl, float2* __restrict__ x) {
-  const long long total = (long long)n * cols;
-  for (long long idx = (long long)blockIdx.x * RT + threadIdx.x; idx < total; idx += (long long)gridDim.x * RT) {
-    const int i = (int)(idx / cols), j = (int)(idx % cols);
+    for (GridIdx g(n, cols); g.ok(); g.next()) {
+    const int i = g.i, j = g.j;
     const size_t o = (size_t)i * ldl + j, oy = (size_t)i * ldy + j;
     const float2 a = w[o], b = w2[o];
     x[o] = make_float2((float)(yr[oy] - (double)a.x - (double)b.x), (float)(yi[oy] - (double)a.y - (double)b.y));

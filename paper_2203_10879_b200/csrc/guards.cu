@@ -150,10 +150,9 @@ __global__ void power_finish_kernel(int n, double2* __restrict__ v, const double
 __global__ void finite_flag_kernel(int m, int n, const double* __restrict__ re, const double* __restrict__ im,
                                    long long ld, int* flags, int bit) {
   bool bad = false;
-  const long long total = (long long)m * n;
-  for (long long k = blockIdx.x * (long long)PT + threadIdx.x; k < total; k += (long long)gridDim.x * PT) {
-    const long long i = k / n, j = k % n;
-    bad = bad || !isfinite(re[i * ld + j]) || (im && !isfinite(im[i * ld + j]));
+  for (GridIdx g(m, n); g.ok(); g.next()) {
+    const long long o = (long long)g.i * ld + g.j;
+    bad = bad || !isfinite(re[o]) || (im && !isfinite(im[o]));
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, bit);
 }

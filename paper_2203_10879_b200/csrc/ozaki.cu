@@ -604,10 +604,18 @@ __global__ void __launch_bounds__(256, G ? 3 : 1) decode_kernel(const __grid_con
   constexpr bool ONE = G;                    // both Gaussian planes in one pass
   constexpr int CPT = (G && NC > 2) ? 2 : 4;  // columns per thread
   const int ngrp = (p.N + CPT - 1) / CPT;
-  const long long total = (long long)p.M * ngrp;
-  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(idx / ngrp), j0 = (int)(idx % ngrp) * CPT;
+  // idx = i ngrp + jg stepped by the grid stride without a 64-bit division per
+  // entry group (its I2F / MUFU / F2I sequence runs on the narrow XU pipe)
+  const long long start = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const int sq = (int)(stride / ngrp), sr = (int)(stride % ngrp);
+  int i = (int)(start / ngrp), jg = (int)(start % ngrp);
+  for (; i < p.M; i += sq, jg += sr) {
+    if (jg >= ngrp) {
+      jg -= ngrp;
+      if (++i >= p.M) break;
+    }
+    const int j0 = jg * CPT;
     if (p.hermitian && (j0 >> 7) > (i >> 7)) continue;  // upper GEMM tile: mirrored afterwards
     const int rho = p.beta_a - ea[i];
 #pragma unroll 1
@@ -841,13 +849,40 @@ __device__ __forceinline__ double digits_to_chunk(const uint32_t* T) {
 
 // one unit = DTC_TB column tiles of row i; tile b valid when inside the matrix
 // and (Hermitian) inside the lower 128 x 128 GEMM tiles
-__device__ __forceinline__ int unit_mask(const DecodeTcArgs& t, int u, int& i, int& jt0) {
-  i = u / t.units_n;
-  jt0 = (u - i * t.units_n) * DTC_TB;
+__device__ __forceinline__ int unit_mask_at(const DecodeTcArgs& t, int i, int r, int& jt0) {
+  jt0 = r * DTC_TB;
   const int hi = t.herm ? min(t.tiles_n, (i >> 7) + 1) : t.tiles_n;
   const int nv = max(0, min(DTC_TB, hi - jt0));
   return (1 << nv) - 1;
 }
+
+// a CTA's units u = blockIdx.x + k grid as (row i, unit r in the row), stepped
+// without integer divisions (their I2F / MUFU.RCP / F2I sequences ran on the
+// narrow XU pipe of every epilogue warp: 12 % XU issue in the decode)
+struct UnitIt {
+  int u, i, r;
+  int gq, gr;  // grid = gq units_n + gr
+  __device__ __forceinline__ void init(const DecodeTcArgs& t, int u0, int grid) {
+    u = u0;
+    i = u0 / t.units_n;
+    r = u0 - i * t.units_n;
+    gq = grid / t.units_n;
+    gr = grid - gq * t.units_n;
+  }
+  __device__ __forceinline__ void step(const DecodeTcArgs& t, int grid) {
+    u += grid;
+    i += gq;
+    r += gr;
+    if (r >= t.units_n) {
+      r -= t.units_n;
+      ++i;
+    }
+  }
+  __device__ __forceinline__ int mask(const DecodeTcArgs& t, int& row, int& jt0) const {
+    row = i;
+    return unit_mask_at(t, i, r, jt0);
+  }
+};
 
 // Persistent, warp-specialised, one CTA per SM.  The TMA warp streams units
 // (DTC_TB x 128 output columns of one row: one 4-d box of 2 nmod slot rows per
@@ -913,9 +948,10 @@ __global__ void __launch_bounds__(DTC_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       int k = 0;
-      for (int u = blockIdx.x; u < total; u += grid) {
+      UnitIt it;
+      for (it.init(t, blockIdx.x, grid); it.u < total; it.step(t, grid)) {
         int i, jt0;
-        const int m = unit_mask(t, u, i, jt0);
+        const int m = it.mask(t, i, jt0);
         if (!m) continue;
         const int s = k % DTC_STAGES;
         if (k >= DTC_STAGES) mbar_wait(empty_bar(s), ((k / DTC_STAGES) - 1) & 1);
@@ -933,9 +969,10 @@ __global__ void __launch_bounds__(DTC_THREADS, 1)
       const uint32_t idesc = t.idesc;
       const bool two = t.kmma > 1;
       int k = 0;
-      for (int u = blockIdx.x; u < total; u += grid) {
+      UnitIt it;
+      for (it.init(t, blockIdx.x, grid); it.u < total; it.step(t, grid)) {
         int i, jt0;
-        const int m = unit_mask(t, u, i, jt0);
+        const int m = it.mask(t, i, jt0);
         if (!m) continue;
         const int s = k % DTC_STAGES, g = k % DTC_NG, r = k / DTC_NG;
         mbar_wait(tempty_bar(g), (r & 1) ^ 1);
@@ -964,19 +1001,19 @@ __global__ void __launch_bounds__(DTC_THREADS, 1)
       double xr[DTC_TB], xi[DTC_TB];
     };
     // the unit after u among this group's units (NG live units on)
-    auto next_unit = [&](int u, int steps) {
+    auto next_unit = [&](UnitIt u, int steps) {
       for (int c = 0; c < steps;) {
-        u += grid;
-        if (u >= total) return total;
+        u.step(t, grid);
+        if (u.u >= total) return u;
         int i, jt0;
-        if (unit_mask(t, u, i, jt0)) ++c;
+        if (u.mask(t, i, jt0)) ++c;
       }
       return u;
     };
-    auto prefetch = [&](int u, Pre& r) {
+    auto prefetch = [&](const UnitIt& u, Pre& r) {
       r.m = 0;
-      if (u >= total) return;
-      r.m = unit_mask(t, u, r.i, r.jt0);
+      if (u.u >= total) return;
+      r.m = u.mask(t, r.i, r.jt0);
       r.rho = p.beta_a - __ldg(ea + r.i);
 #pragma unroll
       for (int b = 0; b < DTC_TB; ++b) {
@@ -991,10 +1028,11 @@ __global__ void __launch_bounds__(DTC_THREADS, 1)
         }
       }
     };
-    int u = blockIdx.x;
+    UnitIt u;
+    u.init(t, blockIdx.x, grid);
     {
       int i, jt0;
-      if (u < total && !unit_mask(t, u, i, jt0)) u = next_unit(u, 1);
+      if (u.u < total && !u.mask(t, i, jt0)) u = next_unit(u, 1);
     }
     u = next_unit(u, g);  // this group's first unit
     // two operand sets, software-pipelined: the loads for a unit are issued a
@@ -1051,15 +1089,15 @@ __global__ void __launch_bounds__(DTC_THREADS, 1)
     };
     Pre A, B;
     prefetch(u, A);
-    int ub = next_unit(u, DTC_NG);
+    UnitIt ub = next_unit(u, DTC_NG);
     prefetch(ub, B);
-    for (int r = 0; u < total; r += 2) {
+    for (int r = 0; u.u < total; r += 2) {
       process(A, r);
-      const int ua = next_unit(ub, DTC_NG);
+      const UnitIt ua = next_unit(ub, DTC_NG);
       prefetch(ua, A);
-      if (ub >= total) break;
+      if (ub.u >= total) break;
       process(B, r + 1);
-      const int ub2 = next_unit(ua, DTC_NG);
+      const UnitIt ub2 = next_unit(ua, DTC_NG);
       prefetch(ub2, B);
       u = ua;
       ub = ub2;

@@ -90,3 +90,33 @@ __device__ __forceinline__ void cp_async_wait() {
   do {                                    \
   } while (0)
 #endif
+
+// (row, column) of a grid-stride loop over a rows x cols matrix, stepped
+// without a 64-bit division per element (its I2F / MUFU / F2I sequence runs
+// on the narrow XU pipe and made the lighter passes issue-bound); every thread
+// visits the same entries in the same order as a flat idx loop would
+struct GridIdx {
+  int i, j, rows, cols, sq, sr;
+  __device__ __forceinline__ GridIdx(int rows_, int cols_) : rows(rows_), cols(cols_) {
+    const long long start = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    if (cols <= 0) {
+      i = rows;
+      j = sq = sr = 0;
+      return;
+    }
+    i = (int)(start / cols);
+    j = (int)(start % cols);
+    sq = (int)(stride / cols);
+    sr = (int)(stride % cols);
+  }
+  __device__ __forceinline__ bool ok() const { return i < rows; }
+  __device__ __forceinline__ void next() {
+    i += sq;
+    j += sr;
+    if (j >= cols) {
+      j -= cols;
+      ++i;
+    }
+  }
+};

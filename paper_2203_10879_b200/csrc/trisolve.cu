@@ -640,10 +640,8 @@ __global__ void __launch_bounds__(FT) far_kernel(FarArgs p, const C* __restrict_
 template <typename C>
 __global__ void init_kernel(int n, const C* __restrict__ E, C* __restrict__ Rn, C* __restrict__ Rf,
                             C* __restrict__ L, long long ld) {
-  const long long total = (long long)n * n;
-  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(idx / n), j = (int)(idx % n);
+  for (GridIdx g(n, n); g.ok(); g.next()) {
+    const int i = g.i, j = g.j;
     const size_t o = (size_t)i * ld + j;
     C r = czero<C>();
     if (i > j) {

@@ -734,20 +734,11 @@ int enqueue(SolveCtx& c, int n, const C* t, const C* e, long long ld, C* l, doub
   constexpr bool kC64 = std::is_same<C, float2>::value;
   const bool use_tc = kC64 && (ld % 2) == 0 && !getenv("SR_SOLVE_SIMT_FAR");
   FarTcPlan plan;
-  if constexpr (kC64) {
-    if (use_tc) {
-      const int rc = far_tc_prepare(&plan, n, t, ld, (char*)ws + 2 * rb, origin);
-      if (rc != SR_OK) return rc;
-    }
-  }
   {
     const long long total = (long long)n * n;
     const long long blocks = (total + 255) / 256;
     const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
     init_kernel<C><<<grid, 256, 0, origin>>>(n, e, Rn, Rf, l, ld);
-    SR_LAUNCH_CHECK();
-    dim3 b(32, 8), g(sr_ceil_div(n, 32), sr_ceil_div(n, 8));
-    separation_kernel<C><<<g, b, 0, origin>>>(n, t, ld, d_flags);
     SR_LAUNCH_CHECK();
   }
   const size_t smem_solve = sizeof(C) * (9 * NB * LD + NB * NB);
@@ -759,6 +750,17 @@ int enqueue(SolveCtx& c, int n, const C* t, const C* e, long long ld, C* l, doub
   if (s_solve != origin) SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, c.ev_in, 0));
   SR_CUDA_CHECK(cudaStreamWaitEvent(s_near, c.ev_in, 0));
   SR_CUDA_CHECK(cudaStreamWaitEvent(s_far, c.ev_in, 0));
+  // off the critical path: the far updates' T forms on the far stream (first
+  // read by the far launches of batch 0, after four levels); the separation
+  // scan (its flag is read after the join) on the far stream beside the last
+  // levels, which have no far targets left and leave most SMs idle
+  if constexpr (kC64) {
+    if (use_tc) {
+      const int rc = far_tc_prepare(&plan, n, t, ld, (char*)ws + 2 * rb, s_far);
+      if (rc != SR_OK) return rc;
+    }
+  }
+  const int sep_level = N > 8 ? N - 8 : 0;
   const typename Real<C>::T cl = (typename Real<C>::T)clip;
   for (int lev = 0; lev < N; ++lev) {
     // SOLVE(lev): after NEAR(lev-1) (ev_u) and FAR(lev/4 - 1 - FAR_LA)
@@ -782,6 +784,11 @@ int enqueue(SolveCtx& c, int n, const C* t, const C* e, long long ld, C* l, doub
     }
     SR_CUDA_CHECK(cudaEventRecord(c.ev_s, s_solve));
     SR_CUDA_CHECK(cudaEventRecord(c.ev_u, s_near));
+    if (lev == sep_level) {
+      dim3 b(32, 8), g(sr_ceil_div(n, 32), sr_ceil_div(n, 8));
+      separation_kernel<C><<<g, b, 0, s_far>>>(n, t, ld, d_flags);
+      SR_LAUNCH_CHECK();
+    }
     // FAR(b) once the last level of batch b is solved, if any tile sits on a far target level
 #ifndef SR_DIAG_NO_FAR  // timing diagnostic only (tools/solve_bench.py): wrong results without it
     if (lev % BW == BW - 1) {

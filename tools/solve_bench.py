@@ -33,6 +33,16 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / reps
 print("trisolve n=%d: %.2f ms per solve (%.1f GFLOP/s useful, n^3/3 cmac)" % (n, ms, 8 * n ** 3 / 3 / ms / 1e6))
+if len(sys.argv) > 3:  # every solve from an idle GPU (as inside a refinement): event and host times
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        h0 = time.perf_counter()
+        e0.record()
+        solve_lp_device(t, e, l, n, None, work, st)
+        h1 = time.perf_counter()
+        e1.record()
+        torch.cuda.synchronize()
+        print("  isolated solve: %.2f ms on the device, host enqueue %.2f ms" % (e0.elapsed_time(e1), (h1 - h0) * 1e3))
 lv = l[:, :n]
 res = torch.linalg.matrix_norm(torch.tril(t[:, :n].to(torch.complex128) @ lv.to(torch.complex128)
                                - lv.to(torch.complex128) @ t[:, :n].to(torch.complex128), -1)

@@ -115,7 +115,8 @@ int sr_skew_c64(int n, const void* l, long long ld, void* w, double* d_norm_w, i
    orthogonal.py:191-201), planar FP64, summed left to right:
    S = ((((2I + 2W) - Y) - YW) + W^2) + W^3 [+ W^2 Y + W^2 Y W].
    w, yw, w2, w3 (and optional w2y, w2yw, NULL to skip) are complex64;
-   w2 = w3 = NULL: yw holds the fused product YW - W^2 - W^3.
+   w2 = w3 = NULL: yw holds the fused product YW - W^2 - W^3 (yw = NULL too:
+   that product lies below the update's error budget and is left out).
    with_identity = 0 drops the 2I term (S' = S - 2I, used by the Ozaki path,
    which forms Q S / 2 = Q + Q S' / 2 exactly).  n rows x cols columns (a
    column block of S' in the sharded driver; cols == n with the identity). */
@@ -127,7 +128,8 @@ int sr_sigma_merged_f64(int n, int cols, const void* w, const double* y_re, cons
 /* X = Y - W - W^2 (complex64 out; Y planar FP64, W and W^2 complex64): the A
    operand of the fused lp product X W = YW - W^2 - W^3, passed as `yw` to
    sr_sigma_merged_f64 with w2 = w3 = NULL (merged_update, orthogonal.py:191-195,
-   with two lp products instead of three). */
+   with two lp products instead of three).  w2 = NULL: X = Y - W (the W^3
+   term lies below the update's error budget). */
 int sr_fused_lp_operand_c64(int n, const double* y_re, const double* y_im, long long ldy, const void* w,
                             const void* w2, long long ld_lp, void* x, void* stream);
 

@@ -192,9 +192,11 @@ __global__ void sigma_merged_kernel(int rows, int n, const float2* __restrict__ 
     double im = 2.0 * (double)wv.y;
     re = re - yr[(size_t)i * ldy + j];
     im = im - yi[(size_t)i * ldy + j];
-    float2 a = yw[o];
-    re = re - (double)a.x;
-    im = im - (double)a.y;
+    if (yw) {  // null yw (fused form only): X W below the update's error budget
+      float2 a = yw[o];
+      re = re - (double)a.x;
+      im = im - (double)a.y;
+    }
     if (w2) {  // null w2 / w3: the fused form, yw already holds YW - W^2 - W^3
       float2 b = w2[o], c = w3[o];
       re = re + (double)b.x;
@@ -431,14 +433,14 @@ __global__ void fused_lp_operand_kernel(int n, int cols, const double* __restric
     for (GridIdx g(n, cols); g.ok(); g.next()) {
     const int i = g.i, j = g.j;
     const size_t o = (size_t)i * ldl + j, oy = (size_t)i * ldy + j;
-    const float2 a = w[o], b = w2[o];
+    const float2 a = w[o], b = w2 ? w2[o] : make_float2(0.f, 0.f);  // null w2: W^2 below the update's error budget
     x[o] = make_float2((float)(yr[oy] - (double)a.x - (double)b.x), (float)(yi[oy] - (double)a.y - (double)b.y));
   }
 }
 
 extern "C" int sr_fused_lp_operand_c64(int n, const double* y_re, const double* y_im, long long ldy, const void* w,
                                        const void* w2, long long ld_lp, void* x, void* stream) {
-  if (n < 0 || !y_re || !y_im || !w || !w2 || !x) return SR_EINVAL;
+  if (n < 0 || !y_re || !y_im || !w || !x) return SR_EINVAL;
   if (n == 0) return SR_OK;
   fused_lp_operand_kernel<<<ew_grid((long long)n * n), RT, 0, (cudaStream_t)stream>>>(
       n, n, y_re, y_im, ldy, (const float2*)w, (const float2*)w2, ld_lp, (float2*)x);
@@ -463,7 +465,7 @@ extern "C" int sr_split_lp_block_c64(int rows, int cols, int col0, const double*
 extern "C" int sr_fused_lp_operand_block_c64(int rows, int cols, const double* y_re, const double* y_im,
                                              long long ldy, const void* w, const void* w2, long long ld_lp, void* x,
                                              void* stream) {
-  if (rows < 0 || cols < 0 || !y_re || !y_im || !w || !w2 || !x) return SR_EINVAL;
+  if (rows < 0 || cols < 0 || !y_re || !y_im || !w || !x) return SR_EINVAL;
   if ((long long)rows * cols == 0) return SR_OK;
   fused_lp_operand_kernel<<<ew_grid((long long)rows * cols), RT, 0, (cudaStream_t)stream>>>(
       rows, cols, y_re, y_im, ldy, (const float2*)w, (const float2*)w2, ld_lp, (float2*)x);
@@ -478,6 +480,7 @@ extern "C" int sr_sigma_merged_f64(int n, int cols, const void* w, const double*
   if (n < 0 || cols < 0 || (w2y == nullptr) != (w2yw == nullptr) || (w2 == nullptr) != (w3 == nullptr))
     return SR_EINVAL;
   if (!w2 && w2y) return SR_EINVAL;  // the fused form has no restore_full_sigma terms
+  if (!yw && w2) return SR_EINVAL;   // only the fused form may drop its lp term
   if (with_identity && cols != n) return SR_EINVAL;
   if ((long long)n * cols == 0) return SR_OK;
   sigma_merged_kernel<<<ew_grid((long long)n * cols), RT, 0, (cudaStream_t)stream>>>(

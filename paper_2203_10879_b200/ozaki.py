@@ -300,6 +300,16 @@ def lp_product_beta(scale, n, hi=LP_BETA, lo=LP_MIN_BETA, slack_bits=26):
     return max(lo, min(hi, b))
 
 
+def lp_product_negligible(scale, slack_bits=26):
+    """True when an lp product of the fused update is smaller than the error
+    lp_product_beta allows it (2^-slack_bits ||W||_F): with scale the norm
+    bound of the term it contributes, in units of ||W||_F — ||W||_F^2 for
+    W^2, which enters S' only through X W as the W^3 term; ||X||_F for X W —
+    leaving the product out changes S' by less than computing it at the
+    adaptive precision may."""
+    return math.isfinite(scale) and 0.0 <= scale <= 2.0 ** -slack_bits
+
+
 def correction_beta(bound, n, hi=HP_BETA, lo=LP_BETA, unit_bits=53):
     """Operand precision for a correction product X S whose result is added to
     an O(1) matrix before one rounding (Q + Q S'/2, Q^ - Q^ (G - I)/2):

@@ -15,6 +15,8 @@ with one rounding instead of a K-long accumulation).  DmmaProducts runs
 them on the FP64 DMMA pipe (csrc/zgemm_f64.cu) and the FP32 SIMT lp GEMM
 (csrc/cgemm_c64.cu); it is kept as the native-FP64 comparison point.
 """
+import os
+
 import torch
 
 from . import _lib, ozaki
@@ -26,16 +28,17 @@ def _stream():
     return torch.cuda.current_stream().cuda_stream
 
 
-def _sigma(ws, restore_full_sigma, with_identity, fused=False):
+def _sigma(ws, restore_full_sigma, with_identity, fused=False, drop_lp=False):
     """S (or S' = S - 2I) from W, Y and the lp products; fused: ws.yw holds
-    X W = YW - W^2 - W^3 (X = Y - W - W^2) and W^2, W^3 are not separate."""
+    X W = YW - W^2 - W^3 (X = Y - W - W^2) and W^2, W^3 are not separate;
+    drop_lp (fused only): that product is negligible, S' = 2W - Y."""
     n = ws.n
     w2y = w2yw = None
     if restore_full_sigma:
         w2y, w2yw = ws.w2y.data_ptr(), ws.w2yw.data_ptr()
     w2, w3 = (None, None) if fused else (ws.w2.data_ptr(), ws.w3.data_ptr())
     _lib.call("sr_sigma_merged_f64", n, n, ws.w_lp.data_ptr(), ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld,
-              ws.yw.data_ptr(), w2, w3, w2y, w2yw, ws.w_lp.shape[1],
+              None if (fused and drop_lp) else ws.yw.data_ptr(), w2, w3, w2y, w2yw, ws.w_lp.shape[1],
               ws.sigma.re_ptr(), ws.sigma.im_ptr(), ws.sigma.ld, 1 if with_identity else 0, _stream())
 
 
@@ -187,28 +190,39 @@ class OzakiProducts:
         ws, hp, lp, n = self.ws, self.hp, self.lp, self.ws.n
         if not restore_full_sigma:
             p_w2, p_xw = self._lp_plans(norm_y, norm_w)
-            # two lp products instead of three: X W = YW - W^2 - W^3 with X = Y - W - W^2
-            if self.gauss:
-                # W is exactly skew-Hermitian (sr_skew_c64): column j of W is -conj(row j),
-                # with the same scale, so W's B operand is its A operand with the
-                # Gaussian planes swapped and negated — one encoding of W, the
-                # sign folded into the decode (alpha = -1)
-                ozaki.encode(ws.w_lp, n, n, "a", p_w2, out=self.lb)       # W, A role
-                self._lp_with(p_w2, self.lb, ozaki.conj_view(self.lb), ws.w2, hermitian=True, alpha=-1.0)  # W^2
+            # a product below its own error budget is not formed (ozaki.lp_product_negligible):
+            # W^2 only feeds the W^3 term of X W; X W itself is at most ||X|| ||W||
+            skip_w2, skip_xw = lp_skips(norm_y, norm_w)
+            if skip_xw:
+                _sigma(ws, False, False, fused=True, drop_lp=True)       # S' = 2W - Y
             else:
-                ozaki.encode(ws.w_lp, n, n, "b", p_w2, out=self.lb)       # W, B role
-                ozaki.encode(ws.w_lp, n, n, "a", p_w2, out=self.la)
-                self._lp_with(p_w2, self.la, self.lb, ws.w2, hermitian=self.w_skew)  # W^2 (W skew-Hermitian)
-            _lib.call("sr_fused_lp_operand_c64", n, ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld, ws.w_lp.data_ptr(),
-                      ws.w2.data_ptr(), ws.w_lp.shape[1], ws.y_lp.data_ptr(), _stream())
-            if p_xw is not p_w2:
-                ozaki.encode(ws.w_lp, n, n, "a" if self.gauss else "b", p_xw, out=self.lb)
-            ozaki.encode(ws.y_lp, n, n, "a", p_xw, out=self.la)
-            if self.gauss:
-                self._lp_with(p_xw, self.la, ozaki.conj_view(self.lb), ws.yw, alpha=-1.0)  # X W
-            else:
-                self._lp_with(p_xw, self.la, self.lb, ws.yw)             # X W
-            _sigma(ws, False, False, fused=True)                         # S' = S - 2I
+                # two lp products instead of three: X W = YW - W^2 - W^3 with X = Y - W - W^2
+                w_plan = None  # the plan self.lb holds W's encoding for
+                if skip_w2:
+                    pass
+                elif self.gauss:
+                    # W is exactly skew-Hermitian (sr_skew_c64): column j of W is -conj(row j),
+                    # with the same scale, so W's B operand is its A operand with the
+                    # Gaussian planes swapped and negated — one encoding of W, the
+                    # sign folded into the decode (alpha = -1)
+                    ozaki.encode(ws.w_lp, n, n, "a", p_w2, out=self.lb)       # W, A role
+                    self._lp_with(p_w2, self.lb, ozaki.conj_view(self.lb), ws.w2, hermitian=True, alpha=-1.0)  # W^2
+                    w_plan = p_w2
+                else:
+                    ozaki.encode(ws.w_lp, n, n, "b", p_w2, out=self.lb)       # W, B role
+                    ozaki.encode(ws.w_lp, n, n, "a", p_w2, out=self.la)
+                    self._lp_with(p_w2, self.la, self.lb, ws.w2, hermitian=self.w_skew)  # W^2 (W skew-Hermitian)
+                    w_plan = p_w2
+                _lib.call("sr_fused_lp_operand_c64", n, ws.y.re_ptr(), ws.y.im_ptr(), ws.y.ld, ws.w_lp.data_ptr(),
+                          None if skip_w2 else ws.w2.data_ptr(), ws.w_lp.shape[1], ws.y_lp.data_ptr(), _stream())
+                if p_xw is not w_plan:
+                    ozaki.encode(ws.w_lp, n, n, "a" if self.gauss else "b", p_xw, out=self.lb)
+                ozaki.encode(ws.y_lp, n, n, "a", p_xw, out=self.la)
+                if self.gauss:
+                    self._lp_with(p_xw, self.la, ozaki.conj_view(self.lb), ws.yw, alpha=-1.0)  # X W
+                else:
+                    self._lp_with(p_xw, self.la, self.lb, ws.yw)             # X W
+                _sigma(ws, False, False, fused=True)                         # S' = S - 2I
         else:
             ozaki.encode(ws.w_lp, n, n, "b", lp, out=self.lb)            # W, B role (all lp products)
             ozaki.encode(ws.w_lp, n, n, "a", lp, out=self.la)
@@ -243,6 +257,16 @@ def lp_plans(n, norm_y, norm_w, gauss, default):
     b_w2 = ozaki.lp_product_beta(norm_w * norm_w, n)      # W^2 error x ||W|| vs u ||W||
     b_xw = ozaki.lp_product_beta(nx, n)                   # (X W) error vs u ||W||
     return ozaki.plan(n, b_w2, b_w2, gauss), ozaki.plan(n, b_xw, b_xw, gauss)
+
+
+def lp_skips(norm_y, norm_w):
+    """(skip W^2, skip X W) for the fused update: the lp products that lie
+    below their own error budget (ozaki.lp_product_negligible, the scales of
+    lp_plans).  SR_LP_SKIP=0 forms every product (A/B runs)."""
+    if norm_y is None or norm_w is None or not (norm_w > 0.0) or os.environ.get("SR_LP_SKIP") == "0":
+        return False, False
+    nx = norm_y + norm_w + norm_w * norm_w
+    return ozaki.lp_product_negligible(norm_w * norm_w), ozaki.lp_product_negligible(nx)
 
 
 def sigma_prime_bound(norm_y, norm_w, restore_full_sigma):

@@ -258,19 +258,29 @@ class OzakiShardBackend:
         Q_new_J = Q_J + Q S'_J / 2 (orthogonal.py:172-201, fused form)."""
         n, w, j0, j1, st = self.n, self.w, self.j0, self.j1, _stream()
         p_w2, p_xw = products.lp_plans(n, norm_y, norm_w, True, self.lp)
+        # lp products below their own error budget are not formed (products.lp_skips;
+        # the norms are all-reduced, so every rank decides alike)
+        skip_w2, skip_xw = products.lp_skips(norm_y, norm_w)
         self.wj[:, :w].copy_(self.w_lp[:, j0:j1])
-        ozaki.encode(self.w_lp, n, n, "a", p_w2, out=self.la)         # W (replicated), A role
-        ozaki.encode(self.wj, n, w, "b", p_w2, out=self.lb)           # W_J, B role
-        self._prod(p_w2, self.la, self.lb, self.lres, self.w2j)       # W^2_J
-        _lib.call("sr_fused_lp_operand_block_c64", n, w, self.yj.re_ptr(), self.yj.im_ptr(), self.yj.ld,
-                  self.wj.data_ptr(), self.w2j.data_ptr(), self.wj.shape[1], self.xj.data_ptr(), st)
-        self._gather_lp(self.xj, self.x_lp)                          # X = Y - W - W^2 (full)
-        if p_xw is not p_w2:
-            ozaki.encode(self.wj, n, w, "b", p_xw, out=self.lb)
-        ozaki.encode(self.x_lp, n, n, "a", p_xw, out=self.la)
-        self._prod(p_xw, self.la, self.lb, self.lres, self.xwj)       # (X W)_J = (YW - W^2 - W^3)_J
+        xw = None
+        if not skip_xw:
+            w_plan = None
+            if not skip_w2:
+                ozaki.encode(self.w_lp, n, n, "a", p_w2, out=self.la)     # W (replicated), A role
+                ozaki.encode(self.wj, n, w, "b", p_w2, out=self.lb)       # W_J, B role
+                self._prod(p_w2, self.la, self.lb, self.lres, self.w2j)   # W^2_J
+                w_plan = p_w2
+            _lib.call("sr_fused_lp_operand_block_c64", n, w, self.yj.re_ptr(), self.yj.im_ptr(), self.yj.ld,
+                      self.wj.data_ptr(), None if skip_w2 else self.w2j.data_ptr(), self.wj.shape[1],
+                      self.xj.data_ptr(), st)
+            self._gather_lp(self.xj, self.x_lp)                      # X = Y - W - W^2 (full)
+            if p_xw is not w_plan:
+                ozaki.encode(self.wj, n, w, "b", p_xw, out=self.lb)
+            ozaki.encode(self.x_lp, n, n, "a", p_xw, out=self.la)
+            self._prod(p_xw, self.la, self.lb, self.lres, self.xwj)   # (X W)_J = (YW - W^2 - W^3)_J
+            xw = self.xwj.data_ptr()
         _lib.call("sr_sigma_merged_f64", n, w, self.wj.data_ptr(), self.yj.re_ptr(), self.yj.im_ptr(), self.yj.ld,
-                  self.xwj.data_ptr(), None, None, None, None, self.wj.shape[1], self.sj.re_ptr(), self.sj.im_ptr(),
+                  xw, None, None, None, None, self.wj.shape[1], self.sj.re_ptr(), self.sj.im_ptr(),
                   self.sj.ld, 0, st)                                  # S'_J = 2 W_J - Y_J - (X W)_J
         bound = products.sigma_prime_bound(norm_y, norm_w, False)
         beta = ozaki.correction_beta(bound, n)

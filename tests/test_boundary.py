@@ -88,3 +88,22 @@ def test_ddschur_import_shim_maps_the_hot_path():
     env = dict(os.environ, PYTHONPATH=os.pathsep.join([os.path.join(REPO, "tools", "ddschur_shim"), REPO]))
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr
+
+
+def test_negligible_lp_products_rule(monkeypatch):
+    """The fused update leaves out an lp product only when its norm bound is
+    below the error the adaptive plans allow it (2^-26 ||W||_F): W^2 (which
+    only feeds the W^3 term) from ||W||_F^2 <= 2^-26, X W from ||X||_F <= 2^-26."""
+    from paper_2203_10879_b200 import ozaki, products
+
+    assert ozaki.lp_product_negligible(2.0 ** -26) and not ozaki.lp_product_negligible(2.0 ** -25.9)
+    assert not ozaki.lp_product_negligible(float("nan")) and not ozaki.lp_product_negligible(float("inf"))
+    monkeypatch.delenv("SR_LP_SKIP", raising=False)
+    assert products.lp_skips(None, 1e-9) == (False, False)           # no norms (merged_update export): every product
+    assert products.lp_skips(1e-7, 0.0) == (False, False)
+    assert products.lp_skips(1e-7, 1e-3) == (False, False)           # first updates: W^2 matters
+    assert products.lp_skips(1e-10, 1e-5) == (True, False)           # ||W||^2 = 1e-10 < 2^-26, ||X|| ~ 1e-5 is not
+    assert products.lp_skips(1e-13, 2e-9) == (True, True)            # last update of a converging run
+    assert products.lp_skips(1e-6, 2e-9) == (True, False)            # a large orthogonality defect keeps X W
+    monkeypatch.setenv("SR_LP_SKIP", "0")
+    assert products.lp_skips(1e-13, 2e-9) == (False, False)

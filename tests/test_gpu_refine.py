@@ -242,3 +242,26 @@ def test_host_inputs_fortran_order():
         assert torch.equal(p_c.q.cpu(), p_f.q.cpu()) and torch.equal(p_c.t.cpu(), p_f.t.cpu())
         assert torch.equal(p_c.q.cpu(), p_t.q.cpu())
         assert r_c.residual_history == r_f.residual_history == r_t.residual_history
+
+
+def test_negligible_lp_products_do_not_change_the_run(monkeypatch):
+    """products.lp_skips leaves out lp products below their own error budget
+    (the late updates' W^2 and X W); the run forming every product
+    (SR_LP_SKIP=0) has the same status, iterations and residual history to
+    measurement noise, and the same Q to a few units of roundoff."""
+    n = 300
+    a = inputs.gaussian_complex(n, 11)
+    q = inputs.schur_vectors(a).astype(np.complex128)
+    cfg = RefineConfig(precision="fp64", tol_factor=10.0 / n, max_iters=10)
+    monkeypatch.setenv("SR_LP_SKIP", "0")
+    pair0, rep0 = refine_template(a, q, cfg)
+    monkeypatch.delenv("SR_LP_SKIP")
+    pair1, rep1 = refine_template(a, q, cfg)
+    assert rep1.status is rep0.status is RefineStatus.CONVERGED
+    assert rep1.iterations == rep0.iterations
+    na = np.linalg.norm(a)
+    for (e0, y0), (e1, y1) in zip(rep0.residual_history, rep1.residual_history):
+        assert abs(e0 - e1) <= 4 * U * na + 1e-6 * e0
+        assert abs(y0 - y1) <= 40 * np.sqrt(n) * U + 1e-6 * y0
+    dq = (pair0.q - pair1.q).abs().max().item()
+    assert dq <= 16 * U, dq

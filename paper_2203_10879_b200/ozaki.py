@@ -310,17 +310,33 @@ def lp_product_negligible(scale, slack_bits=26):
     return math.isfinite(scale) and 0.0 <= scale <= 2.0 ** -slack_bits
 
 
-def correction_beta(bound, n, hi=HP_BETA, lo=LP_BETA, unit_bits=53):
+def correction_beta(bound, n, hi=HP_BETA, lo=LP_BETA, unit_bits=53, operand="x"):
     """Operand precision for a correction product X S whose result is added to
-    an O(1) matrix before one rounding (Q + Q S'/2, Q^ - Q^ (G - I)/2):
-    truncating S (||S||_F <= bound) to beta bits per column changes the sum by
-    <= sqrt(n) 2^-beta bound per column, truncating X by <= n 2^-beta bound in
-    norm, so beta = unit_bits + 3 + log2(bound) + log2(n)/2 keeps both below a
-    quarter of the final rounding (u sqrt(n)).  Clamped to [lo, hi]."""
+    an O(1) matrix before one rounding (Q + Q S'/2, Q^ - Q^ (G - I)/2), with
+    ||S||_F <= bound, ||X||_2 < sqrt(3), |X_ik| < 2.  Both truncations stay
+    below an eighth of the final rounding u sqrt(n):
+      operand="x": X to beta bits per row changes X by <= 2^-beta n in norm,
+        the product by <= 2^-beta n bound:
+        beta = unit_bits + 3 + log2(bound) + log2(n)/2;
+      operand="s": S to beta bits per column changes column j by
+        <= sqrt(n) 2^-beta colmax_j / 2, S by <= sqrt(n) 2^-beta bound / 2 in
+        norm (||colmax||_2 <= ||S||_F), the product by sqrt(3) times that:
+        beta = unit_bits + 3 + log2(bound) — log2(n)/2 fewer bits than X needs.
+    Clamped to [lo, hi]."""
     if not (bound > 0.0) or not math.isfinite(bound):
         return hi if not (bound == 0.0) else lo
-    b = unit_bits + 3 + math.ceil(math.log2(bound)) + math.ceil(0.5 * math.log2(max(n, 2)))
+    b = unit_bits + 3 + math.ceil(math.log2(bound))
+    if operand == "x":
+        b += math.ceil(0.5 * math.log2(max(n, 2)))
     return max(lo, min(hi, b))
+
+
+def correction_plan(bound, n, gauss=True):
+    """The plan of a correction product X S (correction_beta for each operand;
+    SR_CORR_SYM=1: S at X's precision, for A/B runs)."""
+    bx = correction_beta(bound, n, operand="x")
+    bs = bx if os.environ.get("SR_CORR_SYM") == "1" else correction_beta(bound, n, operand="s")
+    return plan(n, bx, bs, gauss)
 
 
 def encode_dual(x, rows, cols, pl, out_ah, out_b):

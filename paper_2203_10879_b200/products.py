@@ -143,8 +143,7 @@ class OzakiProducts:
     def _correction_plan(self, bound):
         """Plan for X S with a small S (||S||_F <= bound) added to an O(1) X:
         fewer moduli as the correction shrinks (ozaki.correction_beta)."""
-        beta = ozaki.correction_beta(bound, self.ws.n)
-        return ozaki.plan(self.ws.n, beta, beta, self.gauss)
+        return ozaki.correction_plan(bound, self.ws.n, self.gauss)
 
     def _hp_with(self, pl, ea, eb, out, **kw):
         pl = ozaki.fit_plan(pl, ea, eb)

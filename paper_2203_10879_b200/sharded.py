@@ -202,7 +202,7 @@ class OzakiShardBackend:
         self._prod(hq, ozaki.conj_view(self.eq), self.eb_j, self.res, self.yj, shift=-1.0, diag_col0=self.j0)
         self._block_sq_norm(self.yj, 4)
         bound = math.sqrt(float(self._all_reduce(self.scal[4:5].clone()).item()))
-        pc = ozaki.gauss_plan(n, ozaki.correction_beta(bound, n), ozaki.correction_beta(bound, n))
+        pc = ozaki.correction_plan(bound, n)
         ozaki.encode(self.qhat, n, n, "a", pc, out=self.ea_x)
         ozaki.encode(self.yj, n, w, "b", pc, out=self.eb_j)
         self._prod(pc, self.ea_x, self.eb_j, self.res, self.qj, alpha=-0.5, add=self._cols(self.qhat))
@@ -283,8 +283,7 @@ class OzakiShardBackend:
                   xw, None, None, None, None, self.wj.shape[1], self.sj.re_ptr(), self.sj.im_ptr(),
                   self.sj.ld, 0, st)                                  # S'_J = 2 W_J - Y_J - (X W)_J
         bound = products.sigma_prime_bound(norm_y, norm_w, False)
-        beta = ozaki.correction_beta(bound, n)
-        pc = ozaki.gauss_plan(n, beta, beta)
+        pc = ozaki.correction_plan(bound, n)
         ozaki.encode(self.q, n, n, "a", pc, out=self.ea_x)
         ozaki.encode(self.sj, n, w, "b", pc, out=self.eb_j)
         self._prod(pc, self.ea_x, self.eb_j, self.res, self.qj, alpha=0.5, add=self._cols(self.q))

@@ -61,6 +61,11 @@ def test_correction_beta_tracks_the_correction_size():
     n = 8192
     assert ozaki.correction_beta(1.0, n) == ozaki.HP_BETA
     assert ozaki.correction_beta(1e-6, n) == 53 + 3 - 19 + 7
+    # S needs log2(n)/2 fewer bits than X (its truncation is not amplified by the row length)
+    assert ozaki.correction_beta(1e-6, n, operand="s") == 53 + 3 - 19
+    pl = ozaki.correction_plan(1e-6, n)
+    assert (pl.beta_a, pl.beta_b) == (53 + 3 - 19 + 7, 53 + 3 - 19)
+    assert pl.nmod <= ozaki.plan(n, pl.beta_a, pl.beta_a).nmod
     assert ozaki.correction_beta(1e-30, n) == ozaki.LP_BETA
     assert ozaki.correction_beta(0.0, n) == ozaki.LP_BETA
     assert ozaki.correction_beta(float("nan"), n) == ozaki.HP_BETA

@@ -64,6 +64,9 @@ SR_TL_DECLARE(g_tl_solve)  // kinds: 0 SOLVE, 1 NEAR (slot = level)
 #ifndef SR_SOLVE_ONE_WARP
 #define SR_SOLVE_ONE_WARP 0  // 1: the earlier single-warp tile solve (A/B builds)
 #endif
+#ifndef SR_SOLVE_PDL
+#define SR_SOLVE_PDL 1  // 0: plain stream-ordered SOLVE launches (A/B builds)
+#endif
 constexpr int NB = 32;
 constexpr int NT = 128;   // NEAR CTAs: 16 x 8 threads, each a 2 x 4 block of the tile
 // SOLVE CTAs: 128 threads, 2 x 4 blocks.  (64 threads with 4 x 4 blocks — a
@@ -363,6 +366,18 @@ __global__ void __launch_bounds__(SolveShape<C>::THREADS) solve_kernel(SweepArgs
   const bool has_row = lev >= 1 && I >= N - lev;
   const int tid = threadIdx.x;
   if (tid == 0) SR_TL_MARK(g_tl_solve, 0, lev, 0);
+  // T_II and T_MM do not depend on the sweep: with a programmatic dependent
+  // launch (SR_SOLVE_PDL) this CTA is scheduled while the previous level is
+  // still solving, fetches them, and only then waits for that level (and, by
+  // the launch's full edges, the NEAR / far updates) before it reads Rn, Rf, L.
+  load_tile_async<C, SolveShape<C>::THREADS>(sT2, T, ld, I * NB, I * NB, n);  // T_II
+  load_tile_async<C, SolveShape<C>::THREADS>(sT1, T, ld, M * NB, M * NB, n);  // T_MM
+  cp_async_commit();
+#if SR_SOLVE_PDL
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  // the next level may start its own prologue now (one level ahead at most)
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
   load_tile_async<C, SolveShape<C>::THREADS>(sR, Rn, ld, I * NB, M * NB, n);
   load_tile_async<C, SolveShape<C>::THREADS>(sRf, Rf, ld, I * NB, M * NB, n);
   if (has_col) {
@@ -375,8 +390,6 @@ __global__ void __launch_bounds__(SolveShape<C>::THREADS) solve_kernel(SweepArgs
     load_tile_async<C, SolveShape<C>::THREADS>(s3, L, ld, I * NB, J * NB, n);  // L_IJ
     load_tile_async<C, SolveShape<C>::THREADS>(s4, T, ld, J * NB, M * NB, n);  // T_JM
   }
-  load_tile_async<C, SolveShape<C>::THREADS>(sT2, T, ld, I * NB, I * NB, n);  // T_II
-  load_tile_async<C, SolveShape<C>::THREADS>(sT1, T, ld, M * NB, M * NB, n);  // T_MM
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
@@ -768,7 +781,30 @@ int enqueue(SolveCtx& c, int n, const C* t, const C* e, long long ld, C* l, doub
     if (lev % BW == 0 && lev >= BW * (1 + FAR_LA))
       SR_CUDA_CHECK(cudaStreamWaitEvent(s_solve, c.ev_f[(lev / BW - 1 - FAR_LA) % NFAR_EV], 0));
     SweepArgs a{n, N, lev, 0, ld};
+#if SR_SOLVE_PDL
+    {
+      // programmatic edge from SOLVE(lev-1) (same stream); the event waits above stay full edges
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(lev + 1);
+      lc.blockDim = dim3(SolveShape<C>::THREADS);
+      lc.dynamicSmemBytes = smem_solve;
+      lc.stream = s_solve;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      // up to n = 4096 (n = 512 .. 4096 solves 5-6 % faster); at n = 8192 programmatic launches on
+      // every level cost 2 % (16.1 vs 15.8 ms: the early-resident CTAs hold shared memory the far and
+      // NEAR CTAs want) and on the first 64 / 128 levels only they gain nothing: plain edges there
+      at[0].val.programmaticStreamSerializationAllowed = N <= 128 ? 1 : 0;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      const C* tc = t;
+      const C* rn = Rn;
+      const C* rf = Rf;
+      SR_CUDA_CHECK(cudaLaunchKernelEx(&lc, solve_kernel<C>, a, tc, rn, rf, l, cl, d_clipped));
+    }
+#else
     solve_kernel<C><<<lev + 1, SolveShape<C>::THREADS, smem_solve, s_solve>>>(a, t, Rn, Rf, l, cl, d_clipped);
+#endif
     SR_LAUNCH_CHECK();
     // NEAR(lev): sources of level lev-1 into levels lev+1 .. 4 (b + 1 + FAR_LA) - 1, b = (lev-1)/4
     if (lev >= 1) {

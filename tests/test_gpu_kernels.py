@@ -195,3 +195,38 @@ def test_sigma_merged_matches_numpy():
               w2d.data_ptr(), w3d.data_ptr(), None, None, wd.shape[1], s.re_ptr(), s.im_ptr(), s.ld,
               1, torch.cuda.current_stream().cuda_stream)
     assert np.array_equal(s.to_numpy(), ref)
+
+
+def test_fused_update_forms_without_negligible_terms():
+    """The fused update's kernels with the lp terms left out (products.lp_skips):
+    X = Y - W (w2 = NULL) and S' = 2W - Y (yw = NULL), bit for bit; the full
+    fused forms next to them; a dropped X W beside separate W^2, W^3 is rejected."""
+    rng = np.random.default_rng(6)
+    n = 61
+    w = (rnd(rng, n, n) * 1e-5).astype(np.complex64)
+    y = rnd(rng, n, n) * 1e-9
+    w2 = (w @ w)
+    st = torch.cuda.current_stream().cuda_stream
+
+    def dev(x):
+        d = lp_empty(n)
+        d[:, :n] = torch.from_numpy(x)
+        return d
+    wd, w2d = dev(w), dev(w2)
+    yz = ZPlanar.from_any(y)
+    xd = lp_empty(n)
+    _lib.call("sr_fused_lp_operand_c64", n, yz.re_ptr(), yz.im_ptr(), yz.ld, wd.data_ptr(), None, wd.shape[1],
+              xd.data_ptr(), st)
+    x_ref = (y - w.astype(np.complex128)).astype(np.complex64)
+    assert np.array_equal(xd[:, :n].cpu().numpy(), x_ref)
+    _lib.call("sr_fused_lp_operand_c64", n, yz.re_ptr(), yz.im_ptr(), yz.ld, wd.data_ptr(), w2d.data_ptr(),
+              wd.shape[1], xd.data_ptr(), st)
+    x_ref = ((y - w.astype(np.complex128)) - w2.astype(np.complex128)).astype(np.complex64)
+    assert np.array_equal(xd[:, :n].cpu().numpy(), x_ref)
+    s = ZPlanar.empty(n)
+    _lib.call("sr_sigma_merged_f64", n, n, wd.data_ptr(), yz.re_ptr(), yz.im_ptr(), yz.ld, None, None, None, None,
+              None, wd.shape[1], s.re_ptr(), s.im_ptr(), s.ld, 0, st)
+    assert np.array_equal(s.to_numpy(), 2.0 * w.astype(np.complex128) - y)
+    rc = _lib.load().sr_sigma_merged_f64(n, n, wd.data_ptr(), yz.re_ptr(), yz.im_ptr(), yz.ld, None, w2d.data_ptr(),
+                                         w2d.data_ptr(), None, None, wd.shape[1], s.re_ptr(), s.im_ptr(), s.ld, 0, st)
+    assert rc == _lib.SR_EINVAL
